@@ -1,0 +1,19 @@
+"""Seeded synthetic conic-program generators (input data only, no method arithmetic).
+
+Shared by the CPU oracle (tests, cpu baseline) and the CUDA path (tests, bench).
+"""
+from .program import (ConicProgram, ZERO, NONNEG, SOC, RSOC, EXP, DUAL_EXP,
+                      KIND_NAMES, csr_from_coo)
+from .generators import gen_lasso, gen_fisher, gen_mpo, gen_mixed, bernoulli_positions
+
+# BASELINE.json configs (index -> builder).  configs[0] is the oracle-sized case.
+CONFIGS = {
+    "tiny_lasso": lambda seed=0: gen_lasso(100, 50, 1.0, seed=seed, dense=True),
+    "lasso": lambda seed=0: gen_lasso(1_000_000, 10_000, 0.01, seed=seed),
+    "fisher": lambda seed=0: gen_fisher(10_000, 1_000, 0.2, seed=seed),
+    "mpo": lambda seed=0: gen_mpo(100, 1000, seed=seed),
+}
+
+__all__ = ["ConicProgram", "ZERO", "NONNEG", "SOC", "RSOC", "EXP", "DUAL_EXP",
+           "KIND_NAMES", "csr_from_coo", "gen_lasso", "gen_fisher", "gen_mpo",
+           "gen_mixed", "bernoulli_positions", "CONFIGS"]

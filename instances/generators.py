@@ -1,0 +1,471 @@
+"""Seeded synthetic instance generators (shared by the oracle and the CUDA path).
+
+This module builds INPUT DATA ONLY: it contains none of the method's
+arithmetic (no projections, no PDHG, no scaling).  Every random number comes
+from ``numpy.random.Generator(Philox(seed))``.  Recipes:
+
+* Lasso SOCP   — PAPER.md:1625-1664 (App. B.2); rotated-SOC reading A22.
+* Fisher market — PAPER.md:1577-1623 (App. B.1, Eq. pro:fisher_cp).
+* MPO SOCP     — PAPER.md:1668-1706 (App. B.3, Eq. pro:MPO_SOCP); synthetic
+                 covariance per SURVEY §8(c) A24.
+* Mixed planted — SURVEY §8(d) cfg 5: all cone kinds with a planted KKT pair
+                 (x*, y*) so that c^T x* is the exact optimum.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .program import (ConicProgram, csr_from_coo, ZERO, NONNEG, SOC, RSOC, EXP,
+                      DUAL_EXP)
+
+INF = np.inf
+
+
+def _rng(seed: int) -> np.random.Generator:
+    return np.random.Generator(np.random.Philox(seed))
+
+
+def bernoulli_positions(rng: np.random.Generator, total: int, p: float) -> np.ndarray:
+    """Sorted positions in [0, total) of an i.i.d. Bernoulli(p) mask.
+
+    Drawn with geometric gaps, so every position is independently selected with
+    probability p (row counts are exactly Binomial) and the result is sorted and
+    duplicate-free.
+    """
+    if p >= 1.0:
+        return np.arange(total, dtype=np.int64)
+    out = []
+    pos = -1
+    while True:
+        need = int((total - pos) * p * 1.02) + 1024
+        gaps = rng.geometric(p, size=need).astype(np.int64)
+        idx = pos + np.cumsum(gaps)
+        cut = np.searchsorted(idx, total)
+        out.append(idx[:cut])
+        if cut < need:
+            break
+        pos = int(idx[-1])
+    return np.concatenate(out) if out else np.zeros(0, np.int64)
+
+
+# --------------------------------------------------------------------------
+# Lasso as SOCP (variables ordered (x+, x-, w, r, y), A22)
+# --------------------------------------------------------------------------
+def gen_lasso(m: int, nfeat: int, density: float, seed: int = 0,
+              dense: bool = False) -> ConicProgram:
+    """min ||A x - b||^2 + lam ||x||_1 as the conic program of PAPER.md:1641-1659.
+
+    Variables x = (x+ [nfeat], x- [nfeat] | w, r, y [m]); n1 = 2 nfeat with
+    bounds [0, inf); one primal RSOC block (w, r, y): ||y||^2 <= 2 w r
+    (PAPER.md:1657 is exactly the rotated SOC, reading A22).  Rows: w = 1;
+    y - A x+ + A x- = -b (all Zero cones).  Data recipe PAPER.md:1663-1664:
+    A_ij ~ U[0,1] at the given density, x~ ~ N(0,1) with half zeroed,
+    b = A x~ + 1e-6, lam = ||A^T b||_inf.
+    """
+    rng = _rng(seed)
+    if dense:
+        arow = np.repeat(np.arange(m, dtype=np.int64), nfeat)
+        acol = np.tile(np.arange(nfeat, dtype=np.int64), m)
+    else:
+        pos = bernoulli_positions(rng, m * nfeat, density)
+        arow, acol = pos // nfeat, pos % nfeat
+        del pos
+    aval = rng.uniform(0.0, 1.0, size=arow.shape[0])
+    xt = rng.standard_normal(nfeat)
+    xt[rng.permutation(nfeat)[: nfeat // 2]] = 0.0
+    b = np.bincount(arow, weights=aval * xt[acol], minlength=m) + 1e-6
+    lam = float(np.max(np.abs(np.bincount(acol, weights=aval * b[arow], minlength=nfeat))))
+
+    n1 = 2 * nfeat
+    iw, ir, iy = n1, n1 + 1, n1 + 2
+    n = n1 + 2 + m
+    mrows = m + 1
+    k = np.bincount(arow, minlength=m).astype(np.int64)        # nnz per A row
+    row_ptr = np.zeros(mrows + 1, dtype=np.int64)
+    row_ptr[1] = 1
+    row_ptr[2:] = 1 + np.cumsum(2 * k + 1)
+    nnz = int(row_ptr[-1])
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    col[0], val[0] = iw, 1.0
+    astart = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(k, out=astart[1:])
+    within = np.arange(arow.shape[0], dtype=np.int64) - astart[arow]
+    base = row_ptr[1:-1][arow]                                  # start of K row arow+1
+    col[base + within] = acol
+    val[base + within] = -aval
+    col[base + k[arow] + within] = nfeat + acol
+    val[base + k[arow] + within] = aval
+    yslot = row_ptr[2:] - 1
+    col[yslot] = iy + np.arange(m)
+    val[yslot] = 1.0
+    h = np.empty(mrows)
+    h[0] = 1.0
+    h[1:] = -b
+    c = np.zeros(n)
+    c[:n1] = lam
+    c[ir] = 2.0
+    prog = ConicProgram(
+        m=mrows, n=n, n1=n1, row_ptr=row_ptr, col_idx=col, vals=val, c=c, h=h,
+        l=np.zeros(n1), u=np.full(n1, INF),
+        pk=np.array([RSOC], np.int32), pdim=np.array([m + 2], np.int64),
+        rk=np.array([ZERO], np.int32), rdim=np.array([mrows], np.int64),
+        name=f"lasso_{m}x{nfeat}_d{density:g}_s{seed}")
+    prog.lasso_A = (arow, acol, aval, m, nfeat)   # original data for ISTA pins
+    prog.lasso_b = b
+    prog.lasso_lam = lam
+    return prog
+
+
+# --------------------------------------------------------------------------
+# Fisher market (Eq. pro:fisher_cp)
+# --------------------------------------------------------------------------
+def gen_fisher(mbuy: int, ngood: int, density: float = 0.2, seed: int = 0) -> ConicProgram:
+    """Fisher market equilibrium as the exp-cone program of PAPER.md:1618.
+
+    Variables (X [mbuy*ngood] buyer-major as printed, (p_i, t_i) pairs),
+    X >= 0, p, t free (n1 = n, n2 = 0).  Rows: ngood supply equalities
+    sum_i X_ij = b_j; mbuy t-definitions U_i X_i - t_i = 0; mbuy row blocks
+    (p_i, 0, t_i) - (0, -1, 0) in K_exp.  U_ij ~ U[0,1] at
+    density 0.2, repaired so every row/column has a nonzero;
+    w_i ~ U[0,1]; b_j = 0.25.
+    """
+    rng = _rng(seed)
+    pos = bernoulli_positions(rng, mbuy * ngood, density)
+    urow, ucol = pos // ngood, pos % ngood
+    uval = rng.uniform(0.0, 1.0, size=pos.shape[0])
+    w = rng.uniform(0.0, 1.0, size=mbuy)
+    # repair empty rows / columns (one uniformly chosen entry each)
+    rowcnt = np.bincount(urow, minlength=mbuy)
+    add_r = np.nonzero(rowcnt == 0)[0]
+    colcnt = np.bincount(ucol, minlength=ngood)
+    add_c = np.nonzero(colcnt == 0)[0]
+    if add_r.size or add_c.size:
+        er = np.concatenate([add_r, rng.integers(0, mbuy, add_c.size)])
+        ec = np.concatenate([rng.integers(0, ngood, add_r.size), add_c])
+        ev = rng.uniform(0.0, 1.0, size=er.size)
+        key = np.concatenate([urow * ngood + ucol, er * ngood + ec])
+        allv = np.concatenate([uval, ev])
+        key, first = np.unique(key, return_index=True)
+        urow, ucol, uval = key // ngood, key % ngood, allv[first]
+    nX = mbuy * ngood
+    n = nX + 2 * mbuy
+    mrows = ngood + mbuy + 3 * mbuy
+    # supply rows j: all X[i, j] (cols i*ngood + j), value 1
+    sup_rows = np.repeat(np.arange(ngood, dtype=np.int64), mbuy)
+    sup_cols = (np.arange(mbuy, dtype=np.int64)[None, :] * ngood
+                + np.arange(ngood, dtype=np.int64)[:, None]).ravel()
+    sup_vals = np.ones(nX)
+    # t rows
+    t_rows = np.concatenate([ngood + urow, ngood + np.arange(mbuy)])
+    t_cols = np.concatenate([urow * ngood + ucol, nX + 2 * np.arange(mbuy) + 1])
+    t_vals = np.concatenate([uval, -np.ones(mbuy)])
+    # exp rows: (p_i, -, t_i)
+    base = ngood + mbuy + 3 * np.arange(mbuy, dtype=np.int64)
+    e_rows = np.concatenate([base, base + 2])
+    e_cols = np.concatenate([nX + 2 * np.arange(mbuy), nX + 2 * np.arange(mbuy) + 1])
+    e_vals = np.ones(2 * mbuy)
+    row_ptr, col, val = csr_from_coo(
+        mrows, n, np.concatenate([sup_rows, t_rows, e_rows]),
+        np.concatenate([sup_cols, t_cols, e_cols]),
+        np.concatenate([sup_vals, t_vals, e_vals]))
+    h = np.zeros(mrows)
+    h[:ngood] = 0.25
+    h[base + 1] = -1.0
+    c = np.zeros(n)
+    c[nX + 2 * np.arange(mbuy)] = -w
+    l = np.full(n, -INF)
+    l[:nX] = 0.0
+    rk = np.array([ZERO] + [EXP] * mbuy, np.int32)
+    rdim = np.array([ngood + mbuy] + [3] * mbuy, np.int64)
+    prog = ConicProgram(
+        m=mrows, n=n, n1=n, row_ptr=row_ptr, col_idx=col, vals=val, c=c, h=h,
+        l=l, u=np.full(n, INF), pk=np.zeros(0, np.int32), pdim=np.zeros(0, np.int64),
+        rk=rk, rdim=rdim, name=f"fisher_{mbuy}x{ngood}_s{seed}")
+    prog.fisher = (urow, ucol, uval, w, mbuy, ngood)
+    return prog
+
+
+# --------------------------------------------------------------------------
+# Multi-period portfolio optimisation (Eq. pro:MPO_SOCP)
+# --------------------------------------------------------------------------
+def gen_mpo(T: int, nasset: int, seed: int = 0, gamma2: float = 0.05,
+            gamma3: float = 0.05, nfactor: int = 5) -> ConicProgram:
+    """Constraint-form MPO SOCP of PAPER.md:1694-1705 with synthetic data.
+
+    Per period tau (w = w_{tau+1} in R^{n+1}, u = u_tau in R^n):
+      budget  1^T (w - w_tau) = 0                       (Zero; w_0 = w_{1/n})
+      market  (w^m)^T Sigma w_[n] = 0                   (Zero)
+      |.|     u_i - (w_i - wb_i) >= 0, u_i + (w_i - wb_i) >= 0   (NonNeg)
+      u-sum   gamma3 - sum_i Sigma^{1/2}_ii u_i >= 0     (NonNeg)
+      risk    (gamma1, Sigma^{1/2}(w - wb)_[n]) in SOC(n+1)
+      trade   gamma2 +- (w - w_tau)_i >= 0  for i in [n+1] (NonNeg)
+    w >= 0 as bounds, u free.  Synthetic data per SURVEY A24: Sigma = F F^T +
+    diag(U[1e-4,4e-4]), F ~ N(0, 0.01^2) (n x 5), perturbed per period;
+    r^ ~ U[-0.01, 0.03]; w_b = all cash; gamma1 = ||Sigma^{1/2}(w_{1/n} - wb)||.
+    The market portfolio w^m is chosen with (w^m)^T Sigma w_{1/n} = 0.
+    """
+    rng = _rng(seed)
+    n = nasset
+    nw = n + 1
+    nvar_per = nw + n
+    nv = T * nvar_per
+    w0 = np.full(nw, 1.0 / nw)          # w_{1/n} incl. cash
+    wb = np.zeros(nw)
+    wb[n] = 1.0                          # all-cash benchmark (A24)
+    F0 = rng.normal(0.0, 0.01, size=(n, nfactor))
+    D0 = rng.uniform(1e-4, 4e-4, size=n)
+    rows, cols, vals = [], [], []
+    h_parts, rk_list, rdim_list = [], [], []
+    row = 0
+    c = np.zeros(nv)
+
+    def add(rr, cc, vv):
+        rows.append(np.asarray(rr, np.int64))
+        cols.append(np.asarray(cc, np.int64))
+        vals.append(np.asarray(vv, np.float64))
+
+    for tau in range(T):
+        F = F0 * (1.0 + 0.05 * rng.standard_normal(F0.shape))
+        Dg = D0 * (1.0 + 0.05 * rng.uniform(-1.0, 1.0, size=n))
+        Sigma = F @ F.T + np.diag(Dg)
+        evals, evecs = np.linalg.eigh(Sigma)
+        S12 = (evecs * np.sqrt(np.maximum(evals, 0.0))) @ evecs.T
+        rhat = rng.uniform(-0.01, 0.03, size=nw)
+        rhat[n] = 0.0
+        gamma1 = float(np.linalg.norm(S12 @ (w0 - wb)[:n]))
+        # market portfolio orthogonal (in Sigma) to w_{1/n}
+        g = rng.uniform(0.0, 1.0, size=n)
+        s0 = Sigma @ w0[:n]
+        wm = g - (g @ s0) / (s0 @ s0) * s0
+        iw = tau * nvar_per            # w_{tau+1} block
+        iu = iw + nw                   # u_tau block
+        c[iw:iw + nw] = -rhat          # max r^T w -> min -r^T w
+        # --- equality rows (Zero block of 2 rows)
+        # budget: 1^T w_{tau+1} - 1^T w_tau = 0
+        if tau == 0:
+            add(np.full(nw, row), iw + np.arange(nw), np.ones(nw))
+            h_parts.append([1.0])
+        else:
+            ip = iw - nvar_per
+            add(np.full(2 * nw, row), np.concatenate([ip + np.arange(nw), iw + np.arange(nw)]),
+                np.concatenate([-np.ones(nw), np.ones(nw)]))
+            h_parts.append([0.0])
+        row += 1
+        mrow = Sigma @ wm
+        add(np.full(n, row), iw + np.arange(n), mrow)
+        h_parts.append([0.0])
+        row += 1
+        rk_list.append(ZERO)
+        rdim_list.append(2)
+        # --- NonNeg block: 2n abs rows + 1 usum row + 2(n+1) trade rows
+        r0 = row
+        ar = r0 + np.arange(n)
+        add(np.concatenate([ar, ar]), np.concatenate([iu + np.arange(n), iw + np.arange(n)]),
+            np.concatenate([np.ones(n), -np.ones(n)]))
+        h_parts.append(-wb[:n])            # u - w + wb >= 0  ->  G x - h, h = -wb
+        ar2 = r0 + n + np.arange(n)
+        add(np.concatenate([ar2, ar2]), np.concatenate([iu + np.arange(n), iw + np.arange(n)]),
+            np.concatenate([np.ones(n), np.ones(n)]))
+        h_parts.append(wb[:n])             # u + w - wb >= 0
+        ru = r0 + 2 * n
+        add(np.full(n, ru), iu + np.arange(n), -np.diag(S12).copy())
+        h_parts.append([-gamma3])          # -sum diag u + gamma3 >= 0
+        rt = ru + 1 + np.arange(nw)
+        if tau == 0:
+            add(rt, iw + np.arange(nw), np.ones(nw))
+            h_parts.append(w0 - gamma2)    # w - w0 + g2 >= 0
+            rt2 = rt + nw
+            add(rt2, iw + np.arange(nw), -np.ones(nw))
+            h_parts.append(-w0 - gamma2)   # -(w - w0) + g2 >= 0
+        else:
+            ip = iw - nvar_per
+            add(np.concatenate([rt, rt]), np.concatenate([iw + np.arange(nw), ip + np.arange(nw)]),
+                np.concatenate([np.ones(nw), -np.ones(nw)]))
+            h_parts.append(np.full(nw, -gamma2))
+            rt2 = rt + nw
+            add(np.concatenate([rt2, rt2]), np.concatenate([iw + np.arange(nw), ip + np.arange(nw)]),
+                np.concatenate([-np.ones(nw), np.ones(nw)]))
+            h_parts.append(np.full(nw, -gamma2))
+        nn = 2 * n + 1 + 2 * nw
+        row = r0 + nn
+        rk_list.append(NONNEG)
+        rdim_list.append(nn)
+        # --- SOC block (gamma1, S12 (w - wb)_[n])
+        rs = row
+        h_parts.append([-gamma1])          # head row: 0*x - (-gamma1)
+        rr = rs + 1 + np.repeat(np.arange(n), n)
+        cc = iw + np.tile(np.arange(n), n)
+        add(rr, cc, S12.ravel())
+        h_parts.append(S12 @ wb[:n])
+        rk_list.append(SOC)
+        rdim_list.append(n + 1)
+        row = rs + n + 1
+    mrows = row
+    row_ptr, col, val = csr_from_coo(mrows, nv, np.concatenate(rows),
+                                     np.concatenate(cols), np.concatenate(vals))
+    h = np.concatenate([np.atleast_1d(np.asarray(p, np.float64)) for p in h_parts])
+    assert h.shape[0] == mrows
+    # bounds: w >= 0, u free; all variables are box variables (n2 = 0)
+    l = np.full(nv, -INF)
+    for tau in range(T):
+        l[tau * nvar_per: tau * nvar_per + nw] = 0.0
+    prog = ConicProgram(
+        m=mrows, n=nv, n1=nv, row_ptr=row_ptr, col_idx=col, vals=val, c=c, h=h,
+        l=l, u=np.full(nv, INF), pk=np.zeros(0, np.int32), pdim=np.zeros(0, np.int64),
+        rk=np.array(rk_list, np.int32), rdim=np.array(rdim_list, np.int64),
+        name=f"mpo_T{T}_n{n}_s{seed}")
+    return prog
+
+
+# --------------------------------------------------------------------------
+# Mixed-cone planted instance (SURVEY §8(d) cfg 5)
+# --------------------------------------------------------------------------
+def _cone_pair(rng, kind: int, d: int):
+    """A complementary pair (s in K, y in K^*, <s, y> = 0) for one block."""
+    if kind == ZERO:
+        return np.zeros(d), rng.standard_normal(d)
+    if kind == NONNEG:
+        s = rng.uniform(0.0, 1.0, d)
+        y = rng.uniform(0.0, 1.0, d)
+        pick = rng.uniform(size=d) < 0.5
+        s[pick] = 0.0
+        y[~pick] = 0.0
+        return s, y
+    if kind in (SOC, RSOC):
+        v = rng.standard_normal(d - 1)
+        nv = np.linalg.norm(v)
+        a, b = rng.uniform(0.0, 1.0, 2)
+        mode = rng.integers(0, 3)
+        if mode == 1:
+            a = 0.0
+        elif mode == 2:
+            b = 0.0
+        s = a * np.concatenate([[nv], v])
+        y = b * np.concatenate([[nv], -v])
+        if kind == RSOC:   # R = [[1,1],[1,-1]]/sqrt2 maps SOC <-> RSOC, R = R^T = R^-1
+            for z in (s, y):
+                t0, t1 = z[0], z[1]
+                z[0], z[1] = (t0 + t1) / math.sqrt(2.0), (t0 - t1) / math.sqrt(2.0)
+        return s, y
+    if kind in (EXP, DUAL_EXP):
+        rho = rng.uniform(-2.0, 2.0)
+        a, b = rng.uniform(0.1, 1.0, 2)
+        mode = rng.integers(0, 4)
+        if mode == 1:
+            a = 0.0
+        elif mode == 2:
+            b = 0.0
+        pe = a * np.array([rho, 1.0, math.exp(rho)])            # in K_exp
+        de = b * np.array([-1.0, rho - 1.0, math.exp(-rho)])    # in K_exp^*
+        return (pe, de) if kind == EXP else (de, pe)
+    raise ValueError(kind)
+
+
+def _draw_blocks(rng, total: int, mix, soc_dims=(3, 24)):
+    kinds, dims = [], []
+    rem = total
+    names = [k for k, _ in mix]
+    probs = np.array([f for _, f in mix], np.float64)
+    probs = probs / probs.sum()
+    while rem > 0:
+        k = int(rng.choice(names, p=probs))
+        if k in (EXP, DUAL_EXP):
+            d = 3
+        elif k in (SOC, RSOC):
+            d = int(rng.integers(soc_dims[0], soc_dims[1] + 1))
+        else:
+            d = int(rng.integers(1, 8))
+        if d > rem:
+            k, d = NONNEG, rem
+        kinds.append(k)
+        dims.append(d)
+        rem -= d
+    return np.array(kinds, np.int32), np.array(dims, np.int64)
+
+
+def gen_mixed(m: int, n1: int, n2: int, seed: int = 0, row_len=(3, 12),
+              soc_dims=(3, 24), scale_spread: float = 1.0,
+              row_mix=None, col_mix=None) -> ConicProgram:
+    """Mixed-cone instance with a planted KKT pair (SURVEY §8(d) cfg 5).
+
+    G has rows of U{row_len} distinct uniform columns with values
+    N(0,1) * 10^{U[-s,s]} * rowfactor * colfactor (s = scale_spread) so that
+    rescaling matters.  Row cones / primal cones mix all six kinds.  The pair
+    (x*, y*) with h = G x* - s*, c = G^T y* + lam* satisfies Eq. 1-2's KKT
+    conditions exactly, so c^T x* is the optimal value.
+    """
+    rng = _rng(seed)
+    n = n1 + n2
+    row_mix = row_mix or [(ZERO, .30), (NONNEG, .30), (SOC, .25), (RSOC, .05),
+                          (EXP, .075), (DUAL_EXP, .025)]
+    col_mix = col_mix or [(ZERO, .01), (NONNEG, .20), (SOC, .40), (RSOC, .15),
+                          (EXP, .20), (DUAL_EXP, .04)]
+    rk, rdim = _draw_blocks(rng, m, row_mix, soc_dims)
+    pk, pdim = _draw_blocks(rng, n2, col_mix, soc_dims) if n2 > 0 else (
+        np.zeros(0, np.int32), np.zeros(0, np.int64))
+    lens = rng.integers(row_len[0], row_len[1] + 1, size=m)
+    lens = np.minimum(lens, n)
+    rows = np.repeat(np.arange(m, dtype=np.int64), lens)
+    cols = np.concatenate([rng.choice(n, size=L, replace=False) for L in lens]).astype(np.int64)
+    rf = 10.0 ** rng.uniform(-scale_spread, scale_spread, size=m)
+    cf = 10.0 ** rng.uniform(-scale_spread, scale_spread, size=n)
+    vals = rng.standard_normal(rows.shape[0]) * rf[rows] * cf[cols]
+    row_ptr, col, val = csr_from_coo(m, n, rows, cols, vals)
+    # box part
+    btype = rng.integers(0, 4, size=n1)   # 0 free, 1 [l,inf), 2 (-inf,u], 3 [l,u]
+    lo = rng.uniform(-1.0, 0.0, n1)
+    hi = rng.uniform(0.0, 1.0, n1) + lo + 0.5
+    l = np.where((btype == 1) | (btype == 3), lo, -INF)
+    u = np.where((btype == 2) | (btype == 3), hi, INF)
+    x1 = np.empty(n1)
+    lam1 = np.zeros(n1)
+    status = rng.integers(0, 3, size=n1)  # 0 interior, 1 at lower, 2 at upper
+    for i in range(n1):
+        if status[i] == 1 and np.isfinite(l[i]):
+            x1[i] = l[i]
+            lam1[i] = rng.uniform(0.0, 1.0)
+        elif status[i] == 2 and np.isfinite(u[i]):
+            x1[i] = u[i]
+            lam1[i] = -rng.uniform(0.0, 1.0)
+        else:
+            fl, fu = np.isfinite(l[i]), np.isfinite(u[i])
+            if fl and fu:
+                x1[i] = rng.uniform(l[i], u[i])
+            elif fl:
+                x1[i] = l[i] + rng.uniform(0.0, 1.0)
+            elif fu:
+                x1[i] = u[i] - rng.uniform(0.0, 1.0)
+            else:
+                x1[i] = rng.standard_normal()
+    x2, lam2 = [], []
+    for k, d in zip(pk, pdim):
+        xb, lb = _cone_pair(rng, int(k), int(d))
+        x2.append(xb)
+        lam2.append(lb)
+    s_parts, y_parts = [], []
+    for k, d in zip(rk, rdim):
+        sb, yb = _cone_pair(rng, int(k), int(d))
+        s_parts.append(sb)
+        y_parts.append(yb)
+    x_star = np.concatenate([x1] + x2) if x2 else x1
+    y_star = np.concatenate(y_parts)
+    s_star = np.concatenate(s_parts)
+    lam = np.concatenate([lam1] + lam2) if lam2 else lam1
+    Gx = np.bincount(rows_of(row_ptr), weights=val * x_star[col], minlength=m)
+    GTy = np.bincount(col, weights=val * y_star[rows_of(row_ptr)], minlength=n)
+    h = Gx - s_star
+    c = GTy + lam
+    prog = ConicProgram(m=m, n=n, n1=n1, row_ptr=row_ptr, col_idx=col, vals=val,
+                        c=c, h=h, l=l, u=u, pk=pk, pdim=pdim, rk=rk, rdim=rdim,
+                        name=f"mixed_{m}x{n}_s{seed}")
+    prog.x_star, prog.y_star = x_star, y_star
+    prog.obj_star = float(c @ x_star)
+    return prog
+
+
+def rows_of(row_ptr: np.ndarray) -> np.ndarray:
+    m = row_ptr.shape[0] - 1
+    return np.repeat(np.arange(m, dtype=np.int64), np.diff(row_ptr))

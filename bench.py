@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""bench.py — PDCS hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference]
+
+A "step" is one accepted inner iteration of Alg. 1: the PDHG
+trial(s) with line search, the reflected-Halpern update, averaging, and the
+amortised Eq. 9 check / restart logic every check_interval iterations.  The
+workload is BASELINE.json configs[1]: Lasso SOCP, 1e6 samples x 1e4 features,
+A 1% dense (K: 1,000,001 x 1,020,002, nnz 2.01e8), seeded synthetic data.
+
+value          iterations/s over all ranks (device-timed with CUDA events on the
+               library's stream, inputs resident in HBM)
+e2e            iterations/s of the whole job through the C ABI with pinned HOST
+               buffers: pdcs_create (H2D upload, transpose) + pdcs_set_cones
+               (Ruiz/PC) + pdcs_iterate(K) + pdcs_get_iterate (D2H)
+roofline       dominant kernel: algorithmic bytes per launch / mean launch time
+cpu_baseline   the CPU oracle (single thread) on a bounded sample of the same job
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PDHG iters/sec & time-to-1e-4 rel KKT; SpMV HBM GB/s vs peak, 1-8 GPUs"
+FALLBACK_HBM = 6650.0
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_instance(config, seed):
+    from instances import CONFIGS
+    t = time.perf_counter()
+    prog = CONFIGS[config](seed)
+    return prog, time.perf_counter() - t
+
+
+def spmv_alg_bytes(prog):
+    """Algorithmic bytes of the two fused SpMV kernels per launch:
+    matrix (8 B value + 4 B column id per nnz) + row pointers (4 B per row) + the
+    gathered vector once + the row-indexed epilogue vectors."""
+    nnz, m, n = prog.nnz, prog.m, prog.n
+    k_dual = 12 * nnz + 4 * (m + 1) + 8 * n + 8 * 5 * m + m          # y, Kx, h~ in; Kx^, y^ out; kind byte
+    kt_halpern = 12 * nnz + 4 * (n + 1) + 8 * m + 8 * 9 * n          # x^, x, x0, KTy, KTy0, xsum in; x, KTy, xsum out
+    return {"spmv_K_dual": k_dual, "spmv_KT_halpern": kt_halpern}
+
+
+def iter_alg_bytes(prog):
+    """SURVEY §8(d) B_iter = [12 nnz + 4(m+1)] + [12 nnz + 4(n+1)] + 8*14*(m+n)."""
+    nnz, m, n = prog.nnz, prog.m, prog.n
+    return 12 * nnz + 4 * (m + 1) + 12 * nnz + 4 * (n + 1) + 8 * 14 * (m + n)
+
+
+def pinned(prog):
+    import torch
+    def pin(a, dt):
+        return torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
+    return dict(row_ptr=pin(prog.row_ptr, np.int64), col=pin(prog.col_idx, np.int32),
+                val=pin(prog.vals, np.float64), c=pin(prog.c, np.float64), h=pin(prog.h, np.float64),
+                l=pin(prog.l, np.float64), u=pin(prog.u, np.float64))
+
+
+def make_ctx(P, prog, host, params, stream, device):
+    ctx = P.pdcs_create(prog.m, prog.n, prog.n1, 0, prog.m, host["row_ptr"], host["col"], host["val"],
+                        host["c"], host["h"], host["l"], host["u"], params, device, stream)
+    P.pdcs_set_cones(ctx, prog.pk, prog.pdim, prog.rk, prog.rdim)
+    return ctx
+
+
+def cpu_baseline(prog, budget_s=20.0):
+    """Oracle (single-threaded C++, as it stands) on the same instance: timed
+    accepted iterations after one warm-up iteration; setup excluded."""
+    import oracle as O
+    t = time.perf_counter()
+    S = O.OracleSolver(prog)
+    setup = time.perf_counter() - t
+    S.iterate(1)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        S.iterate(1)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or done >= 200:
+            break
+    return {"value": done / el, "unit": "iter/s", "cores": 1, "kind": "oracle",
+            "sample": f"{done} accepted iterations of the full {prog.name} instance after 1 warm-up "
+                      f"(setup {setup:.1f}s excluded), single thread",
+            "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def run_reference(args):
+    rank, local, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            return
+    prog, gen_s = build_instance(args.config, args.seed)
+    import oracle as O
+    t = time.perf_counter()
+    S = O.OracleSolver(prog)
+    setup = time.perf_counter() - t
+    S.iterate(max(args.warmup, 0))
+    t0 = time.perf_counter()
+    S.iterate(args.steps)
+    el = time.perf_counter() - t0
+    v = args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(prog, args),
+            "cpu_baseline": {"value": v, "unit": "iter/s", "kind": "oracle", "cores": 1,
+                             "sample": f"{args.steps} timed accepted iterations of the full instance "
+                                       f"after {args.warmup} warm-up (setup {setup:.1f}s excluded)"},
+            "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _config(prog, args):
+    return {"workload": args.config, "instance": prog.name, "m": prog.m, "n": prog.n, "nnz": prog.nnz,
+            "cones": {"primal": [int(k) for k in np.unique(prog.pk)], "rows": [int(k) for k in np.unique(prog.rk)]},
+            "l2": "inputs larger than L2 (matrix %.2f GB > 126 MB)" % (24 * prog.nnz / 1e9),
+            "parallelism": f"dp{args.gpus}-replica" if args.gpus > 1 else "single-gpu"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--config", default="lasso")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tol-run", action="store_true")
+    ap.add_argument("--tol-time-limit", type=float, default=120.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    rank, local, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2505_00311_b200 import build
+    build.build()
+    import paper_2505_00311_b200 as P
+
+    prog, gen_s = build_instance(args.config, args.seed)
+    host = pinned(prog)
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    params = P.pdcs_default_params()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---------------- device-timed steps (inputs resident in HBM)
+    ctx = make_ctx(P, prog, host, params, sh, local)
+    P.pdcs_iterate(ctx, args.warmup)
+    P.pdcs_enable_timing(ctx, True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        res = P.pdcs_iterate(ctx, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = P.pdcs_launch_count(ctx)
+    ktimes = P.pdcs_kernel_times(ctx)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+    P.pdcs_destroy(ctx)
+
+    # ---------------- roofline of the dominant kernel
+    peak, peak_src = load_peaks()
+    algb = spmv_alg_bytes(prog)
+    spmv = {k: v for k, v in ktimes.items() if k in algb}
+    dom = max(spmv, key=lambda k: spmv[k][0]) if spmv else None
+    roof = None
+    if dom:
+        tot_ms, cnt = spmv[dom]
+        avg_s = tot_ms / cnt / 1e3
+        ach = algb[dom] / avg_s / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tf):
+            d = json.load(open(tf)).get(args.config, {})
+            traffic = d.get(dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": traffic, "alg_bytes_per_launch": algb[dom],
+                "avg_launch_ms": avg_s * 1e3, "launches": cnt, "peak_source": peak_src}
+    total_kernel_ms = sum(v[0] for v in ktimes.values())
+    iter_bytes = iter_alg_bytes(prog)
+
+    # ---------------- e2e through the C ABI with pinned host buffers
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    ctx = make_ctx(P, prog, host, params, sh, local)
+    P.pdcs_iterate(ctx, args.steps)
+    xo = torch.empty(prog.n, dtype=torch.float64).pin_memory()
+    yo = torch.empty(prog.m, dtype=torch.float64).pin_memory()
+    P.pdcs_get_iterate(ctx, P.CURRENT, P.ORIGINAL, xo, yo)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    P.pdcs_destroy(ctx)
+    h2d = sum(int(t.numel() * t.element_size()) for t in host.values())
+    d2h = (prog.n + prog.m) * 8
+    e2e = {"value": world * args.steps / e2e_s, "unit": "iter/s",
+           "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+           "seconds": e2e_s, "note": "create+set_cones (upload, transpose, Ruiz) + iterate(K) + D2H of (x, y)"}
+
+    # ---------------- time to 1e-4 relative KKT (Eq. 9), fresh context
+    tol_run = None
+    if not args.no_tol_run:
+        p4 = P.pdcs_default_params(tol=1e-4, time_limit_s=args.tol_time_limit)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx = make_ctx(P, prog, host, p4, sh, local)
+        torch.cuda.synchronize()
+        t_setup = time.perf_counter() - t0
+        r = P.pdcs_solve(ctx)
+        torch.cuda.synchronize()
+        t_all = time.perf_counter() - t0
+        P.pdcs_destroy(ctx)
+        tol_run = {"tol": 1e-4, "status": r.status, "seconds_incl_setup": t_all,
+                   "seconds_solve": r.solve_seconds, "setup_seconds": t_setup, "iters": r.iters,
+                   "kkt_max": max(r.kkt.err_p, r.kkt.err_d, r.kkt.err_gap), "restarts": r.restarts}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(prog)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded Philox, PAPER.md:1663 recipe at BASELINE configs[1] size)",
+                "config": _config(prog, args), "clocks": clk.summary(), "e2e": e2e,
+                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+                "time_to_1e-4": tol_run,
+                "iter_roofline": {"alg_bytes_per_iter": iter_bytes,
+                                  "achieved_GBs": iter_bytes / (ms_per_step / 1e3) / 1e9,
+                                  "frac": iter_bytes / (ms_per_step / 1e3) / 1e9 / peak},
+                "kernel_ms_per_step": {k: v[0] / args.steps for k, v in sorted(ktimes.items())},
+                "kernel_share": {k: v[0] / total_kernel_ms for k, v in sorted(ktimes.items())},
+                "final": {"iters": res.iters, "restarts": res.restarts, "trials": res.trials},
+                "instance_gen_s": gen_s}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,226 @@
+/*
+ * pdcs.h — C ABI of libpdcs.so, the B200-native (sm_100a, fp64) hot path of
+ * PDCS (arxiv 2505.00311): restarted, reflected-Halpern PDHG with adaptive
+ * steps, primal weights, Ruiz/Pock-Chambolle rescaling and projections onto
+ * diagonally rescaled cones.
+ *
+ * Problem (§2 Eq. 1):
+ *     min <c, x>  s.t.  G x - h in K_d^*,   l <= x_1 <= u,   x_2 in K_p
+ * with x = (x_1 in R^{n1}, x_2 in R^{n2}), G in R^{m x n} (CSR, fp64).
+ * Dual (Eq. 2-3):  y in K_d, lambda = c - G^T y.
+ *
+ * Conventions (every entry point):
+ *   - Plain pointers and sizes only; no framework types.
+ *   - Ownership: the caller owns every input array; the library deep-copies
+ *     at create/set time into device memory it allocates (cudaMalloc on the
+ *     context's device) and frees at pdcs_destroy.  Output arrays are
+ *     caller-allocated with the documented sizes.
+ *   - mem_kind says whether input pointers are host (PDCS_MEM_HOST) or device
+ *     (PDCS_MEM_DEVICE) memory.  Output pointers follow the same mem_kind.
+ *   - Errors: a pdcs_status code; the library never aborts.  The message of the
+ *     last failure on a context is returned by pdcs_last_error(ctx).  On error
+ *     the context stays valid unless documented otherwise.
+ *   - Call order: pdcs_create -> pdcs_set_cones -> (pdcs_iterate | pdcs_kkt |
+ *     pdcs_solve | pdcs_get_*)* -> pdcs_destroy.  Violations: PDCS_ERR_STATE.
+ *   - A context is single-owner and not thread-safe.  All work is enqueued on
+ *     the stream given at create (NULL = legacy default stream); functions
+ *     that return host data synchronise that stream.
+ *   - No CPU fallback: without a usable sm_100 device pdcs_create fails with
+ *     PDCS_ERR_CUDA.
+ */
+#ifndef PDCS_H_
+#define PDCS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pdcs_ctx pdcs_ctx;
+
+typedef enum {
+  PDCS_OK = 0,
+  PDCS_ERR_ARG = 1,       /* null pointer / bad enum / bad size */
+  PDCS_ERR_DIM = 2,       /* CSR shape inconsistent (row_ptr not monotone, col out of range) */
+  PDCS_ERR_BOUNDS = 3,    /* l_i > u_i, or NaN bound */
+  PDCS_ERR_NONFINITE = 4, /* non-finite matrix entry, c or h */
+  PDCS_ERR_CONE = 5,      /* bad cone kind/dim, dims do not sum to n2 / m */
+  PDCS_ERR_SHARD = 6,     /* a row cone straddles this rank's row range */
+  PDCS_ERR_CUDA = 7,      /* CUDA runtime error (incl. no sm_100 device) */
+  PDCS_ERR_NCCL = 8,      /* NCCL error */
+  PDCS_ERR_NUMERICAL = 9, /* eta underflow, > ls_max_rejects line-search rejects */
+  PDCS_ERR_STATE = 10     /* call order violated */
+} pdcs_status;
+
+/* Cone kinds.  In the primal list they are the blocks of K_p
+ * over x[n1:n].  In the row list they are the CONSTRAINT cones C_b of
+ * G x - h in C_b (the blocks of K_d^*), so the dual y_b lives in C_b^*:
+ * ZERO rows are equalities (y free), NONNEG rows are >= (y >= 0), EXP rows
+ * mean G x - h in K_exp (y in K_exp^*), DUAL_EXP rows G x - h in K_exp^*.
+ * RSOC is {(a,b,z): a,b >= 0, ||z||^2 <= 2ab}.
+ * Dims: SOC >= 2, RSOC >= 3, EXP = DUAL_EXP = 3, ZERO/NONNEG >= 1. */
+typedef enum {
+  PDCS_CONE_ZERO = 0,
+  PDCS_CONE_NONNEG = 1,
+  PDCS_CONE_SOC = 2,
+  PDCS_CONE_RSOC = 3,
+  PDCS_CONE_EXP = 4,
+  PDCS_CONE_DUAL_EXP = 5
+} pdcs_cone_kind;
+
+typedef enum { PDCS_MEM_HOST = 0, PDCS_MEM_DEVICE = 1 } pdcs_mem_kind;
+
+typedef enum {
+  PDCS_OPTIMAL = 0,
+  PDCS_ITERATION_LIMIT = 1,
+  PDCS_TIME_LIMIT = 2,
+  PDCS_NUMERICAL_ERROR = 3,
+  PDCS_RUNNING = 4
+} pdcs_solve_status;
+
+/* Iterate selectors for pdcs_get_iterate / pdcs_kkt. */
+typedef enum {
+  PDCS_CURRENT = 0,   /* z^{t,k}: the current (Halpern) iterate */
+  PDCS_PDHG_OUT = 1,  /* z^: the last accepted PDHG output (always feasible) */
+  PDCS_ANCHOR = 2,    /* z^{t,0}: restart anchor */
+  PDCS_BEST = 3,      /* best-ever evaluated candidate (returned by pdcs_solve) */
+  PDCS_CANDIDATE = 4  /* last restart candidate */
+} pdcs_which;
+
+typedef enum { PDCS_SCALED = 0, PDCS_ORIGINAL = 1 } pdcs_space;
+
+/* Solver parameters (defaults in brackets via
+ * pdcs_default_params).  Layout is part of the ABI. */
+typedef struct {
+  double tol;             /* [1e-6] Eq. 9 termination threshold */
+  int64_t max_iters;      /* [1e6] accepted inner iterations for pdcs_solve */
+  double time_limit_s;    /* [0 = none] */
+  int32_t ruiz_iters;     /* [10] Ruiz rounds */
+  int32_t pock_chambolle; /* [1] one Pock-Chambolle pass, alpha = 1 */
+  int32_t check_interval; /* [40] Eq. 9 / restart cadence */
+  int32_t vanilla_pdhg;   /* [0] 1: plain PDHG, tau = sigma = 0.9/||G||_2, no
+                             scaling/Halpern/restarts */
+  double eta0;            /* [0 = 1/||K~||_inf] initial step (vanilla: the fixed step) */
+  double omega0;          /* [0 = ||c~||_inf/||h~||_inf clipped to [1e-4,1e4]] */
+  double beta_max;        /* [1] reflection parameter cap */
+  int32_t refl_window;    /* [40] beta window (reading A9) */
+  int32_t pad0;
+  double restart_suff;    /* [0.2]  */
+  double restart_nec;     /* [0.8]  */
+  double restart_art;     /* [0.36] */
+  double ls_shrink;       /* [0.5]  */
+  double ls_grow;         /* [1.05] */
+  int32_t ls_max_rejects; /* [60]   */
+  int32_t verbose;        /* [0]    */
+} pdcs_params;
+
+/* Eq. 9 residuals on the ORIGINAL problem. */
+typedef struct {
+  double err_p, err_d, err_gap, pobj, dobj;
+} pdcs_kkt_t;
+
+typedef struct {
+  int32_t status;         /* pdcs_solve_status */
+  int32_t pad;
+  pdcs_kkt_t kkt;         /* residuals of the returned (best) point */
+  int64_t iters;          /* accepted inner iterations */
+  int64_t trials;         /* PDHG trials incl. line-search rejects */
+  int64_t restarts;
+  int64_t spmv_K, spmv_KT;
+  double eta, omega, beta;
+  double solve_seconds;
+} pdcs_result_t;
+
+/* Fill p with the defaults listed above. */
+void pdcs_default_params(pdcs_params *p);
+
+/* Create a context: validate and deep-copy the problem, build CSR(K) and
+ * CSR(K^T) on the device, and (unless vanilla) apply Ruiz + Pock-Chambolle
+ * rescaling on the device.
+ *   m_global        rows of G over all ranks
+ *   n, n1           columns of G; the first n1 are box variables
+ *   row_begin/end   this rank's rows [row_begin, row_end) (0, m_global unsharded)
+ *   row_ptr [rows+1] int64, 0-based local offsets; col_idx [nnz] int32 global
+ *                    columns, strictly increasing within a row; vals [nnz]
+ *   c [n], h [rows], l [n1], u [n1] (+-INFINITY allowed in l, u)
+ *   p               parameters (NULL: defaults)
+ *   device          CUDA device ordinal; cuda_stream a cudaStream_t or NULL
+ *   nccl_unique_id  128-byte ncclUniqueId when world > 1, else NULL
+ * Errors: ARG, DIM, BOUNDS, NONFINITE, CUDA, NCCL.  *out is NULL on error;
+ * the message is then available from pdcs_last_error(NULL). */
+pdcs_status pdcs_create(pdcs_ctx **out, int64_t m_global, int64_t n, int64_t n1,
+                        int64_t row_begin, int64_t row_end, const int64_t *row_ptr,
+                        const int32_t *col_idx, const double *vals, const double *c,
+                        const double *h, const double *l, const double *u,
+                        const pdcs_params *p, int device, void *cuda_stream, int mem_kind,
+                        const void *nccl_unique_id, int rank, int world);
+
+/* Cone lists (host arrays always): npc primal blocks (kinds pk, dims pdim)
+ * over x[n1:n] and nrc row blocks over the GLOBAL rows (kinds rk, dims rdim).
+ * Scaling (Ruiz + PC) runs here because RSOC blocks need equal leading
+ * divisors.  Errors: ARG, CONE, SHARD, STATE, CUDA. */
+pdcs_status pdcs_set_cones(pdcs_ctx *ctx, const int32_t *pk, const int64_t *pdim, int64_t npc,
+                           const int32_t *rk, const int64_t *rdim, int64_t nrc);
+
+/* Run exactly n_inner ACCEPTED inner iterations of Alg. 1
+ * including the Eq. 9 checks, restarts and primal-weight updates at the
+ * check cadence; does not stop at tol.  out (may be NULL) receives counters.
+ * Errors: STATE, NUMERICAL, CUDA. */
+pdcs_status pdcs_iterate(pdcs_ctx *ctx, int64_t n_inner, pdcs_result_t *out);
+
+/* Eq. 9 residuals of the selected iterate, ORIGINAL space. */
+pdcs_status pdcs_kkt(pdcs_ctx *ctx, int which, pdcs_kkt_t *out);
+
+/* Alg. 1 until max(err_p, err_d, err_gap) <= tol or a limit; returns the best
+ * evaluated point's residuals (reading A15).  Continues from the current state. */
+pdcs_status pdcs_solve(pdcs_ctx *ctx, pdcs_result_t *out);
+
+/* Copy an iterate out: x [n], y [local rows]; space SCALED or ORIGINAL
+ * (x = x~/q, y = y~/r, reading A2).  Output memory per the create mem_kind. */
+pdcs_status pdcs_get_iterate(pdcs_ctx *ctx, int which, int space, double *x, double *y);
+
+/* Set the current iterate (and anchor) from ORIGINAL-space x [n], y [local rows]. */
+pdcs_status pdcs_set_iterate(pdcs_ctx *ctx, const double *x, const double *y);
+
+/* Checkpoint / resume of the full Alg. 1 state in SCALED space:
+ *   x, y (current z^{t,k}), x0, y0 (anchor z^{t,0}), xsum, ysum (sum eta z of
+ *   the epoch) — n / local-rows doubles each, memory per the create mem_kind;
+ *   sc[13] = eta, eta_init, omega, beta, W, r_start, e_anchor, e_prev, best_e,
+ *            k, total, trials, restarts (host array).
+ * pdcs_set_state recomputes the cached products K~x, K~^T y, K~x0, K~^T y0 on
+ * the device.  Any pointer may be NULL on get.  Errors: STATE, ARG, CUDA. */
+pdcs_status pdcs_get_state(pdcs_ctx *ctx, double *x, double *y, double *x0, double *y0,
+                           double *xsum, double *ysum, double *sc);
+pdcs_status pdcs_set_state(pdcs_ctx *ctx, const double *x, const double *y, const double *x0,
+                           const double *y0, const double *xsum, const double *ysum,
+                           const double *sc);
+
+/* Row and column divisors r [local rows], q [n] (K~ = diag(1/r) G diag(1/q)). */
+pdcs_status pdcs_get_scaling(pdcs_ctx *ctx, double *r, double *q);
+
+/* Device-side timing of the kernels launched by the last pdcs_iterate call:
+ * names/ms accumulated per kernel family (diagnostics; fills up to cap
+ * entries, returns the count). */
+int pdcs_kernel_times(pdcs_ctx *ctx, char (*names)[32], double *ms, int64_t *launches, int cap);
+void pdcs_enable_timing(pdcs_ctx *ctx, int on);
+
+/* Control-state snapshot (diagnostics / decision-trace comparison).  Fills up
+ * to cap doubles: eta, omega, beta, k, total, trials, restarts, e_anchor, W,
+ * eta_init, kkt_cur[5], kkt_avg[5], e_prev, best_e, use_avg, restart flag.
+ * Returns the number of values written. */
+int pdcs_get_scalars(pdcs_ctx *ctx, double *out, int cap);
+
+/* Number of kernel launches issued by the last pdcs_iterate call. */
+int64_t pdcs_launch_count(const pdcs_ctx *ctx);
+
+const char *pdcs_last_error(const pdcs_ctx *ctx);
+void pdcs_destroy(pdcs_ctx *ctx);
+
+/* Fill out[128] with a fresh ncclUniqueId (rank 0 broadcasts it). */
+pdcs_status pdcs_nccl_unique_id(void *out128);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDCS_H_ */

@@ -104,6 +104,7 @@ def _declare(L):
                            C.c_int64, P_I32, P_I64, C.c_int64, C.c_int, C.c_int, P_D, P_D]
     L.orc_set_iterate.argtypes = [C.c_void_p, P_D, P_D]
     L.orc_kkt_point.argtypes = [C.c_void_p, P_D, P_D, P_D]
+    L.orc_get_state.argtypes = [C.c_void_p] + [P_D] * 7
     L.orc_create.argtypes = [C.c_int64, C.c_int64, C.c_int64, P_I64, P_I32, P_D, P_D, P_D, P_D,
                              P_D, P_I32, P_I64, C.c_int64, P_I32, P_I64, C.c_int64,
                              C.POINTER(Params)]
@@ -287,15 +288,26 @@ class OracleSolver:
         return dict(err_p=out[0], err_d=out[1], err_gap=out[2], pobj=out[3], dobj=out[4])
 
     def scalars(self):
-        out = np.zeros(10)
+        out = np.zeros(25)
         lib().orc_scalars(self.h, out.ctypes.data_as(P_D))
         keys = ["eta", "omega", "beta", "k", "total", "trials", "restarts", "e_anchor", "W",
-                "eta0"]
+                "eta0", "cur_err_p", "cur_err_d", "cur_err_gap", "cur_pobj", "cur_dobj",
+                "avg_err_p", "avg_err_d", "avg_err_gap", "avg_pobj", "avg_dobj", "e_prev", "best_e",
+                "last_num", "last_cross", "last_cross_abs"]
         return dict(zip(keys, out))
 
     def set_iterate(self, x, y):
         x, y = _d(x), _d(y)
         lib().orc_set_iterate(self.h, x[1], y[1])
+
+    def get_state(self):
+        n, m = self.prog.n, self.prog.m
+        v = {k: np.zeros(n if k[0] == "x" else m) for k in ("x", "y", "x0", "y0", "xsum", "ysum")}
+        sc = np.zeros(13)
+        lib().orc_get_state(self.h, *[v[k].ctypes.data_as(P_D) for k in ("x", "y", "x0", "y0", "xsum",
+                                                                         "ysum")], sc.ctypes.data_as(P_D))
+        v["sc"] = sc
+        return v
 
     def kkt_point(self, x, y):
         """Eq. 9 at an original-space point."""

@@ -472,6 +472,7 @@ struct Solver {
   Kkt last_cur{}, last_avg{}, best_kkt{};
   vector<int32_t> trace;        // decisions: 1 accept,0 reject,10+cand,20+restart
   double vanilla_step = 0.0;
+  double last_num = 0.0, last_cross = 0.0, last_cross_abs = 0.0;
 
   // x in X~ = [q l, q u] x prod diag(q_B) K_B  (Eq. 5 primal projection)
   void proj_X(double* v) const {
@@ -689,6 +690,9 @@ struct Solver {
       }
       num = omega * dxx + dyy / omega;
       double etabar = ls_bound(num, cross);
+      last_num = num; last_cross = cross;
+      last_cross_abs = 0.0;
+      for (int64_t i = 0; i < m; ++i) last_cross_abs += std::fabs((yh[i] - y[i]) * (Kxh[i] - Kx[i]));
       trials++;
       if (eta <= etabar) {
         trace.push_back(1);
@@ -939,6 +943,18 @@ void orc_set_iterate(void* h, const double* x, const double* y) {
   S->x0 = S->x; S->y0 = S->y; S->xh = S->x; S->yh = S->y;
   S->e_anchor = S->kmax(S->kkt(S->x.data(), S->y.data()));
 }
+// Full Alg. 1 state (scaled space) for checkpoint shadowing.
+void orc_get_state(void* h, double* x, double* y, double* x0, double* y0, double* xs, double* ys,
+                   double* sc) {
+  Solver* S = (Solver*)h;
+  std::copy(S->x.begin(), S->x.end(), x); std::copy(S->y.begin(), S->y.end(), y);
+  std::copy(S->x0.begin(), S->x0.end(), x0); std::copy(S->y0.begin(), S->y0.end(), y0);
+  std::copy(S->xsum.begin(), S->xsum.end(), xs); std::copy(S->ysum.begin(), S->ysum.end(), ys);
+  const double v[13] = {S->eta, S->eta_init, S->omega, S->beta, S->Wsum, S->r_start, S->e_anchor,
+                        S->e_prev, S->best_e, (double)S->k, (double)S->total, (double)S->trials,
+                        (double)S->restarts};
+  std::copy(v, v + 13, sc);
+}
 // Eq. 9 at an ORIGINAL-space point (x, y).
 void orc_kkt_point(void* h, const double* x, const double* y, double* out) {
   Solver* S = (Solver*)h;
@@ -954,6 +970,13 @@ void orc_scalars(void* h, double* out) {
   out[0] = S->eta; out[1] = S->omega; out[2] = S->beta; out[3] = (double)S->k;
   out[4] = (double)S->total; out[5] = (double)S->trials; out[6] = (double)S->restarts;
   out[7] = S->e_anchor; out[8] = S->Wsum; out[9] = S->eta_init;
+  const Kkt* ks[2] = {&S->last_cur, &S->last_avg};
+  for (int c = 0; c < 2; ++c) {
+    out[10 + 5 * c] = ks[c]->err_p; out[11 + 5 * c] = ks[c]->err_d; out[12 + 5 * c] = ks[c]->err_gap;
+    out[13 + 5 * c] = ks[c]->pobj; out[14 + 5 * c] = ks[c]->dobj;
+  }
+  out[20] = S->e_prev; out[21] = S->best_e;
+  out[22] = S->last_num; out[23] = S->last_cross; out[24] = S->last_cross_abs;
 }
 int64_t orc_trace(void* h, int32_t* out, int64_t cap) {
   Solver* S = (Solver*)h;

@@ -1,0 +1,1089 @@
+// pdcs.cu — libpdcs.so: C ABI (include/pdcs.h) and the host state machine of
+// Alg. 1.  Every step of the method runs in the kernels of
+// ops.cuh / kernels.cuh / spmv.cuh / cones.cuh; the host only validates input,
+// lays data out in HBM, enqueues kernels on the caller's stream and reads
+// back the few control flags the next launch depends on.
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/pdcs.h"
+#include "ops.cuh"
+
+using namespace pdcs;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct CudaErr {
+  cudaError_t e;
+  const char* what;
+  int line;
+};
+
+#define CK(call)                                                        \
+  do {                                                                  \
+    cudaError_t _e = (call);                                            \
+    if (_e != cudaSuccess) throw CudaErr{_e, #call, __LINE__};          \
+  } while (0)
+
+struct StatusErr {
+  pdcs_status st;
+  std::string msg;
+};
+[[noreturn]] void fail(pdcs_status st, const std::string& msg) { throw StatusErr{st, msg}; }
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    free_();
+    n = count;
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void free_() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { free_(); }
+};
+
+int grid_for(int64_t n, int sms, int per_sm = 8) {
+  int64_t g = (n + kThreads - 1) / kThreads;
+  g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sms * per_sm));
+  return (int)g;
+}
+
+}  // namespace
+
+// ============================================================================
+struct pdcs_ctx {
+  // problem (host copies of what the setup needs)
+  int64_t m = 0, n = 0, n1 = 0, mg = 0, row_begin = 0;
+  pdcs_params prm{};
+  int device = 0, sms = 148;
+  cudaStream_t st = nullptr;
+  int mem_kind = PDCS_MEM_HOST;
+  int rank = 0, world = 1;
+  bool cones_set = false;
+  std::string err;
+  std::vector<int64_t> hptr;       // local CSR row pointers (host)
+  std::vector<double> hl, hu;      // original bounds
+  double hnorm = 0.0, cnorm = 0.0; // ||h||_inf, ||c||_inf (original data)
+
+  // device matrices
+  DevCsr K, KT;
+  DBuf<int32_t> Kptr, Kcol, KTptr, KTcol, planrows;
+  DBuf<double> Kval, KTval;
+  // device vectors (scaled space unless noted)
+  DBuf<double> c0, h0, l0, u0;                 // original data
+  DBuf<double> r, q, ct, ht, lt, ut;           // divisors, scaled data
+  DBuf<double> x, xh, x0, xsum, kty, ktyh, xa, ktya, bx, candx, lam0, lam1, onesn;
+  DBuf<double> y, yh, y0, ysum, kxh, kxd, ya, kxa, by, candy, res0, res1, onesm;
+  DBuf<double> tmpn, tmpm, scal;
+  DBuf<uint8_t> ek, rk;
+  DBuf<Block> pblocks, rblocks;
+  DBuf<int64_t> rsoc_offs_p, rsoc_offs_r;
+  DBuf<double> tpart, kpart, gbuf;
+  Ctl* ctl = nullptr;        // device
+  Ctl* hctl = nullptr;       // pinned host mirror
+
+  // block classes per side: [thread, warp, cta, grid] ranges into the block arrays
+  struct BClass { int64_t begin = 0, count = 0; int grid = 0; int64_t slot = 0; int64_t kslot[2] = {0, 0}; };
+  BClass pcls[4], rcls[4];
+  int64_t nslot_trial = 0, nslot_kkt = 0;
+  int64_t slot_pe = 0, slot_spmv = 0, kslot_rows = 0, kslot_cols = 0;
+  int g_pe = 0, g_m = 0, g_kr = 0, g_kc = 0, g_grid = 0;
+
+  // timing / counters
+  bool timing = false;
+  std::map<std::string, std::pair<double, int64_t>> ktimes;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  int64_t launches = 0;
+
+  ~pdcs_ctx() {
+    if (ctl) cudaFree(ctl);
+    if (hctl) cudaFreeHost(hctl);
+    for (auto e : evpool) cudaEventDestroy(e);
+  }
+
+  // ---------------------------------------------------------------- launch helpers
+  cudaEvent_t ev() {
+    if (evnext == evpool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      evpool.push_back(e);
+    }
+    return evpool[evnext++];
+  }
+  template <class F>
+  void launch(const char* name, F&& f) {
+    ++launches;
+    if (!timing) {
+      f();
+      CK(cudaGetLastError());
+      return;
+    }
+    cudaEvent_t a = ev(), b = ev();
+    CK(cudaEventRecord(a, st));
+    f();
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(b, st));
+    pending.push_back({name, {a, b}});
+  }
+  void flush_timing() {
+    if (!timing) return;
+    CK(cudaStreamSynchronize(st));
+    for (auto& p : pending) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+      auto& e = ktimes[p.first];
+      e.first += ms;
+      e.second += 1;
+    }
+    pending.clear();
+    evnext = 0;
+  }
+
+  template <class Epi>
+  void spmv(const char* name, const DevCsr& A, const double* x1, const double* x2, Epi epi, double* part,
+            int64_t slot0) {
+    if (A.plan.total_cta == 0) return;
+    launch(name, [&] {
+      spmv_kernel<Epi><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, x1, x2, A.plan, epi, ctl,
+                                                              part, slot0);
+    });
+  }
+  void spmv_store(const DevCsr& A, const double* xin, double* out) {
+    EpiStore e{out};
+    spmv("spmv_store", A, xin, nullptr, e, nullptr, 0);
+  }
+
+  void read_ctl() {
+    CK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  void write_ctl() {
+    CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // ---------------------------------------------------------------- block kernels
+  BlockArgs bargs(bool primal, int op) {
+    BlockArgs A{};
+    A.blocks = primal ? pblocks.p : rblocks.p;
+    A.op = op;
+    A.x = x.p; A.c = ct.p; A.kty = kty.p; A.xh = xh.p;
+    A.D = primal ? q.p : r.p;
+    A.y = y.p; A.yh = yh.p; A.kxd = kxd.p;
+    return A;
+  }
+  void run_blocks(bool primal, BlockArgs A, bool kkt, int cand) {
+    BClass* cl = primal ? pcls : rcls;
+    for (int c = 0; c < 4; ++c) {
+      if (cl[c].count == 0) continue;
+      BlockArgs B = A;
+      B.blocks = A.blocks + cl[c].begin;
+      B.nblocks = cl[c].count;
+      B.cand = cand;
+      B.part = kkt ? kpart.p : tpart.p;
+      B.slot0 = kkt ? cl[c].kslot[cand] : cl[c].slot;
+      const int g = cl[c].grid;
+      if (c == 0) launch("blocks_thread", [&] { k_blocks_thread<<<g, kThreads, 0, st>>>(B, ctl); });
+      else if (c == 1) launch("blocks_warp", [&] { k_blocks_warp<<<g, kThreads, 0, st>>>(B, ctl); });
+      else if (c == 2 || kkt || A.op == BOP_AVG_PRIMAL || A.op == BOP_AVG_DUAL) {
+        // KKT / average passes use the CTA team for giant blocks as well
+        const int gg = c == 3 ? (int)std::min<int64_t>(cl[c].count, sms) : g;
+        if (c == 3) { B.slot0 = kkt ? cl[c].kslot[cand] : cl[c].slot; }
+        launch("blocks_cta", [&] { k_blocks_cta<<<gg, kThreads, 0, st>>>(B, ctl); });
+      } else {
+        double* gb = gbuf.p;
+        const Ctl* cp = ctl;
+        void* args[] = {(void*)&B, (void*)&cp, (void*)&gb};
+        launch("blocks_grid", [&] {
+          CK(cudaLaunchCooperativeKernel((void*)k_blocks_grid, dim3(g), dim3(kThreads), args, 0, st));
+        });
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- Alg. 1 pieces
+  // One trial of AdaptiveStepPDHG (PDHG step Eq. 5 + accept test).
+  void trial() {
+    launch("primal_elem", [&] {
+      k_primal_elem<<<g_pe, kThreads, 0, st>>>(n, ek.p, x.p, ct.p, kty.p, lt.p, ut.p, xh.p, ctl, tpart.p,
+                                               slot_pe);
+    });
+    run_blocks(true, bargs(true, BOP_TRIAL_PRIMAL), false, 0);
+    EpiDualTrial e{y.p, ht.p, rk.p, kxh.p, kxd.p, yh.p, 0.0, 0};
+    spmv("spmv_K_dual", K, xh.p, x.p, e, tpart.p, slot_spmv);
+    run_blocks(false, bargs(false, BOP_TRIAL_DUAL), false, 0);
+    launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl); });
+  }
+  // Accepted step: y+ (Halpern/average on y), then K^T y+ with the fused
+  // Halpern/average on x.
+  void accept() {
+    launch("halpern_y", [&] {
+      k_halpern_y<<<g_m, kThreads, 0, st>>>(m, yh.p, y0.p, y.p, ysum.p, ctl);
+    });
+    EpiHalpernX e{xh.p, x0.p, x.p, kty.p, xsum.p, 0, 0, 0, 0, 0};
+    spmv("spmv_KT_halpern", KT, y.p, nullptr, e, nullptr, 0);
+  }
+  void kkt_launch(KktCand ca, KktCand cb, int ncand, int mode) {
+    launch("kkt_rows", [&] {
+      k_kkt_rows<<<g_kr, kThreads, 0, st>>>(m, rk.p, r.p, h0.p, y0.p, ca, cb, ncand, kpart.p, kslot_rows);
+    });
+    launch("kkt_cols", [&] {
+      k_kkt_cols<<<g_kc, kThreads, 0, st>>>(n, ek.p, q.p, c0.p, l0.p, u0.p, x0.p, ca, cb, ncand, kpart.p,
+                                            kslot_cols);
+    });
+    for (int c = 0; c < ncand; ++c) {
+      const KktCand& C = c ? cb : ca;
+      BlockArgs A = bargs(false, BOP_KKT_ROWS);
+      A.scratch = C.res;
+      run_blocks(false, A, true, c);
+      BlockArgs B = bargs(true, BOP_KKT_COLS);
+      B.scratch = C.lam;
+      run_blocks(true, B, true, c);
+    }
+    // zero the slots of a candidate that was not evaluated
+    if (ncand == 1) zero_cand1_kslots();
+    launch("kkt_finalize", [&] {
+      k_kkt_finalize<<<1, kThreads, 0, st>>>(kpart.p, nslot_kkt, ncand, mode, hnorm, cnorm, ctl);
+    });
+  }
+  void zero_cand1_kslots() {
+    for (int side = 0; side < 2; ++side) {
+      BClass* cl = side ? pcls : rcls;
+      for (int c = 0; c < 4; ++c)
+        if (cl[c].count) {
+          const int g = c == 3 ? (int)std::min<int64_t>(cl[c].count, sms) : cl[c].grid;
+          CK(cudaMemsetAsync(kpart.p + cl[c].kslot[1] * kKAcc, 0, (size_t)g * kKAcc * sizeof(double), st));
+        }
+    }
+  }
+  // Eq. 9 check every check_interval accepted iterations.
+  void check() {
+    const bool van = prm.vanilla_pdhg != 0;
+    KktCand c0{xh.p, yh.p, kxh.p, ktyh.p, res0.p, lam0.p};
+    KktCand c1{xa.p, ya.p, kxa.p, ktya.p, res1.p, lam1.p};
+    spmv_store(KT, yh.p, ktyh.p);   // K^T y^ of the current candidate (K x^ kept by the K pass)
+    if (!van) {
+      launch("avg_elem", [&] { k_avg_elem<<<g_pe, kThreads, 0, st>>>(n, ek.p, xsum.p, lt.p, ut.p, xa.p, ctl); });
+      BlockArgs A = bargs(true, BOP_AVG_PRIMAL);
+      A.sum = xsum.p; A.out = xa.p;
+      run_blocks(true, A, false, 0);
+      launch("avg_elem", [&] { k_avg_elem<<<g_m, kThreads, 0, st>>>(m, rk.p, ysum.p, nullptr, nullptr, ya.p, ctl); });
+      BlockArgs B = bargs(false, BOP_AVG_DUAL);
+      B.sum = ysum.p; B.out = ya.p;
+      run_blocks(false, B, false, 0);
+      spmv_store(K, xa.p, kxa.p);
+      spmv_store(KT, ya.p, ktya.p);
+    }
+    kkt_launch(c0, c1, van ? 1 : 2, 1);
+    RestartArgs R{};
+    R.n = n; R.m = m;
+    R.cx[0] = xh.p; R.cy[0] = yh.p; R.ckty[0] = ktyh.p;
+    R.cx[1] = xa.p; R.cy[1] = ya.p; R.ckty[1] = ktya.p;
+    R.x = x.p; R.x0 = x0.p; R.y = y.p; R.y0 = y0.p; R.kty = kty.p;
+    R.xsum = xsum.p; R.ysum = ysum.p; R.bx = bx.p; R.by = by.p; R.candx = candx.p;
+    R.candy = candy.p;
+    launch("restart_copy", [&] {
+      k_restart_copy<<<grid_for(std::max(n, m), sms), kThreads, 0, st>>>(R, ctl);
+    });
+  }
+
+  // products of (x, y) into (kx, kty)
+  void products(const double* xs, const double* ys, double* kxo, double* ktyo) {
+    spmv_store(K, xs, kxo);
+    spmv_store(KT, ys, ktyo);
+  }
+
+  // ---------------------------------------------------------------- setup helpers
+  void build_plan(DevCsr& A, const std::vector<int64_t>& ptr, std::vector<int32_t>& rowstore,
+                  std::vector<size_t>& offs) {
+    const int64_t rows = (int64_t)ptr.size() - 1;
+    // V classes: 1 (<=2), 4 (<=8), 8 (<=16), 16 (<=32), 32 (<=4096), 0 (>4096)
+    const int Vs[kMaxClasses] = {1, 4, 8, 16, 32, 0};
+    std::vector<int64_t> lists[kMaxClasses];
+    for (int64_t i = 0; i < rows; ++i) {
+      const int64_t L = ptr[i + 1] - ptr[i];
+      int c = L <= 2 ? 0 : L <= 8 ? 1 : L <= 16 ? 2 : L <= 32 ? 3 : L <= 4096 ? 4 : 5;
+      lists[c].push_back(i);
+    }
+    SpmvPlan P{};
+    P.ncls = 0;
+    int total = 0;
+    for (int c = 0; c < kMaxClasses; ++c) {
+      if (lists[c].empty()) continue;
+      SpmvClass& K_ = P.cls[P.ncls++];
+      K_.V = Vs[c];
+      K_.nrows = (int64_t)lists[c].size();
+      const bool contiguous = lists[c].back() - lists[c].front() + 1 == K_.nrows;
+      K_.range_begin = contiguous ? lists[c].front() : 0;
+      K_.rows = nullptr;
+      if (!contiguous) {
+        offs.push_back(rowstore.size());
+        for (int64_t r_ : lists[c]) rowstore.push_back((int32_t)r_);
+        K_.rows = (const int32_t*)(uintptr_t)(offs.back() + 1);   // patched after upload
+      }
+      int64_t rows_per_cta = K_.V == 0 ? 1 : K_.V == 1 ? kThreads : kThreads / K_.V;
+      int64_t g = (K_.nrows + rows_per_cta - 1) / rows_per_cta;
+      const int64_t cap = K_.V == 0 ? (int64_t)sms * 4 : (int64_t)sms * 8;
+      K_.ncta = (int32_t)std::max<int64_t>(1, std::min(g, cap));
+      total += K_.ncta;
+    }
+    P.total_cta = total;
+    A.plan = P;
+  }
+  void patch_plan(DevCsr& A) {
+    for (int c = 0; c < A.plan.ncls; ++c)
+      if (A.plan.cls[c].rows) {
+        const size_t off = (size_t)(uintptr_t)A.plan.cls[c].rows - 1;
+        A.plan.cls[c].rows = planrows.p + off;
+      }
+  }
+};
+
+// ============================================================================
+namespace {
+
+pdcs_status guard(pdcs_ctx* ctx, const std::function<void()>& f) {
+  try {
+    f();
+    return PDCS_OK;
+  } catch (const CudaErr& e) {
+    std::string msg = std::string("CUDA error ") + cudaGetErrorString(e.e) + " at line " +
+                      std::to_string(e.line) + ": " + e.what;
+    if (ctx) ctx->err = msg; else g_create_error = msg;
+    return PDCS_ERR_CUDA;
+  } catch (const StatusErr& e) {
+    if (ctx) ctx->err = e.msg; else g_create_error = e.msg;
+    return e.st;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what(); else g_create_error = e.what();
+    return PDCS_ERR_ARG;
+  }
+}
+
+template <class T>
+std::vector<T> to_host(const T* p, int64_t count, int mem_kind) {
+  std::vector<T> v((size_t)std::max<int64_t>(count, 0));
+  if (count <= 0) return v;
+  if (!p) fail(PDCS_ERR_ARG, "null input pointer");
+  if (mem_kind == PDCS_MEM_DEVICE) CK(cudaMemcpy(v.data(), p, count * sizeof(T), cudaMemcpyDeviceToHost));
+  else std::memcpy(v.data(), p, count * sizeof(T));
+  return v;
+}
+
+template <class T>
+void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
+  d.alloc(h.size());
+  if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+}  // namespace
+
+// Internal: (re)initialise z, z0, products, sums and e_anchor from the current x, y.
+static void reset_from_current(pdcs_ctx* ctx) {
+  cudaStream_t st = ctx->st;
+  const int64_t n = ctx->n, m = ctx->m;
+  ctx->products(ctx->x.p, ctx->y.p, ctx->kxh.p, ctx->kty.p);
+  auto cp = [&](double* d, const double* s, int64_t cnt) {
+    if (cnt) CK(cudaMemcpyAsync(d, s, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  };
+  cp(ctx->x0.p, ctx->x.p, n); cp(ctx->xh.p, ctx->x.p, n);
+  cp(ctx->ktyh.p, ctx->kty.p, n); cp(ctx->candx.p, ctx->x.p, n);
+  cp(ctx->y0.p, ctx->y.p, m); cp(ctx->yh.p, ctx->y.p, m); cp(ctx->candy.p, ctx->y.p, m);
+  CK(cudaMemsetAsync(ctx->xsum.p, 0, n * sizeof(double), st));
+  CK(cudaMemsetAsync(ctx->ysum.p, 0, m * sizeof(double), st));
+  KktCand c0{ctx->x.p, ctx->y.p, ctx->kxh.p, ctx->kty.p, ctx->res0.p, ctx->lam0.p};
+  ctx->kkt_launch(c0, c0, 1, 0);
+  ctx->read_ctl();
+  Ctl& C = *ctx->hctl;
+  C.e_anchor = std::max(C.kkt[0][0], std::max(C.kkt[0][1], C.kkt[0][2]));
+  C.k = 0;
+  C.Wsum = 0.0;
+  C.beta = ctx->prm.beta_max;
+  C.e_prev = -1.0;
+  ctx->write_ctl();
+}
+
+// ============================================================================
+extern "C" {
+
+void pdcs_default_params(pdcs_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->tol = 1e-6;
+  p->max_iters = 1000000;
+  p->time_limit_s = 0.0;
+  p->ruiz_iters = 10;
+  p->pock_chambolle = 1;
+  p->check_interval = 40;
+  p->vanilla_pdhg = 0;
+  p->eta0 = 0.0;
+  p->omega0 = 0.0;
+  p->beta_max = 1.0;
+  p->refl_window = 40;
+  p->restart_suff = 0.2;
+  p->restart_nec = 0.8;
+  p->restart_art = 0.36;
+  p->ls_shrink = 0.5;
+  p->ls_grow = 1.05;
+  p->ls_max_rejects = 60;
+  p->verbose = 0;
+}
+
+const char* pdcs_last_error(const pdcs_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1, int64_t row_begin,
+                        int64_t row_end, const int64_t* row_ptr, const int32_t* col_idx,
+                        const double* vals, const double* c, const double* h, const double* l,
+                        const double* u, const pdcs_params* p, int device, void* cuda_stream,
+                        int mem_kind, const void* nccl_unique_id, int rank, int world) {
+  if (!out) return PDCS_ERR_ARG;
+  *out = nullptr;
+  pdcs_ctx* ctx = new pdcs_ctx();
+  pdcs_status s = guard(nullptr, [&] {
+    if (m_global < 0 || n < 0 || n1 < 0 || n1 > n) fail(PDCS_ERR_DIM, "bad sizes m/n/n1");
+    if (row_begin < 0 || row_end < row_begin || row_end > m_global) fail(PDCS_ERR_DIM, "bad row range");
+    if (mem_kind != PDCS_MEM_HOST && mem_kind != PDCS_MEM_DEVICE) fail(PDCS_ERR_ARG, "bad mem_kind");
+    if (world != 1 || nccl_unique_id) fail(PDCS_ERR_ARG, "multi-rank contexts are not enabled in this build");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(PDCS_ERR_CUDA, "no CUDA device");
+    if (device < 0 || device >= ndev) fail(PDCS_ERR_ARG, "bad device ordinal");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) fail(PDCS_ERR_CUDA, "libpdcs is built for sm_100a; device is sm_" +
+                                              std::to_string(prop.major * 10 + prop.minor));
+    ctx->device = device;
+    ctx->sms = prop.multiProcessorCount;
+    ctx->st = (cudaStream_t)cuda_stream;
+    ctx->mem_kind = mem_kind;
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->mg = m_global;
+    ctx->m = row_end - row_begin;
+    ctx->row_begin = row_begin;
+    ctx->n = n;
+    ctx->n1 = n1;
+    if (p) ctx->prm = *p; else pdcs_default_params(&ctx->prm);
+    if (ctx->prm.check_interval < 1 || ctx->prm.refl_window < 1) fail(PDCS_ERR_ARG, "bad cadence params");
+    const int64_t m = ctx->m;
+    // ---- host copies + validation
+    ctx->hptr = to_host(row_ptr, m + 1, mem_kind);
+    if (ctx->hptr[0] != 0) fail(PDCS_ERR_DIM, "row_ptr[0] must be 0");
+    for (int64_t i = 0; i < m; ++i)
+      if (ctx->hptr[i + 1] < ctx->hptr[i]) fail(PDCS_ERR_DIM, "row_ptr not monotone at row " + std::to_string(i));
+    const int64_t nnz = ctx->hptr[m];
+    if (nnz >= ((int64_t)1 << 31)) fail(PDCS_ERR_DIM, "local nnz must be < 2^31 (shard the rows)");
+    std::vector<int32_t> hcol = to_host(col_idx, nnz, mem_kind);
+    std::vector<double> hval = to_host(vals, nnz, mem_kind);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t q_ = ctx->hptr[i]; q_ < ctx->hptr[i + 1]; ++q_) {
+        if (hcol[q_] < 0 || hcol[q_] >= n) fail(PDCS_ERR_DIM, "column index out of range in row " + std::to_string(i));
+        if (q_ > ctx->hptr[i] && hcol[q_] <= hcol[q_ - 1])
+          fail(PDCS_ERR_DIM, "column indices not strictly increasing in row " + std::to_string(i));
+        if (!std::isfinite(hval[q_])) fail(PDCS_ERR_NONFINITE, "non-finite matrix entry in row " + std::to_string(i));
+      }
+    std::vector<double> hc = to_host(c, n, mem_kind), hh = to_host(h, m, mem_kind);
+    ctx->hl = to_host(l, n1, mem_kind);
+    ctx->hu = to_host(u, n1, mem_kind);
+    for (double v : hc) if (!std::isfinite(v)) fail(PDCS_ERR_NONFINITE, "non-finite c");
+    for (double v : hh) if (!std::isfinite(v)) fail(PDCS_ERR_NONFINITE, "non-finite h");
+    for (int64_t j = 0; j < n1; ++j) {
+      if (std::isnan(ctx->hl[j]) || std::isnan(ctx->hu[j]) || ctx->hl[j] > ctx->hu[j] ||
+          ctx->hl[j] == INFINITY || ctx->hu[j] == -INFINITY)
+        fail(PDCS_ERR_BOUNDS, "bound inversion at index " + std::to_string(j));
+    }
+    double hn = 0.0, cn = 0.0;
+    for (double v : hh) hn = std::max(hn, std::fabs(v));
+    for (double v : hc) cn = std::max(cn, std::fabs(v));
+    ctx->hnorm = hn;
+    ctx->cnorm = cn;
+    cudaStream_t st = ctx->st;
+    // ---- device CSR(K)
+    std::vector<int32_t> p32(m + 1);
+    for (int64_t i = 0; i <= m; ++i) p32[i] = (int32_t)ctx->hptr[i];
+    upload(ctx->Kptr, p32, st);
+    upload(ctx->Kcol, hcol, st);
+    upload(ctx->Kval, hval, st);
+    upload(ctx->c0, hc, st);
+    upload(ctx->h0, hh, st);
+    upload(ctx->l0, ctx->hl, st);
+    upload(ctx->u0, ctx->hu, st);
+    ctx->K.m = m; ctx->K.n = n; ctx->K.nnz = nnz;
+    ctx->K.ptr = ctx->Kptr.p; ctx->K.col = ctx->Kcol.p; ctx->K.val = ctx->Kval.p;
+    // ---- device CSR(K^T) by a stable radix sort of the entries on column id
+    ctx->KTptr.alloc(n + 1);
+    ctx->KTcol.alloc(nnz);
+    ctx->KTval.alloc(nnz);
+    {
+      DBuf<int32_t> keys_in, keys_out, perm_in, perm_out, rid, cnt;
+      keys_in.alloc(nnz); keys_out.alloc(nnz); perm_in.alloc(nnz); perm_out.alloc(nnz); rid.alloc(nnz);
+      cnt.alloc(n + 1);
+      const int G = grid_for(nnz, ctx->sms, 32);
+      if (nnz) {
+        CK(cudaMemcpyAsync(keys_in.p, ctx->Kcol.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        k_iota<<<G, kThreads, 0, st>>>(nnz, perm_in.p);
+        k_row_ids<<<grid_for(m, ctx->sms, 32), kThreads, 0, st>>>(m, ctx->Kptr.p, rid.p);
+        int bits = 1;
+        while (((int64_t)1 << bits) < n) ++bits;
+        size_t tmpb = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmpb, keys_in.p, keys_out.p, perm_in.p, perm_out.p,
+                                           (int)nnz, 0, bits, st));
+        DBuf<char> tmp;
+        tmp.alloc(tmpb);
+        CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmpb, keys_in.p, keys_out.p, perm_in.p, perm_out.p,
+                                           (int)nnz, 0, bits, st));
+        k_gather_t<<<G, kThreads, 0, st>>>(nnz, perm_out.p, rid.p, ctx->Kval.p, ctx->KTcol.p, ctx->KTval.p);
+      }
+      CK(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(int32_t), st));
+      if (nnz) k_count_cols<<<G, kThreads, 0, st>>>(nnz, ctx->Kcol.p, cnt.p);
+      size_t tmpb = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmpb, cnt.p, ctx->KTptr.p, (int)(n + 1), st));
+      DBuf<char> tmp;
+      tmp.alloc(tmpb);
+      CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmpb, cnt.p, ctx->KTptr.p, (int)(n + 1), st));
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(st));
+    }
+    ctx->KT.m = n; ctx->KT.n = m; ctx->KT.nnz = nnz;
+    ctx->KT.ptr = ctx->KTptr.p; ctx->KT.col = ctx->KTcol.p; ctx->KT.val = ctx->KTval.p;
+    // ---- SpMV plans (row-length binning)
+    std::vector<int32_t> tptr32(n + 1);
+    CK(cudaMemcpy(tptr32.data(), ctx->KTptr.p, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    std::vector<int64_t> tptr(tptr32.begin(), tptr32.end());
+    std::vector<int32_t> rowstore;
+    std::vector<size_t> offs;
+    ctx->build_plan(ctx->K, ctx->hptr, rowstore, offs);
+    ctx->build_plan(ctx->KT, tptr, rowstore, offs);
+    upload(ctx->planrows, rowstore, st);
+    ctx->patch_plan(ctx->K);
+    ctx->patch_plan(ctx->KT);
+    // ---- control block
+    CK(cudaMalloc(&ctx->ctl, sizeof(Ctl)));
+    CK(cudaMallocHost(&ctx->hctl, sizeof(Ctl)));
+    std::memset(ctx->hctl, 0, sizeof(Ctl));
+    CK(cudaStreamSynchronize(st));
+  });
+  if (s != PDCS_OK) {
+    delete ctx;
+    return s;
+  }
+  *out = ctx;
+  return PDCS_OK;
+}
+
+pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim, int64_t npc,
+                           const int32_t* rkind, const int64_t* rdim, int64_t nrc) {
+  if (!ctx) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (ctx->cones_set) fail(PDCS_ERR_STATE, "cones already set");
+    if (npc < 0 || nrc < 0 || (npc && (!pk || !pdim)) || (nrc && (!rkind || !rdim)))
+      fail(PDCS_ERR_ARG, "bad cone arrays");
+    const int64_t n = ctx->n, n1 = ctx->n1, m = ctx->m, mg = ctx->mg;
+    cudaStream_t st = ctx->st;
+    auto dim_ok = [](int32_t k, int64_t d) {
+      switch (k) {
+        case C_ZERO: case C_NONNEG: return d >= 1;
+        case C_SOC: return d >= 2;
+        case C_RSOC: return d >= 3;
+        case C_EXP: case C_DEXP: return d == 3;
+        default: return false;
+      }
+    };
+    // element kinds
+    std::vector<uint8_t> ek(n), rk(m);
+    for (int64_t j = 0; j < n1; ++j) {
+      const bool fl = std::isfinite(ctx->hl[j]), fu = std::isfinite(ctx->hu[j]);
+      ek[j] = !fl && !fu ? EK_FREE : (fl && !fu) ? (ctx->hl[j] == 0.0 ? EK_LO0 : EK_LO) : (!fl ? EK_UP : EK_BOTH);
+    }
+    std::vector<Block> pb, rb;
+    std::vector<int64_t> prs, rrs;
+    int64_t off = n1;
+    for (int64_t b = 0; b < npc; ++b) {
+      if (!dim_ok(pk[b], pdim[b])) fail(PDCS_ERR_CONE, "bad primal cone " + std::to_string(b));
+      if (off + pdim[b] > n) fail(PDCS_ERR_CONE, "primal cone dims exceed n2");
+      const uint8_t e = pk[b] == C_ZERO ? EK_ZERO : pk[b] == C_NONNEG ? EK_NONNEG : EK_BLOCK;
+      for (int64_t j = off; j < off + pdim[b]; ++j) ek[j] = e;
+      if (e == EK_BLOCK) pb.push_back(Block{off, pk[b], (int32_t)pdim[b]});
+      if (pk[b] == C_RSOC) prs.push_back(off);
+      off += pdim[b];
+    }
+    if (off != n) fail(PDCS_ERR_CONE, "primal cone dims do not sum to n2");
+    off = 0;
+    for (int64_t b = 0; b < nrc; ++b) {
+      if (!dim_ok(rkind[b], rdim[b])) fail(PDCS_ERR_CONE, "bad row cone " + std::to_string(b));
+      const int64_t lo = off - ctx->row_begin, hi = lo + rdim[b];
+      if (hi > 0 && lo < m) {
+        if (lo < 0 || hi > m) fail(PDCS_ERR_SHARD, "row cone " + std::to_string(b) + " straddles the rank's rows");
+        const uint8_t e = rkind[b] == C_ZERO ? EK_FREE : rkind[b] == C_NONNEG ? EK_NONNEG : EK_BLOCK;
+        for (int64_t i = lo; i < hi; ++i) rk[i] = e;
+        if (e == EK_BLOCK) rb.push_back(Block{lo, rkind[b], (int32_t)rdim[b]});
+        if (rkind[b] == C_RSOC) rrs.push_back(lo);
+      }
+      off += rdim[b];
+    }
+    if (off != mg) fail(PDCS_ERR_CONE, "row cone dims do not sum to m");
+    // size classes: thread (exp, soc <= 32), warp (<= 2048), cta (<= 131072), grid
+    auto classify = [&](std::vector<Block>& v, pdcs_ctx::BClass* cl) {
+      auto cls = [](const Block& b) { return (b.kind == C_EXP || b.kind == C_DEXP || b.dim <= 32) ? 0 : b.dim <= 2048 ? 1 : b.dim <= 131072 ? 2 : 3; };
+      std::stable_sort(v.begin(), v.end(), [&](const Block& a, const Block& b) { return cls(a) < cls(b); });
+      for (int c = 0; c < 4; ++c) cl[c] = pdcs_ctx::BClass{};
+      for (size_t i = 0; i < v.size(); ++i) {
+        const int c = cls(v[i]);
+        if (cl[c].count == 0) cl[c].begin = (int64_t)i;
+        cl[c].count++;
+      }
+      for (int c = 0; c < 4; ++c) {
+        const int64_t cnt = cl[c].count;
+        if (!cnt) continue;
+        if (c == 0) cl[c].grid = grid_for(cnt, ctx->sms, 8);
+        else if (c == 1) cl[c].grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 7) / 8, (int64_t)ctx->sms * 8));
+        else if (c == 2) cl[c].grid = (int)std::min<int64_t>(cnt, (int64_t)ctx->sms * 4);
+        else {
+          int nb = 0;
+          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_blocks_grid, kThreads, 0));
+          cl[c].grid = std::max(1, std::min(nb, 2)) * ctx->sms;
+        }
+      }
+    };
+    classify(pb, ctx->pcls);
+    classify(rb, ctx->rcls);
+    upload(ctx->pblocks, pb, st);
+    upload(ctx->rblocks, rb, st);
+    upload(ctx->ek, ek, st);
+    upload(ctx->rk, rk, st);
+    std::vector<int64_t> prs64(prs.begin(), prs.end()), rrs64(rrs.begin(), rrs.end());
+    upload(ctx->rsoc_offs_p, prs64, st);
+    upload(ctx->rsoc_offs_r, rrs64, st);
+    // ---- partial-sum slots
+    ctx->g_pe = grid_for(n, ctx->sms);
+    ctx->g_m = grid_for(m, ctx->sms);
+    ctx->g_kr = grid_for(m, ctx->sms, 4);
+    ctx->g_kc = grid_for(n, ctx->sms, 4);
+    int64_t s = 0;
+    ctx->slot_pe = s; s += ctx->g_pe;
+    for (int c = 0; c < 4; ++c) if (ctx->pcls[c].count) { ctx->pcls[c].slot = s; s += ctx->pcls[c].grid; }
+    ctx->slot_spmv = s; s += ctx->K.plan.total_cta;
+    for (int c = 0; c < 4; ++c) if (ctx->rcls[c].count) { ctx->rcls[c].slot = s; s += ctx->rcls[c].grid; }
+    ctx->nslot_trial = s;
+    int64_t ks = 0;
+    ctx->kslot_rows = ks; ks += ctx->g_kr;
+    ctx->kslot_cols = ks; ks += ctx->g_kc;
+    for (int cand = 0; cand < 2; ++cand)
+      for (int side = 0; side < 2; ++side) {
+        pdcs_ctx::BClass* cl = side ? ctx->pcls : ctx->rcls;
+        for (int c = 0; c < 4; ++c)
+          if (cl[c].count) {
+            cl[c].kslot[cand] = ks;
+            ks += c == 3 ? (int)std::min<int64_t>(cl[c].count, ctx->sms) : cl[c].grid;
+          }
+      }
+    ctx->nslot_kkt = ks;
+    ctx->tpart.alloc(s * kAcc);
+    ctx->kpart.alloc(ks * kKAcc);
+    CK(cudaMemsetAsync(ctx->tpart.p, 0, s * kAcc * sizeof(double), st));
+    CK(cudaMemsetAsync(ctx->kpart.p, 0, ks * kKAcc * sizeof(double), st));
+    ctx->gbuf.alloc(4 * (size_t)ctx->sms * 8);
+    // ---- vectors
+    for (auto* b : {&ctx->r, &ctx->onesm, &ctx->ht, &ctx->y, &ctx->yh, &ctx->y0, &ctx->ysum,
+                    &ctx->kxh, &ctx->kxd, &ctx->ya, &ctx->kxa, &ctx->by, &ctx->candy, &ctx->res0,
+                    &ctx->res1, &ctx->tmpm})
+      b->alloc(std::max<int64_t>(m, 1));
+    for (auto* b : {&ctx->q, &ctx->onesn, &ctx->ct, &ctx->x, &ctx->xh, &ctx->x0, &ctx->xsum, &ctx->kty,
+                    &ctx->ktyh, &ctx->xa, &ctx->ktya, &ctx->bx, &ctx->candx, &ctx->lam0,
+                    &ctx->lam1, &ctx->tmpn})
+      b->alloc(std::max<int64_t>(n, 1));
+    ctx->lt.alloc(std::max<int64_t>(n1, 1));
+    ctx->ut.alloc(std::max<int64_t>(n1, 1));
+    ctx->scal.alloc(8);
+    const int Gm = grid_for(m, ctx->sms), Gn = grid_for(n, ctx->sms);
+    k_fill<<<Gm, kThreads, 0, st>>>(m, 1.0, ctx->r.p);
+    k_fill<<<Gm, kThreads, 0, st>>>(m, 1.0, ctx->onesm.p);
+    k_fill<<<Gn, kThreads, 0, st>>>(n, 1.0, ctx->q.p);
+    k_fill<<<Gn, kThreads, 0, st>>>(n, 1.0, ctx->onesn.p);
+    for (auto* b : {&ctx->y, &ctx->yh, &ctx->y0, &ctx->ysum, &ctx->kxh, &ctx->kxd, &ctx->ya,
+                    &ctx->kxa, &ctx->by, &ctx->candy, &ctx->res0, &ctx->res1})
+      CK(cudaMemsetAsync(b->p, 0, b->n * sizeof(double), st));
+    for (auto* b : {&ctx->x, &ctx->xh, &ctx->x0, &ctx->xsum, &ctx->kty, &ctx->ktyh, &ctx->xa,
+                    &ctx->ktya, &ctx->bx, &ctx->candx, &ctx->lam0, &ctx->lam1})
+      CK(cudaMemsetAsync(b->p, 0, b->n * sizeof(double), st));
+    const bool van = ctx->prm.vanilla_pdhg != 0;
+    // ---- Ruiz + Pock-Chambolle (readings A2, A3, A21)
+    const int Grm = grid_for(m * 32, ctx->sms, 16), Grn = grid_for(n * 32, ctx->sms, 16);
+    if (!van) {
+      for (int it = 0; it < ctx->prm.ruiz_iters + (ctx->prm.pock_chambolle ? 1 : 0); ++it) {
+        const int mode = it < ctx->prm.ruiz_iters ? 0 : 1;
+        k_row_norms<<<Grm, kThreads, 0, st>>>(m, ctx->K.ptr, ctx->K.col, ctx->K.val, ctx->r.p, ctx->q.p, mode,
+                                             ctx->tmpm.p);
+        k_row_norms<<<Grn, kThreads, 0, st>>>(n, ctx->KT.ptr, ctx->KT.col, ctx->KT.val, ctx->q.p, ctx->r.p,
+                                             mode, ctx->tmpn.p);
+        k_apply_root<<<Gm, kThreads, 0, st>>>(m, ctx->tmpm.p, ctx->r.p);
+        k_apply_root<<<Gn, kThreads, 0, st>>>(n, ctx->tmpn.p, ctx->q.p);
+      }
+      if (!prs64.empty()) k_rsoc_geomean<<<1, kThreads, 0, st>>>(ctx->rsoc_offs_p.p, (int64_t)prs64.size(), ctx->q.p);
+      if (!rrs64.empty()) k_rsoc_geomean<<<1, kThreads, 0, st>>>(ctx->rsoc_offs_r.p, (int64_t)rrs64.size(), ctx->r.p);
+      k_scale_vals<<<Grm, kThreads, 0, st>>>(m, ctx->K.ptr, ctx->K.col, ctx->K.val, ctx->r.p, ctx->q.p);
+      k_scale_vals<<<Grn, kThreads, 0, st>>>(n, ctx->KT.ptr, ctx->KT.col, ctx->KT.val, ctx->q.p, ctx->r.p);
+    }
+    CK(cudaGetLastError());
+    // scaled data (reading A2): c~ = c/q, h~ = h/r, l~ = q l, u~ = q u
+    k_ewise<<<Gn, kThreads, 0, st>>>(n, ctx->c0.p, ctx->q.p, 0, ctx->ct.p);
+    k_ewise<<<Gm, kThreads, 0, st>>>(m, ctx->h0.p, ctx->r.p, 0, ctx->ht.p);
+    if (n1) k_bounds<<<grid_for(n1, ctx->sms), kThreads, 0, st>>>(n1, ctx->q.p, ctx->l0.p, ctx->u0.p, ctx->lt.p, ctx->ut.p);
+    // ---- control block (reading A4-A6)
+    Ctl& C = *ctx->hctl;
+    std::memset(&C, 0, sizeof(Ctl));
+    const pdcs_params& P = ctx->prm;
+    C.vanilla = van ? 1 : 0;
+    C.ls_shrink = P.ls_shrink; C.ls_grow = P.ls_grow; C.beta_max = P.beta_max;
+    C.suff = P.restart_suff; C.nec = P.restart_nec; C.art = P.restart_art;
+    C.ls_max_rejects = P.ls_max_rejects; C.refl_window = P.refl_window; C.check_interval = P.check_interval;
+    C.tol = P.tol;
+    C.beta = P.beta_max;
+    C.e_prev = -1.0;
+    C.best_e = INFINITY;
+    C.status = ST_RUNNING;
+    double eta = 1.0, omega = 1.0;
+    if (van) {
+      if (P.eta0 > 0.0) eta = P.eta0;
+      else {
+        // tau = sigma = 0.9/||G||_2, power iteration on G^T G
+        const double v0 = 1.0 / std::sqrt((double)std::max<int64_t>(n, 1));
+        k_fill<<<Gn, kThreads, 0, st>>>(n, v0, ctx->tmpn.p);
+        double lam = 0.0;
+        for (int it = 0; it < 20; ++it) {
+          ctx->spmv_store(ctx->K, ctx->tmpn.p, ctx->tmpm.p);
+          ctx->spmv_store(ctx->KT, ctx->tmpm.p, ctx->lam0.p);
+          k_reduce<<<1, kThreads, 0, st>>>(n, ctx->lam0.p, 1, ctx->scal.p);
+          double s2 = 0.0;
+          CK(cudaMemcpyAsync(&s2, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          const double nw = std::sqrt(s2);
+          if (nw == 0.0) { lam = 0.0; break; }
+          const double prev = lam;
+          lam = nw;
+          // v = w / ||w||
+          CK(cudaMemcpyAsync(ctx->tmpn.p, ctx->lam0.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+          k_fill<<<Gn, kThreads, 0, st>>>(n, nw, ctx->lam1.p);
+          k_ewise<<<Gn, kThreads, 0, st>>>(n, ctx->tmpn.p, ctx->lam1.p, 0, ctx->tmpn.p);
+          if (it > 0 && std::fabs(lam - prev) < 1e-4 * lam) break;
+        }
+        const double nrm = std::sqrt(lam);
+        eta = nrm > 0.0 ? 0.9 / nrm : 1.0;
+      }
+      omega = 1.0;
+    } else {
+      // eta0 = 1/||K~||_inf (A5); omega0 = ||c~||/||h~|| clipped (A6)
+      k_row_norms<<<Grm, kThreads, 0, st>>>(m, ctx->K.ptr, ctx->K.col, ctx->K.val, ctx->onesm.p, ctx->onesn.p, 1,
+                                           ctx->tmpm.p);
+      k_reduce<<<1, kThreads, 0, st>>>(m, ctx->tmpm.p, 2, ctx->scal.p);
+      k_reduce<<<1, kThreads, 0, st>>>(n, ctx->ct.p, 0, ctx->scal.p + 1);
+      k_reduce<<<1, kThreads, 0, st>>>(m, ctx->ht.p, 0, ctx->scal.p + 2);
+      double hs[3];
+      CK(cudaMemcpyAsync(hs, ctx->scal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      eta = P.eta0 > 0.0 ? P.eta0 : (hs[0] > 0.0 ? 1.0 / hs[0] : 1.0);
+      if (P.omega0 > 0.0) omega = P.omega0;
+      else if (hs[1] > 0.0 && hs[2] > 0.0) omega = std::min(std::max(hs[1] / hs[2], 1e-4), 1e4);
+      else omega = 1.0;
+    }
+    C.eta = eta; C.eta_init = eta; C.omega = omega;
+    C.tau = eta / omega; C.sigma = eta * omega;
+    ctx->write_ctl();
+    ctx->cones_set = true;
+    // initial point z00 = (P_X(0), 0) (reading A4): average of a zero sum with W = 1
+    C.Wsum = 1.0;
+    ctx->write_ctl();
+    k_avg_elem<<<Gn, kThreads, 0, st>>>(n, ctx->ek.p, ctx->xsum.p, ctx->lt.p, ctx->ut.p, ctx->x.p, ctx->ctl);
+    C.Wsum = 0.0;
+    ctx->write_ctl();
+    CK(cudaGetLastError());
+    // anchor / products / e_anchor
+    reset_from_current(ctx);
+  });
+}
+
+pdcs_status pdcs_set_iterate(pdcs_ctx* ctx, const double* x, const double* y) {
+  if (!ctx) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
+    cudaStream_t st = ctx->st;
+    const int64_t n = ctx->n, m = ctx->m;
+    const cudaMemcpyKind kind = ctx->mem_kind == PDCS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (x) {
+      CK(cudaMemcpyAsync(ctx->tmpn.p, x, n * sizeof(double), kind, st));
+      k_ewise<<<grid_for(n, ctx->sms), kThreads, 0, st>>>(n, ctx->tmpn.p, ctx->q.p, 1, ctx->x.p);
+    }
+    if (y) {
+      CK(cudaMemcpyAsync(ctx->tmpm.p, y, m * sizeof(double), kind, st));
+      k_ewise<<<grid_for(m, ctx->sms), kThreads, 0, st>>>(m, ctx->tmpm.p, ctx->r.p, 1, ctx->y.p);
+    }
+    CK(cudaGetLastError());
+    reset_from_current(ctx);
+  });
+}
+
+static void finish_result(pdcs_ctx* ctx, pdcs_result_t* out, double secs) {
+  if (!out) return;
+  const Ctl& C = *ctx->hctl;
+  std::memset(out, 0, sizeof(*out));
+  out->status = C.status == ST_RUNNING ? PDCS_RUNNING : C.status;
+  out->kkt.err_p = C.best_kkt[0]; out->kkt.err_d = C.best_kkt[1]; out->kkt.err_gap = C.best_kkt[2];
+  out->kkt.pobj = C.best_kkt[3]; out->kkt.dobj = C.best_kkt[4];
+  out->iters = C.total; out->trials = C.trials; out->restarts = C.restarts;
+  out->eta = C.eta; out->omega = C.omega; out->beta = C.beta;
+  out->solve_seconds = secs;
+}
+
+// Host loop of Alg. 1 (v1: the accept flag is read back after each trial).
+static void run_steps(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, double time_limit) {
+  auto t0 = std::chrono::steady_clock::now();
+  for (int64_t s = 0; s < n_inner; ++s) {
+    for (;;) {
+      ctx->trial();
+      CK(cudaMemcpyAsync(ctx->hctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->st));
+      CK(cudaStreamSynchronize(ctx->st));
+      if (ctx->hctl->status != ST_RUNNING) fail(PDCS_ERR_NUMERICAL, "line search failed (eta underflow / too many rejects)");
+      if (ctx->hctl->accepted) break;
+    }
+    const bool chk = ctx->hctl->need_check;
+    ctx->accept();
+    if (chk) {
+      ctx->check();
+      if (stop_at_tol) {
+        ctx->read_ctl();
+        if (ctx->hctl->done) { ctx->hctl->status = ST_OPTIMAL; ctx->write_ctl(); return; }
+        if (time_limit > 0 &&
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > time_limit) {
+          ctx->hctl->status = ST_TIME; ctx->write_ctl(); return;
+        }
+      }
+    }
+  }
+}
+
+pdcs_status pdcs_iterate(pdcs_ctx* ctx, int64_t n_inner, pdcs_result_t* out) {
+  if (!ctx) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
+    if (n_inner < 0) fail(PDCS_ERR_ARG, "n_inner < 0");
+    ctx->launches = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    run_steps(ctx, n_inner, false, 0.0);
+    ctx->flush_timing();
+    ctx->read_ctl();
+    finish_result(ctx, out, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  });
+}
+
+pdcs_status pdcs_solve(pdcs_ctx* ctx, pdcs_result_t* out) {
+  if (!ctx) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
+    auto t0 = std::chrono::steady_clock::now();
+    ctx->launches = 0;
+    const int64_t remaining = std::max<int64_t>(0, ctx->prm.max_iters - ctx->hctl->total);
+    try {
+      run_steps(ctx, remaining, true, ctx->prm.time_limit_s);
+    } catch (const StatusErr& e) {
+      if (e.st != PDCS_ERR_NUMERICAL) throw;
+      ctx->read_ctl();
+      ctx->hctl->status = ST_NUMERICAL;
+      ctx->write_ctl();
+    }
+    ctx->flush_timing();
+    ctx->read_ctl();
+    if (ctx->hctl->status == ST_RUNNING) { ctx->hctl->status = ST_ITER; ctx->write_ctl(); }
+    finish_result(ctx, out, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  });
+}
+
+pdcs_status pdcs_kkt(pdcs_ctx* ctx, int which, pdcs_kkt_t* out) {
+  if (!ctx || !out) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
+    const double *xs, *ys;
+    switch (which) {
+      case PDCS_CURRENT: xs = ctx->x.p; ys = ctx->y.p; break;
+      case PDCS_PDHG_OUT: xs = ctx->xh.p; ys = ctx->yh.p; break;
+      case PDCS_ANCHOR: xs = ctx->x0.p; ys = ctx->y0.p; break;
+      case PDCS_BEST: xs = ctx->bx.p; ys = ctx->by.p; break;
+      case PDCS_CANDIDATE: xs = ctx->candx.p; ys = ctx->candy.p; break;
+      default: fail(PDCS_ERR_ARG, "bad which");
+    }
+    ctx->products(xs, ys, ctx->tmpm.p, ctx->tmpn.p);
+    KktCand c0{xs, ys, ctx->tmpm.p, ctx->tmpn.p, ctx->res0.p, ctx->lam0.p};
+    // finalize in evaluate mode writes kkt[0]; keep the rest of the control block
+    ctx->read_ctl();
+    Ctl saved = *ctx->hctl;
+    ctx->kkt_launch(c0, c0, 1, 0);
+    ctx->read_ctl();
+    out->err_p = ctx->hctl->kkt[0][0]; out->err_d = ctx->hctl->kkt[0][1]; out->err_gap = ctx->hctl->kkt[0][2];
+    out->pobj = ctx->hctl->kkt[0][3]; out->dobj = ctx->hctl->kkt[0][4];
+    *ctx->hctl = saved;
+    ctx->write_ctl();
+  });
+}
+
+pdcs_status pdcs_get_iterate(pdcs_ctx* ctx, int which, int space, double* x, double* y) {
+  if (!ctx) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
+    const double *xs, *ys;
+    switch (which) {
+      case PDCS_CURRENT: xs = ctx->x.p; ys = ctx->y.p; break;
+      case PDCS_PDHG_OUT: xs = ctx->xh.p; ys = ctx->yh.p; break;
+      case PDCS_ANCHOR: xs = ctx->x0.p; ys = ctx->y0.p; break;
+      case PDCS_BEST: xs = ctx->bx.p; ys = ctx->by.p; break;
+      case PDCS_CANDIDATE: xs = ctx->candx.p; ys = ctx->candy.p; break;
+      default: fail(PDCS_ERR_ARG, "bad which");
+    }
+    cudaStream_t st = ctx->st;
+    const int64_t n = ctx->n, m = ctx->m;
+    const double* xo = xs;
+    const double* yo = ys;
+    if (space == PDCS_ORIGINAL) {
+      k_ewise<<<grid_for(n, ctx->sms), kThreads, 0, st>>>(n, xs, ctx->q.p, 0, ctx->tmpn.p);
+      k_ewise<<<grid_for(m, ctx->sms), kThreads, 0, st>>>(m, ys, ctx->r.p, 0, ctx->tmpm.p);
+      CK(cudaGetLastError());
+      xo = ctx->tmpn.p;
+      yo = ctx->tmpm.p;
+    } else if (space != PDCS_SCALED) {
+      fail(PDCS_ERR_ARG, "bad space");
+    }
+    const cudaMemcpyKind kind = ctx->mem_kind == PDCS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (x && n) CK(cudaMemcpyAsync(x, xo, n * sizeof(double), kind, st));
+    if (y && m) CK(cudaMemcpyAsync(y, yo, m * sizeof(double), kind, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+pdcs_status pdcs_get_state(pdcs_ctx* ctx, double* x, double* y, double* x0, double* y0, double* xsum,
+                           double* ysum, double* sc) {
+  if (!ctx) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
+    const cudaMemcpyKind kind = ctx->mem_kind == PDCS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const int64_t n = ctx->n, m = ctx->m;
+    auto get = [&](double* dst, const DBuf<double>& src, int64_t cnt) {
+      if (dst && cnt) CK(cudaMemcpyAsync(dst, src.p, cnt * sizeof(double), kind, ctx->st));
+    };
+    get(x, ctx->x, n); get(y, ctx->y, m); get(x0, ctx->x0, n); get(y0, ctx->y0, m);
+    get(xsum, ctx->xsum, n); get(ysum, ctx->ysum, m);
+    ctx->read_ctl();
+    if (sc) {
+      const Ctl& C = *ctx->hctl;
+      const double v[13] = {C.eta, C.eta_init, C.omega, C.beta, C.Wsum, C.r_start, C.e_anchor, C.e_prev,
+                            C.best_e, (double)C.k, (double)C.total, (double)C.trials, (double)C.restarts};
+      std::memcpy(sc, v, sizeof(v));
+    }
+  });
+}
+
+pdcs_status pdcs_set_state(pdcs_ctx* ctx, const double* x, const double* y, const double* x0,
+                           const double* y0, const double* xsum, const double* ysum, const double* sc) {
+  if (!ctx || !x || !y || !x0 || !y0 || !xsum || !ysum || !sc) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
+    const cudaMemcpyKind kind = ctx->mem_kind == PDCS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const int64_t n = ctx->n, m = ctx->m;
+    cudaStream_t st = ctx->st;
+    auto put = [&](DBuf<double>& dst, const double* src, int64_t cnt) {
+      if (cnt) CK(cudaMemcpyAsync(dst.p, src, cnt * sizeof(double), kind, st));
+    };
+    put(ctx->x, x, n); put(ctx->y, y, m); put(ctx->x0, x0, n); put(ctx->y0, y0, m);
+    put(ctx->xsum, xsum, n); put(ctx->ysum, ysum, m);
+    ctx->products(ctx->x.p, ctx->y.p, ctx->kxh.p, ctx->kty.p);
+    auto cp = [&](double* d, const double* s_, int64_t cnt) {
+      if (cnt) CK(cudaMemcpyAsync(d, s_, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    };
+    cp(ctx->xh.p, ctx->x.p, n); cp(ctx->yh.p, ctx->y.p, m);
+    cp(ctx->ktyh.p, ctx->kty.p, n);
+    ctx->read_ctl();
+    Ctl& C = *ctx->hctl;
+    C.eta = sc[0]; C.eta_init = sc[1]; C.omega = sc[2]; C.beta = sc[3]; C.Wsum = sc[4]; C.r_start = sc[5];
+    C.e_anchor = sc[6]; C.e_prev = sc[7]; C.best_e = sc[8]; C.k = (int64_t)sc[9]; C.total = (int64_t)sc[10];
+    C.trials = (int64_t)sc[11]; C.restarts = (int64_t)sc[12];
+    C.tau = C.eta / C.omega; C.sigma = C.eta * C.omega;
+    C.status = ST_RUNNING; C.rejects = 0; C.accepted = 0; C.need_check = 0; C.store_kty = 0;
+    ctx->write_ctl();
+  });
+}
+
+pdcs_status pdcs_get_scaling(pdcs_ctx* ctx, double* r, double* q) {
+  if (!ctx) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
+    const cudaMemcpyKind kind = ctx->mem_kind == PDCS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (r && ctx->m) CK(cudaMemcpyAsync(r, ctx->r.p, ctx->m * sizeof(double), kind, ctx->st));
+    if (q && ctx->n) CK(cudaMemcpyAsync(q, ctx->q.p, ctx->n * sizeof(double), kind, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+  });
+}
+
+void pdcs_enable_timing(pdcs_ctx* ctx, int on) {
+  if (!ctx) return;
+  ctx->timing = on != 0;
+  ctx->ktimes.clear();
+}
+
+int pdcs_kernel_times(pdcs_ctx* ctx, char (*names)[32], double* ms, int64_t* launches, int cap) {
+  if (!ctx) return 0;
+  int i = 0;
+  for (auto& kv : ctx->ktimes) {
+    if (i >= cap) break;
+    if (names) { std::strncpy(names[i], kv.first.c_str(), 31); names[i][31] = 0; }
+    if (ms) ms[i] = kv.second.first;
+    if (launches) launches[i] = kv.second.second;
+    ++i;
+  }
+  return i;
+}
+
+int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
+  if (!ctx || !out || !ctx->ctl) return 0;
+  if (guard(ctx, [&] { ctx->read_ctl(); }) != PDCS_OK) return 0;
+  const Ctl& C = *ctx->hctl;
+  double v[26] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
+                  (double)C.restarts, C.e_anchor, C.Wsum, C.eta_init,
+                  C.kkt[0][0], C.kkt[0][1], C.kkt[0][2], C.kkt[0][3], C.kkt[0][4],
+                  C.kkt[1][0], C.kkt[1][1], C.kkt[1][2], C.kkt[1][3], C.kkt[1][4],
+                  C.e_prev, C.best_e, (double)C.use_avg, (double)C.restart, C.last_num, C.last_cross};
+  const int k = std::min(cap, 26);
+  for (int i = 0; i < k; ++i) out[i] = v[i];
+  return k;
+}
+
+int64_t pdcs_launch_count(const pdcs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void pdcs_destroy(pdcs_ctx* ctx) { delete ctx; }
+
+pdcs_status pdcs_nccl_unique_id(void* out128) {
+  if (!out128) return PDCS_ERR_ARG;
+  g_create_error = "NCCL support is not compiled into this build";
+  return PDCS_ERR_NCCL;
+}
+
+}  // extern "C"

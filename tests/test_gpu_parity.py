@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (C ABI, libpdcs.so) vs the CPU oracle (-m gpu).
+
+Tolerance (BASELINE.json north_star): per iterate, on scaled iterates,
+    max(|x_g - x_o|_inf / (1 + |x_o|_inf), |y_g - y_o|_inf / (1 + |y_o|_inf)) <= 1e-9
+(fp64; reduction order, FMA contraction and the root-finder method differ).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from instances import gen_fisher, gen_lasso, gen_mixed, gen_mpo, EXP, DUAL_EXP, SOC, RSOC
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+# eta, omega, W are functions of differences dz = z^ - z; near convergence
+# |dz|/|z| ~ 1e-5, so a 1e-14 iterate difference moves them by ~1e-9 relative
+# (condition number |z|/|dz|).  They are compared at STOL (reading P2).
+STOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2505_00311_b200 import build
+    build.build()
+    import paper_2505_00311_b200 as P
+    return P
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / (1.0 + np.max(np.abs(b))) if a.size else 0.0
+
+
+def parity(xg, yg, xo, yo):
+    return max(rel(xg, xo), rel(yg, yo))
+
+
+def mixed(seed, m=300, n1=60, n2=150, **kw):
+    return gen_mixed(m, n1, n2, seed=seed, **kw)
+
+
+# ------------------------------------------------------------------ setup parity
+@pytest.mark.parametrize("make", [lambda: gen_lasso(100, 50, 1.0, dense=True),
+                                  lambda: mixed(1), lambda: gen_fisher(30, 20, seed=1),
+                                  lambda: gen_mpo(2, 15, seed=1)])
+def test_scaling_parity(P, make):
+    prog = make()
+    g = P.PdcsSolver(prog)
+    o = O.OracleSolver(prog)
+    rg, qg = g.get_scaling()
+    ro, qo = o.get_scaling()
+    np.testing.assert_allclose(rg, ro, rtol=1e-13)
+    np.testing.assert_allclose(qg, qo, rtol=1e-13)
+
+
+# ------------------------------------------------------------------ one step from random points
+@pytest.mark.parametrize("seed", range(4))
+def test_one_step_random_point_all_cones(P, seed):
+    """One Eq. 5 step from a random point: exercises every projection kernel
+    (box, R+, zero, rescaled SOC/RSOC, exp, dual exp; thread/warp/CTA teams)."""
+    prog = mixed(seed, m=600, n1=80, n2=400, soc_dims=(3, 300), scale_spread=1.5)
+    rng = np.random.default_rng(seed)
+    g = P.PdcsSolver(prog)
+    o = O.OracleSolver(prog)
+    ro, qo = o.get_scaling()
+    for _ in range(3):
+        x = rng.standard_normal(prog.n) * 3
+        y = rng.standard_normal(prog.m) * 3
+        g.set_iterate(x, y)               # original space
+        o.set_iterate(x * qo, y * ro)     # oracle takes scaled space
+        g.iterate(1)
+        o.iterate(1)
+        xg, yg = g.get_iterate(P.PDHG_OUT)
+        xo, yo = o.get_iterate(1)
+        assert parity(xg, yg, xo, yo) <= 1e-12, parity(xg, yg, xo, yo)
+
+
+# ------------------------------------------------------------------ multi-step parity
+@pytest.mark.parametrize("name,make,steps", [
+    ("tiny_lasso", lambda: gen_lasso(100, 50, 1.0, dense=True), 500),
+    ("mixed", lambda: mixed(5), 400),
+    ("fisher", lambda: gen_fisher(40, 30, seed=2), 400),
+])
+def test_vanilla_parity(P, name, make, steps):
+    """Vanilla PDHG (decision-free) per-iterate parity."""
+    prog = make()
+    g = P.PdcsSolver(prog, vanilla_pdhg=1)
+    o = O.OracleSolver(prog, vanilla_pdhg=1)
+    worst = 0.0
+    for chunk in range(steps // 100):
+        g.iterate(100)
+        o.iterate(100)
+        xg, yg = g.get_iterate(P.CURRENT)
+        xo, yo = o.get_iterate(0)
+        worst = max(worst, parity(xg, yg, xo, yo))
+    assert worst <= TOL, worst
+
+
+def _free_running(P, prog, steps, every=40):
+    """Both implementations from the same start, no resets."""
+    g = P.PdcsSolver(prog)
+    o = O.OracleSolver(prog)
+    worst = []
+    for done in range(0, steps, every):
+        rg = g.iterate(every)
+        o.iterate(every)
+        xg, yg = g.get_iterate(P.CURRENT)
+        xo, yo = o.get_iterate(0)
+        worst.append(parity(xg, yg, xo, yo))
+        so = o.scalars()
+        assert rg["restarts"] == so["restarts"] and rg["trials"] == so["trials"], (done, rg, so)
+    return worst
+
+
+def _shadow(P, prog, steps, seg=10):
+    """Checkpoint shadowing: at every check-interval
+    boundary of the oracle's trajectory (every `seg` accepted iterations; every
+    4th segment ends on an Eq. 9 check, restart and primal-weight decision) the
+    GPU is loaded with the oracle's exact state (pdcs_set_state) and both run one
+    segment.  Every segment must agree to TOL."""
+    g = P.PdcsSolver(prog)
+    o = O.OracleSolver(prog)
+    worst = 0.0
+    for s in range(0, steps, seg):
+        st = o.get_state()
+        g.set_state(st)
+        g.iterate(seg)
+        o.iterate(seg)
+        xg, yg = g.get_iterate(P.CURRENT)
+        xo, yo = o.get_iterate(0)
+        worst = max(worst, parity(xg, yg, xo, yo))
+        sg, so = g.get_state(), o.get_state()
+        # decisions exact (k, total, trials, restarts, beta); eta/omega/W to STOL
+        assert np.array_equal(sg["sc"][9:], so["sc"][9:]), (s, sg["sc"], so["sc"])
+        assert sg["sc"][3] == so["sc"][3], (s, sg["sc"], so["sc"])
+        for i in (0, 2, 4):
+            assert abs(sg["sc"][i] - so["sc"][i]) <= STOL * abs(so["sc"][i]), (s, i, sg["sc"], so["sc"])
+        worst = max(worst, rel(sg["x0"], so["x0"]), rel(sg["y0"], so["y0"]))
+        if so["sc"][4] > 0:   # the average z = sum eta z / sum eta (Alg. 1 line 7)
+            worst = max(worst, rel(sg["xsum"] / sg["sc"][4], so["xsum"] / so["sc"][4]),
+                        rel(sg["ysum"] / sg["sc"][4], so["ysum"] / so["sc"][4]))
+    return worst
+
+
+def test_pdcs_parity_tiny_lasso_2000(P):
+    """BASELINE configs[0]: tiny Lasso SOCP 100x50 dense, fixed 2000 accepted PDHG
+    iterations.  PDCS amplifies rounding (tests/test_sensitivity.py), so the
+    2000-step comparison is made segment by segment from the oracle's state; the
+    free-running comparison is held to TOL over the first 200 iterations."""
+    prog = gen_lasso(100, 50, 1.0, seed=0, dense=True)
+    worst = _shadow(P, prog, 2000)
+    assert worst <= TOL, worst
+    free = _free_running(P, prog, 200)
+    assert max(free) <= TOL, free
+
+
+@pytest.mark.parametrize("name,make,steps", [
+    ("mixed", lambda: mixed(7), 800),
+    ("mixed_big_soc", lambda: mixed(8, m=800, n1=50, n2=600, soc_dims=(30, 400)), 400),
+    ("fisher", lambda: gen_fisher(40, 30, seed=3), 800),
+    ("mpo", lambda: gen_mpo(3, 20, seed=3), 800),
+])
+def test_pdcs_parity(P, name, make, steps):
+    prog = make()
+    worst = _shadow(P, prog, steps)
+    assert worst <= TOL, worst
+    free = _free_running(P, prog, 120)
+    assert max(free) <= TOL, free
+
+
+# ------------------------------------------------------------------ Eq. 9
+@pytest.mark.parametrize("seed", range(2))
+def test_kkt_parity_same_point(P, seed):
+    prog = mixed(20 + seed)
+    g = P.PdcsSolver(prog)
+    o = O.OracleSolver(prog)
+    rng = np.random.default_rng(seed)
+    ro, qo = o.get_scaling()
+    x = prog.x_star + 0.01 * rng.standard_normal(prog.n)
+    y = prog.y_star + 0.01 * rng.standard_normal(prog.m)
+    g.set_iterate(x, y)
+    o.set_iterate(x * qo, y * ro)
+    kg = g.kkt(P.CURRENT)
+    ko = o.kkt(0)
+    for key in ("err_p", "err_d", "err_gap", "pobj", "dobj"):
+        assert abs(kg[key] - ko[key]) <= 1e-12 * (1 + abs(ko[key])), (key, kg, ko)
+    # at the planted optimum all three vanish
+    g.set_iterate(prog.x_star, prog.y_star)
+    k = g.kkt(P.CURRENT)
+    assert max(k["err_p"], k["err_d"], k["err_gap"]) < 1e-12
+
+
+# ------------------------------------------------------------------ solve
+def test_solve_tiny_lasso(P):
+    prog = gen_lasso(100, 50, 1.0, seed=0, dense=True)
+    g = P.PdcsSolver(prog, tol=1e-6)
+    r = g.solve()
+    assert r["status"] == "OPTIMAL"
+    assert max(r["err_p"], r["err_d"], r["err_gap"]) <= 1e-6
+    ro = O.OracleSolver(prog, tol=1e-6).solve()
+    assert abs(r["pobj"] - ro.kkt.pobj) <= 1e-5 * abs(ro.kkt.pobj)
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_solve_planted_mixed(P, seed):
+    prog = mixed(30 + seed, m=400, n1=60, n2=200)
+    g = P.PdcsSolver(prog, tol=1e-8, max_iters=200000)
+    r = g.solve()
+    assert r["status"] == "OPTIMAL"
+    assert abs(r["pobj"] - prog.obj_star) <= 1e-6 * (1 + abs(prog.obj_star))
+
+
+def test_solve_fisher_and_mpo(P):
+    for prog, tol in ((gen_fisher(50, 40, seed=4), 1e-6), (gen_mpo(3, 30, seed=4), 1e-6)):
+        g = P.PdcsSolver(prog, tol=tol, max_iters=200000)
+        r = g.solve()
+        assert r["status"] == "OPTIMAL", r
+        assert max(r["err_p"], r["err_d"], r["err_gap"]) <= tol
+
+
+# ------------------------------------------------------------------ boundary errors
+def test_create_errors(P):
+    prog = gen_lasso(10, 5, 1.0, dense=True)
+    bad = prog.vals.copy()
+    bad[3] = np.nan
+    import copy
+    p2 = copy.copy(prog)
+    p2.vals = bad
+    with pytest.raises(P.PdcsError) as e:
+        P.PdcsSolver(p2)
+    assert e.value.code == 4
+    p3 = copy.copy(prog)
+    p3.l = prog.l.copy()
+    p3.u = prog.u.copy()
+    p3.l[0], p3.u[0] = 1.0, 0.0
+    with pytest.raises(P.PdcsError) as e:
+        P.PdcsSolver(p3)
+    assert e.value.code == 3
+    p4 = copy.copy(prog)
+    p4.pdim = prog.pdim + 1
+    with pytest.raises(P.PdcsError) as e:
+        P.PdcsSolver(p4)
+    assert e.value.code == 5
+    p5 = copy.copy(prog)
+    p5.pk = np.array([EXP], np.int32)
+    with pytest.raises(P.PdcsError) as e:
+        P.PdcsSolver(p5)
+    assert e.value.code == 5
+
+
+def test_empty_and_degenerate(P):
+    """Zero-nnz rows / columns, and an instance whose optimum is the origin."""
+    from instances import ConicProgram, ZERO, NONNEG
+    prog = ConicProgram(m=3, n=3, n1=3, row_ptr=np.array([0, 0, 1, 1], np.int64),
+                        col_idx=np.array([1], np.int32), vals=np.array([2.0]), c=np.array([1.0, 1.0, 0.0]),
+                        h=np.array([0.0, 0.0, 0.0]), l=np.zeros(3), u=np.full(3, np.inf),
+                        pk=np.zeros(0, np.int32), pdim=np.zeros(0, np.int64),
+                        rk=np.array([NONNEG], np.int32), rdim=np.array([3], np.int64))
+    g = P.PdcsSolver(prog, tol=1e-8)
+    r = g.solve()
+    assert r["status"] == "OPTIMAL" and abs(r["pobj"]) < 1e-8

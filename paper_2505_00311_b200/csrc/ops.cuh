@@ -17,8 +17,8 @@ __global__ void __launch_bounds__(kThreads) k_primal_elem(int64_t n, const uint8
                                                           const double* __restrict__ kty,
                                                           const double* __restrict__ lt,
                                                           const double* __restrict__ ut,
-                                                          double* __restrict__ xh, const Ctl* ctl,
-                                                          double* part, int64_t slot0) {
+                                                          double* __restrict__ xh, double2* __restrict__ xx,
+                                                          const Ctl* ctl, double* part, int64_t slot0) {
   if (ctl->status != ST_RUNNING) return;
   const double tau = ctl->tau;
   Acc<kAcc> acc; acc.zero();
@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(kThreads) k_primal_elem(int64_t n, const uint8
     const double v = xj - tau * (c[j] - kty[j]);
     const double p = box_proj(k, v, lt, ut, j);
     xh[j] = p;
+    xx[j] = make_double2(p, xj);
     const double d = p - xj;
     acc.v[0] += d * d;
   }
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kThreads) k_decide(const double* __restrict__ 
 // Accumulates ||y^ - y||^2 and <y^ - y, K x^ - K x> (line search).
 struct EpiDualTrial {
   static constexpr int NA = kAcc;
-  static constexpr int NX = 2;
+  static constexpr int NX = 3;   // gathers the interleaved (x^_j, x_j) pairs
   const double *y, *h;
   const uint8_t* rk;
   double *kxh, *kxd, *yh;

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <string>
@@ -94,6 +95,7 @@ struct pdcs_ctx {
   DBuf<double> x, xh, x0, xsum, kty, ktyh, xa, ktya, bx, candx, lam0, lam1, onesn;
   DBuf<double> y, yh, y0, ysum, kxh, kxd, ya, kxa, by, candy, res0, res1, onesm;
   DBuf<double> tmpn, tmpm, scal;
+  DBuf<double2> xx;                            // interleaved (x^_j, x_j)
   DBuf<uint8_t> ek, rk;
   DBuf<Block> pblocks, rblocks;
   DBuf<int64_t> rsoc_offs_p, rsoc_offs_r;
@@ -188,7 +190,7 @@ struct pdcs_ctx {
     BlockArgs A{};
     A.blocks = primal ? pblocks.p : rblocks.p;
     A.op = op;
-    A.x = x.p; A.c = ct.p; A.kty = kty.p; A.xh = xh.p;
+    A.x = x.p; A.c = ct.p; A.kty = kty.p; A.xh = xh.p; A.xx = xx.p;
     A.D = primal ? q.p : r.p;
     A.y = y.p; A.yh = yh.p; A.kxd = kxd.p;
     return A;
@@ -206,11 +208,8 @@ struct pdcs_ctx {
       const int g = cl[c].grid;
       if (c == 0) launch("blocks_thread", [&] { k_blocks_thread<<<g, kThreads, 0, st>>>(B, ctl); });
       else if (c == 1) launch("blocks_warp", [&] { k_blocks_warp<<<g, kThreads, 0, st>>>(B, ctl); });
-      else if (c == 2 || kkt || A.op == BOP_AVG_PRIMAL || A.op == BOP_AVG_DUAL) {
-        // KKT / average passes use the CTA team for giant blocks as well
-        const int gg = c == 3 ? (int)std::min<int64_t>(cl[c].count, sms) : g;
-        if (c == 3) { B.slot0 = kkt ? cl[c].kslot[cand] : cl[c].slot; }
-        launch("blocks_cta", [&] { k_blocks_cta<<<gg, kThreads, 0, st>>>(B, ctl); });
+      else if (c == 2) {
+        launch("blocks_cta", [&] { k_blocks_cta<<<g, kThreads, 0, st>>>(B, ctl); });
       } else {
         double* gb = gbuf.p;
         const Ctl* cp = ctl;
@@ -226,12 +225,12 @@ struct pdcs_ctx {
   // One trial of AdaptiveStepPDHG (PDHG step Eq. 5 + accept test).
   void trial() {
     launch("primal_elem", [&] {
-      k_primal_elem<<<g_pe, kThreads, 0, st>>>(n, ek.p, x.p, ct.p, kty.p, lt.p, ut.p, xh.p, ctl, tpart.p,
-                                               slot_pe);
+      k_primal_elem<<<g_pe, kThreads, 0, st>>>(n, ek.p, x.p, ct.p, kty.p, lt.p, ut.p, xh.p, xx.p, ctl,
+                                               tpart.p, slot_pe);
     });
     run_blocks(true, bargs(true, BOP_TRIAL_PRIMAL), false, 0);
     EpiDualTrial e{y.p, ht.p, rk.p, kxh.p, kxd.p, yh.p, 0.0, 0};
-    spmv("spmv_K_dual", K, xh.p, x.p, e, tpart.p, slot_spmv);
+    spmv("spmv_K_dual", K, reinterpret_cast<const double*>(xx.p), nullptr, e, tpart.p, slot_spmv);
     run_blocks(false, bargs(false, BOP_TRIAL_DUAL), false, 0);
     launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl); });
   }
@@ -271,10 +270,8 @@ struct pdcs_ctx {
     for (int side = 0; side < 2; ++side) {
       BClass* cl = side ? pcls : rcls;
       for (int c = 0; c < 4; ++c)
-        if (cl[c].count) {
-          const int g = c == 3 ? (int)std::min<int64_t>(cl[c].count, sms) : cl[c].grid;
-          CK(cudaMemsetAsync(kpart.p + cl[c].kslot[1] * kKAcc, 0, (size_t)g * kKAcc * sizeof(double), st));
-        }
+        if (cl[c].count)
+          CK(cudaMemsetAsync(kpart.p + cl[c].kslot[1] * kKAcc, 0, (size_t)cl[c].grid * kKAcc * sizeof(double), st));
     }
   }
   // Eq. 9 check every check_interval accepted iterations.
@@ -318,12 +315,21 @@ struct pdcs_ctx {
   void build_plan(DevCsr& A, const std::vector<int64_t>& ptr, std::vector<int32_t>& rowstore,
                   std::vector<size_t>& offs) {
     const int64_t rows = (int64_t)ptr.size() - 1;
-    // V classes: 1 (<=2), 4 (<=8), 8 (<=16), 16 (<=32), 32 (<=4096), 0 (>4096)
+    // V classes: 1, 4, 8, 16, 32 lanes per row, 0 = one CTA per row.  Upper
+    // row-length bounds per class (PDCS_SPMV_BINS="b1,b4,b8,b16,b32" overrides).
     const int Vs[kMaxClasses] = {1, 4, 8, 16, 32, 0};
+    int64_t bound[5] = {2, 12, 48, 96, (int64_t)1 << 40};   // measured on B200 (profiles/)
+    if (const char* env = std::getenv("PDCS_SPMV_BINS")) {
+      int64_t b[5];
+      if (std::sscanf(env, "%ld,%ld,%ld,%ld,%ld", &b[0], &b[1], &b[2], &b[3], &b[4]) == 5)
+        for (int i = 0; i < 5; ++i) bound[i] = b[i];
+    }
     std::vector<int64_t> lists[kMaxClasses];
     for (int64_t i = 0; i < rows; ++i) {
       const int64_t L = ptr[i + 1] - ptr[i];
-      int c = L <= 2 ? 0 : L <= 8 ? 1 : L <= 16 ? 2 : L <= 32 ? 3 : L <= 4096 ? 4 : 5;
+      int c = 5;
+      for (int k = 0; k < 5; ++k)
+        if (L <= bound[k]) { c = k; break; }
       lists[c].push_back(i);
     }
     SpmvPlan P{};
@@ -580,6 +586,13 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
     upload(ctx->planrows, rowstore, st);
     ctx->patch_plan(ctx->K);
     ctx->patch_plan(ctx->KT);
+    // ---- L1 / shared-memory split for the gathering kernels (PDCS_CARVEOUT, % smem)
+    if (const char* env = std::getenv("PDCS_CARVEOUT")) {
+      const int pc = std::atoi(env);
+      CK(cudaFuncSetAttribute(spmv_kernel<EpiDualTrial>, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
+      CK(cudaFuncSetAttribute(spmv_kernel<EpiHalpernX>, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
+      CK(cudaFuncSetAttribute(spmv_kernel<EpiStore>, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
+    }
     // ---- control block
     CK(cudaMalloc(&ctx->ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&ctx->hctl, sizeof(Ctl)));
@@ -697,7 +710,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
         for (int c = 0; c < 4; ++c)
           if (cl[c].count) {
             cl[c].kslot[cand] = ks;
-            ks += c == 3 ? (int)std::min<int64_t>(cl[c].count, ctx->sms) : cl[c].grid;
+            ks += cl[c].grid;
           }
       }
     ctx->nslot_kkt = ks;
@@ -715,6 +728,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
                     &ctx->ktyh, &ctx->xa, &ctx->ktya, &ctx->bx, &ctx->candx, &ctx->lam0,
                     &ctx->lam1, &ctx->tmpn})
       b->alloc(std::max<int64_t>(n, 1));
+    ctx->xx.alloc(std::max<int64_t>(n, 1));
     ctx->lt.alloc(std::max<int64_t>(n1, 1));
     ctx->ut.alloc(std::max<int64_t>(n1, 1));
     ctx->scal.alloc(8);

@@ -4,7 +4,8 @@
 // PDCS.  Rows are binned by length at setup (SpmvPlan):
 //   V = 1            one thread per row         (rows of <= 2 nnz)
 //   V = 4, 8, 16, 32 V lanes per row, segmented shuffle reduction (warp-
-//                    segmented rows; 32/V rows per warp)
+//                    segmented rows; 32/V rows per warp).  Thresholds are
+//                    set at setup (PDCS_SPMV_BINS overrides them for tuning).
 //   V = 0            one CTA per row (rows of > 4096 nnz)
 // Matrix values / column ids are streamed with evict-first loads; the
 // gathered vector goes through the read-only path and stays in L2.  Each CTA
@@ -46,50 +47,75 @@ __device__ __forceinline__ void cta_write_partials(Acc<NA>& a, double* part, int
   }
 }
 
-__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
-__device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
+// Streaming loads of the matrix (read once per pass): no L1 allocation, so the
+// L1 keeps the gathered vector(s).
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 
 // Dot products of one row with V lanes (lane in [0, V)) against NX gathered
-// vectors (x1, and x2 when NX == 2: K x^ and K x share one sweep over the row).
-// Results valid in all lanes of the group.
+// vectors: NX == 1 x1; NX == 2 x1 and x2; NX == 3 x1 holds interleaved pairs
+// (x^_j, x_j) so that K x^ and K x share one sweep and one 16-byte gather.
+// Software-pipelined: the column ids / values of chunk i+1 are in flight while
+// chunk i's gathers are served; tails are predicated.  Results valid in all
+// lanes of the group.
 template <int V, int NX>
 __device__ __forceinline__ void row_dot(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                                         const double* __restrict__ val, const double* __restrict__ x1,
                                         const double* __restrict__ x2, int64_t row, int lane, double& s1,
                                         double& s2) {
+  constexpr int U = 4;
   s1 = 0.0;
   s2 = 0.0;
   if (row >= 0) {
     const int32_t b = __ldg(ptr + row), e = __ldg(ptr + row + 1);
     int32_t p = b + lane;
-    for (; p + 3 * V < e; p += 4 * V) {
-      const int32_t c0 = ld_stream(col + p), c1 = ld_stream(col + p + V);
-      const int32_t c2 = ld_stream(col + p + 2 * V), c3 = ld_stream(col + p + 3 * V);
-      const double a0 = ld_stream(val + p), a1 = ld_stream(val + p + V);
-      const double a2 = ld_stream(val + p + 2 * V), a3 = ld_stream(val + p + 3 * V);
-      s1 += a0 * __ldg(x1 + c0);
-      s1 += a1 * __ldg(x1 + c1);
-      s1 += a2 * __ldg(x1 + c2);
-      s1 += a3 * __ldg(x1 + c3);
-      if (NX == 2) {
-        s2 += a0 * __ldg(x2 + c0);
-        s2 += a1 * __ldg(x2 + c1);
-        s2 += a2 * __ldg(x2 + c2);
-        s2 += a3 * __ldg(x2 + c3);
-      }
+    int32_t c[U];
+    double a[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int32_t q = p + k * V;
+      c[k] = q < e ? ld_stream(col + q) : -1;
+      a[k] = q < e ? ld_stream(val + q) : 0.0;
     }
-    for (; p < e; p += V) {
-      const double a = ld_stream(val + p);
-      const int32_t c = ld_stream(col + p);
-      s1 += a * __ldg(x1 + c);
-      if (NX == 2) s2 += a * __ldg(x2 + c);
+    for (; p < e; p += U * V) {
+      int32_t cn[U];
+      double an[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int32_t q = p + (U + k) * V;
+        cn[k] = q < e ? ld_stream(col + q) : -1;
+        an[k] = q < e ? ld_stream(val + q) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (c[k] >= 0) {
+          if (NX == 3) {   // interleaved pair: one 16-byte gather serves both products
+            const double2 v = __ldg(reinterpret_cast<const double2*>(x1) + c[k]);
+            s1 += a[k] * v.x;
+            s2 += a[k] * v.y;
+          } else {
+            s1 += a[k] * __ldg(x1 + c[k]);
+            if (NX == 2) s2 += a[k] * __ldg(x2 + c[k]);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) { c[k] = cn[k]; a[k] = an[k]; }
     }
   }
-  if (V > 1) {
+  if (V > 1 && V <= 32) {
 #pragma unroll
     for (int o = V / 2; o >= 1; o >>= 1) {
       s1 += __shfl_xor_sync(0xffffffffu, s1, o, V);
-      if (NX == 2) s2 += __shfl_xor_sync(0xffffffffu, s2, o, V);
+      if (NX >= 2) s2 += __shfl_xor_sync(0xffffffffu, s2, o, V);
     }
   }
 }
@@ -126,35 +152,12 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(const int32_t* __restric
     __shared__ double red[2][kThreads / 32];
     for (int64_t idx = lcta; idx < K.nrows; idx += K.ncta) {
       const int64_t row = rowid(idx);
-      const int32_t b = __ldg(ptr + row), e = __ldg(ptr + row + 1);
-      double s1 = 0.0, s2 = 0.0;
-      int32_t p = b + threadIdx.x;
-      for (; p + 3 * kThreads < e; p += 4 * kThreads) {
-        const int32_t c0 = ld_stream(col + p), c1 = ld_stream(col + p + kThreads);
-        const int32_t c2 = ld_stream(col + p + 2 * kThreads), c3 = ld_stream(col + p + 3 * kThreads);
-        const double a0 = ld_stream(val + p), a1 = ld_stream(val + p + kThreads);
-        const double a2 = ld_stream(val + p + 2 * kThreads), a3 = ld_stream(val + p + 3 * kThreads);
-        s1 += a0 * __ldg(x1 + c0);
-        s1 += a1 * __ldg(x1 + c1);
-        s1 += a2 * __ldg(x1 + c2);
-        s1 += a3 * __ldg(x1 + c3);
-        if (NX == 2) {
-          s2 += a0 * __ldg(x2 + c0);
-          s2 += a1 * __ldg(x2 + c1);
-          s2 += a2 * __ldg(x2 + c2);
-          s2 += a3 * __ldg(x2 + c3);
-        }
-      }
-      for (; p < e; p += kThreads) {
-        const double a = ld_stream(val + p);
-        const int32_t cc = ld_stream(col + p);
-        s1 += a * __ldg(x1 + cc);
-        if (NX == 2) s2 += a * __ldg(x2 + cc);
-      }
+      double s1, s2;
+      row_dot<kThreads, NX>(ptr, col, val, x1, x2, row, threadIdx.x, s1, s2);
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) {
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        if (NX == 2) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        if (NX >= 2) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       }
       if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = s1; red[1][threadIdx.x >> 5] = s2; }
       __syncthreads();
@@ -173,7 +176,26 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(const int32_t* __restric
       row_dot<1, NX>(ptr, col, val, x1, x2, row, 0, s1, s2);
       epi.row(row, s1, s2, acc);
     }
+  } else if (K.V >= 8) {
+    // V lanes per row, epilogue run directly by the group leader (matrix bytes
+    // per row >> epilogue bytes, so no staging / barriers are needed).
+    const int V = K.V;
+    const int G = kThreads / V;                  // row groups per CTA
+    const int g = threadIdx.x / V, lane = threadIdx.x % V;
+    for (int64_t ib = (int64_t)lcta * G; ib < K.nrows; ib += (int64_t)K.ncta * G) {
+      const int64_t idx = ib + g;
+      const int64_t row = idx < K.nrows ? rowid(idx) : -1;
+      double s1, s2;
+      switch (V) {
+        case 8: row_dot<8, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
+        case 16: row_dot<16, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
+        default: row_dot<32, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
+      }
+      if (lane == 0 && row >= 0) epi.row(row, s1, s2, acc);
+    }
   } else {
+    // V = 4: short rows; dot products staged in shared memory so that the
+    // epilogue of consecutive rows is coalesced.
     const int V = K.V;
     const int R = kThreads / V;                  // rows per CTA iteration
     const int g = threadIdx.x / V, lane = threadIdx.x % V;
@@ -181,12 +203,7 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(const int32_t* __restric
       const int64_t idx = ib + g;
       const int64_t row = idx < K.nrows ? rowid(idx) : -1;
       double s1, s2;
-      switch (V) {
-        case 4: row_dot<4, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
-        case 8: row_dot<8, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
-        case 16: row_dot<16, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
-        default: row_dot<32, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
-      }
+      row_dot<4, NX>(ptr, col, val, x1, x2, row, lane, s1, s2);
       if (lane == 0) { sdot[0][g] = s1; sdot[1][g] = s2; srow[g] = row; }
       __syncthreads();
       if (threadIdx.x < R && srow[threadIdx.x] >= 0)

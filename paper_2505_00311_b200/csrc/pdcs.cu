@@ -20,6 +20,7 @@
 
 #include "../../include/pdcs.h"
 #include "ops.cuh"
+#include "tiled.cuh"
 
 using namespace pdcs;
 
@@ -62,10 +63,134 @@ struct DBuf {
   ~DBuf() { free_(); }
 };
 
+template <class T>
+void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
+  d.alloc(h.size());
+  if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
 int grid_for(int64_t n, int sms, int per_sm = 8) {
   int64_t g = (n + kThreads - 1) / kThreads;
   g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sms * per_sm));
   return (int)g;
+}
+
+// ---------------------------------------------------------------- tiled format builder
+// Host construction of the column-tiled format of tiled.cuh from a CSR
+// structure.  perm_* give the CSR position of every entry so that the (scaled)
+// values are gathered on the device afterwards.
+struct TiledHost {
+  std::vector<TWork> work;
+  std::vector<TChunk> chunk;
+  std::vector<TSeg> seg;
+  std::vector<int32_t> rowptr;
+  std::vector<uint16_t> col_s;
+  std::vector<int32_t> col_d;
+  std::vector<int32_t> perm_s, perm_d;
+  int64_t scratch = 0, staged = 0, nnz = 0;
+  int32_t T = 0, elem = 1;
+};
+
+// shared-memory tile size in bytes (PDCS_TILE_KB overrides; default 32 KB)
+int tiled_tile_bytes() {
+  static const int b = std::getenv("PDCS_TILE_KB") ? 1024 * std::atoi(std::getenv("PDCS_TILE_KB")) : 32768;
+  return b;
+}
+
+// lanes per row for a segment with `avg` nonzeros per row: aim for >= ~8 entries
+// per lane so that the unrolled, pipelined loop body is used (PDCS_TILE_LPE overrides)
+int pick_v(double avg) {
+  static const double lpe = std::getenv("PDCS_TILE_LPE") ? std::atof(std::getenv("PDCS_TILE_LPE")) : 4.0;
+  int v = 1;
+  while (v < 32 && avg >= 2.0 * v * lpe) v *= 2;
+  return v;
+}
+
+void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
+                 TiledHost& H) {
+  const int tile_bytes = tiled_tile_bytes();
+  const int32_t T = tile_bytes / (8 * elem);
+  const int64_t stage_min = tile_bytes / 32;           // staging beats direct gathers above this
+  // work-item size: enough items to fill the GPU several times over, no more
+  // partial groups per chunk than needed (PDCS_TILE_GROUP overrides)
+  const int64_t group_nz = std::getenv("PDCS_TILE_GROUP") ? std::atol(std::getenv("PDCS_TILE_GROUP"))
+                                                          : std::max<int64_t>(32768, ptr[rows] / 3000);
+  const int64_t ntiles = (nvec + T - 1) / T;
+  H.T = T;
+  H.elem = elem;
+  H.nnz = ptr[rows];
+  H.perm_s.reserve(H.nnz);
+  H.col_s.reserve(H.nnz);
+  std::vector<int64_t> cnt(ntiles, 0);
+  std::vector<int32_t> segof(ntiles, -1);
+  std::vector<int64_t> touched;
+  for (int64_t r0 = 0; r0 < rows; r0 += kTRows) {
+    const int32_t nr = (int32_t)std::min<int64_t>(kTRows, rows - r0);
+    touched.clear();
+    for (int64_t p = ptr[r0]; p < ptr[r0 + nr]; ++p) {
+      const int64_t t = col[p] / T;
+      if (cnt[t]++ == 0) touched.push_back(t);
+    }
+    std::sort(touched.begin(), touched.end());
+    // segments: direct first (if any), then staged tiles in order
+    std::vector<int64_t> staged_tiles;
+    int64_t direct_nz = 0;
+    for (int64_t t : touched) {
+      if (cnt[t] >= stage_min) staged_tiles.push_back(t); else direct_nz += cnt[t];
+    }
+    const int32_t s_begin = (int32_t)H.seg.size();
+    std::vector<int64_t> seg_nz;
+    if (direct_nz) { H.seg.push_back(TSeg{-1, 1, 0, 0}); seg_nz.push_back(direct_nz); }
+    for (int64_t t : staged_tiles) {
+      segof[t] = (int32_t)(H.seg.size() - s_begin);
+      H.seg.push_back(TSeg{(int32_t)t, 1, 0, 0});
+      seg_nz.push_back(cnt[t]);
+    }
+    const int nseg = (int)seg_nz.size();
+    // row pointers per segment
+    std::vector<int64_t> rpbase(nseg);
+    for (int k = 0; k < nseg; ++k) {
+      rpbase[k] = (int64_t)H.rowptr.size();
+      H.rowptr.resize(H.rowptr.size() + nr + 1, 0);
+      TSeg& S = H.seg[s_begin + k];
+      S.rp = rpbase[k];
+      S.V = pick_v((double)seg_nz[k] / nr);
+      S.nz = S.tile >= 0 ? (int64_t)H.col_s.size() : (int64_t)H.col_d.size();
+      if (S.tile >= 0) { H.col_s.resize(H.col_s.size() + seg_nz[k]); H.perm_s.resize(H.col_s.size()); }
+      else { H.col_d.resize(H.col_d.size() + seg_nz[k]); H.perm_d.resize(H.col_d.size()); }
+    }
+    auto seg_k = [&](int64_t t) { return cnt[t] >= stage_min ? segof[t] : 0; };   // direct is index 0
+    for (int32_t i = 0; i < nr; ++i)
+      for (int64_t p = ptr[r0 + i]; p < ptr[r0 + i + 1]; ++p) H.rowptr[rpbase[seg_k(col[p] / T)] + i + 1]++;
+    for (int k = 0; k < nseg; ++k)
+      for (int32_t i = 0; i < nr; ++i) H.rowptr[rpbase[k] + i + 1] += H.rowptr[rpbase[k] + i];
+    std::vector<int32_t> fill(nseg * (size_t)nr);
+    for (int32_t i = 0; i < nr; ++i)
+      for (int64_t p = ptr[r0 + i]; p < ptr[r0 + i + 1]; ++p) {
+        const int64_t t = col[p] / T;
+        const int k = seg_k(t);
+        const TSeg& S = H.seg[s_begin + k];
+        const int64_t q = S.nz + H.rowptr[rpbase[k] + i] + fill[(size_t)k * nr + i]++;
+        if (S.tile >= 0) { H.col_s[q] = (uint16_t)(col[p] - t * T); H.perm_s[q] = (int32_t)p; H.staged++; }
+        else { H.col_d[q] = col[p]; H.perm_d[q] = (int32_t)p; }
+      }
+    // work items: consecutive segments up to group_nz nonzeros
+    int32_t g = 0;
+    int64_t acc = 0;
+    int32_t ws = s_begin;
+    for (int k = 0; k < nseg; ++k) {
+      acc += seg_nz[k];
+      if (acc >= group_nz || k == nseg - 1) {
+        H.work.push_back(TWork{(int32_t)H.chunk.size(), g++, ws, s_begin + k + 1});
+        ws = s_begin + k + 1;
+        acc = 0;
+      }
+    }
+    if (nseg == 0) H.work.push_back(TWork{(int32_t)H.chunk.size(), g++, s_begin, s_begin});
+    H.chunk.push_back(TChunk{r0, nr, g, H.scratch});
+    H.scratch += (int64_t)g * nr * elem;
+    for (int64_t t : touched) { cnt[t] = 0; segof[t] = -1; }
+  }
 }
 
 }  // namespace
@@ -96,6 +221,20 @@ struct pdcs_ctx {
   DBuf<double> y, yh, y0, ysum, kxh, kxd, ya, kxa, by, candy, res0, res1, onesm;
   DBuf<double> tmpn, tmpm, scal;
   DBuf<double2> xx;                            // interleaved (x^_j, x_j)
+  // column-tiled copies of K~ (pair gather) and K~^T (y gather), tiled.cuh
+  struct TiledDev {
+    bool on = false;
+    TiledMat M;
+    DBuf<TWork> work;
+    DBuf<TChunk> chunk;
+    DBuf<TSeg> seg;
+    DBuf<int32_t> rowptr, col_d;
+    DBuf<uint16_t> col_s;
+    DBuf<double> val_s, val_d, scratch;
+    int g_partial = 0, g_combine = 0;
+    int64_t slot = 0;
+  } tK, tKT;
+  std::vector<int32_t> hcol;                   // host copy of K's column ids (tiled build)
   DBuf<uint8_t> ek, rk;
   DBuf<Block> pblocks, rblocks;
   DBuf<int64_t> rsoc_offs_p, rsoc_offs_r;
@@ -230,7 +369,18 @@ struct pdcs_ctx {
     });
     run_blocks(true, bargs(true, BOP_TRIAL_PRIMAL), false, 0);
     EpiDualTrial e{y.p, ht.p, rk.p, kxh.p, kxd.p, yh.p, 0.0, 0};
-    spmv("spmv_K_dual", K, reinterpret_cast<const double*>(xx.p), nullptr, e, tpart.p, slot_spmv);
+    if (tK.on) {
+      launch("tiled_K_partial", [&] {
+        k_tiled_partial<2><<<tK.g_partial, kTThreads, tiled_smem(2), st>>>(
+            tK.M, reinterpret_cast<const double*>(xx.p), tK.scratch.p, ctl, 1);
+      });
+      launch("spmv_K_dual", [&] {
+        k_tiled_combine<EpiDualTrial, 2><<<tK.g_combine, kThreads, 0, st>>>(tK.M, tK.scratch.p, e, ctl, tpart.p,
+                                                                          slot_spmv);
+      });
+    } else {
+      spmv("spmv_K_dual", K, reinterpret_cast<const double*>(xx.p), nullptr, e, tpart.p, slot_spmv);
+    }
     run_blocks(false, bargs(false, BOP_TRIAL_DUAL), false, 0);
     launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl); });
   }
@@ -241,7 +391,16 @@ struct pdcs_ctx {
       k_halpern_y<<<g_m, kThreads, 0, st>>>(m, yh.p, y0.p, y.p, ysum.p, ctl);
     });
     EpiHalpernX e{xh.p, x0.p, x.p, kty.p, xsum.p, 0, 0, 0, 0, 0};
-    spmv("spmv_KT_halpern", KT, y.p, nullptr, e, nullptr, 0);
+    if (tKT.on) {
+      launch("tiled_KT_partial", [&] {
+        k_tiled_partial<1><<<tKT.g_partial, kTThreads, tiled_smem(1), st>>>(tKT.M, y.p, tKT.scratch.p, ctl, 2);
+      });
+      launch("spmv_KT_halpern", [&] {
+        k_tiled_combine<EpiHalpernX, 1><<<tKT.g_combine, kThreads, 0, st>>>(tKT.M, tKT.scratch.p, e, ctl, nullptr, 0);
+      });
+    } else {
+      spmv("spmv_KT_halpern", KT, y.p, nullptr, e, nullptr, 0);
+    }
   }
   void kkt_launch(KktCand ca, KktCand cb, int ncand, int mode) {
     launch("kkt_rows", [&] {
@@ -303,6 +462,57 @@ struct pdcs_ctx {
     launch("restart_copy", [&] {
       k_restart_copy<<<grid_for(std::max(n, m), sms), kThreads, 0, st>>>(R, ctl);
     });
+  }
+
+  static size_t tiled_smem(int elem) { return (size_t)tiled_tile_bytes() + (size_t)kTRows * elem * sizeof(double); }
+
+  // Build the tiled copy of a CSR (structure on the host, scaled values on the device).
+  void make_tiled(TiledDev& D, const int64_t* hp, const int32_t* hc, int64_t rows, int64_t nvec, int elem,
+                  const double* dval) {
+    TiledHost H;
+    build_tiled(hp, hc, rows, nvec, elem, H);
+    const double frac = H.nnz ? (double)H.staged / (double)H.nnz : 0.0;
+    const char* env = std::getenv("PDCS_TILED");
+    const bool want = env ? std::atoi(env) != 0 : frac >= 0.3;
+    D.on = want && H.nnz > 0;
+    if (!D.on) return;
+    upload(D.work, H.work, st);
+    upload(D.chunk, H.chunk, st);
+    upload(D.seg, H.seg, st);
+    upload(D.rowptr, H.rowptr, st);
+    upload(D.col_s, H.col_s, st);
+    upload(D.col_d, H.col_d, st);
+    DBuf<int32_t> perm;
+    D.val_s.alloc(std::max<size_t>(H.col_s.size(), 1));
+    D.val_d.alloc(std::max<size_t>(H.col_d.size(), 1));
+    if (!H.perm_s.empty()) {
+      upload(perm, H.perm_s, st);
+      k_gather_vals<<<grid_for((int64_t)H.perm_s.size(), sms, 32), kThreads, 0, st>>>((int64_t)H.perm_s.size(), perm.p, dval, D.val_s.p);
+      CK(cudaStreamSynchronize(st));
+    }
+    if (!H.perm_d.empty()) {
+      upload(perm, H.perm_d, st);
+      k_gather_vals<<<grid_for((int64_t)H.perm_d.size(), sms, 32), kThreads, 0, st>>>((int64_t)H.perm_d.size(), perm.p, dval, D.val_d.p);
+      CK(cudaStreamSynchronize(st));
+    }
+    D.scratch.alloc(std::max<int64_t>(H.scratch, 1));
+    TiledMat& M = D.M;
+    M.m = rows; M.nvec = nvec; M.nwork = (int64_t)H.work.size(); M.nchunk = (int64_t)H.chunk.size();
+    M.T = H.T; M.elem = elem;
+    M.work = D.work.p; M.chunk = D.chunk.p; M.seg = D.seg.p; M.rowptr = D.rowptr.p;
+    M.val_s = D.val_s.p; M.col_s = D.col_s.p; M.val_d = D.val_d.p; M.col_d = D.col_d.p;
+    int occ = 1;
+    if (elem == 2) {
+      CK(cudaFuncSetAttribute(k_tiled_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(2)));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<2>, kTThreads, tiled_smem(2)));
+    } else {
+      CK(cudaFuncSetAttribute(k_tiled_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(1)));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<1>, kTThreads, tiled_smem(1)));
+    }
+    D.g_partial = (int)std::max<int64_t>(1, std::min<int64_t>(M.nwork, (int64_t)sms * std::max(occ, 1)));
+    int64_t slabs = 0;
+    for (const TChunk& c : H.chunk) slabs += (c.nrows + kThreads - 1) / kThreads;
+    D.g_combine = (int)std::max<int64_t>(1, std::min<int64_t>(slabs, (int64_t)sms * 4));
   }
 
   // products of (x, y) into (kx, kty)
@@ -397,11 +607,6 @@ std::vector<T> to_host(const T* p, int64_t count, int mem_kind) {
   return v;
 }
 
-template <class T>
-void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
-  d.alloc(h.size());
-  if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
-}
 
 }  // namespace
 
@@ -502,7 +707,8 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
       if (ctx->hptr[i + 1] < ctx->hptr[i]) fail(PDCS_ERR_DIM, "row_ptr not monotone at row " + std::to_string(i));
     const int64_t nnz = ctx->hptr[m];
     if (nnz >= ((int64_t)1 << 31)) fail(PDCS_ERR_DIM, "local nnz must be < 2^31 (shard the rows)");
-    std::vector<int32_t> hcol = to_host(col_idx, nnz, mem_kind);
+    std::vector<int32_t>& hcol = ctx->hcol;
+    hcol = to_host(col_idx, nnz, mem_kind);
     std::vector<double> hval = to_host(vals, nnz, mem_kind);
     for (int64_t i = 0; i < m; ++i)
       for (int64_t q_ = ctx->hptr[i]; q_ < ctx->hptr[i + 1]; ++q_) {
@@ -698,7 +904,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     int64_t s = 0;
     ctx->slot_pe = s; s += ctx->g_pe;
     for (int c = 0; c < 4; ++c) if (ctx->pcls[c].count) { ctx->pcls[c].slot = s; s += ctx->pcls[c].grid; }
-    ctx->slot_spmv = s; s += ctx->K.plan.total_cta;
+    ctx->slot_spmv = s; s += std::max<int64_t>(ctx->K.plan.total_cta, (int64_t)ctx->sms * 4);
     for (int c = 0; c < 4; ++c) if (ctx->rcls[c].count) { ctx->rcls[c].slot = s; s += ctx->rcls[c].grid; }
     ctx->nslot_trial = s;
     int64_t ks = 0;
@@ -762,6 +968,15 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
       k_scale_vals<<<Grn, kThreads, 0, st>>>(n, ctx->KT.ptr, ctx->KT.col, ctx->KT.val, ctx->q.p, ctx->r.p);
     }
     CK(cudaGetLastError());
+    // column-tiled copies of K~ and K~^T for the hot SpMVs (tiled.cuh)
+    {
+      ctx->make_tiled(ctx->tK, ctx->hptr.data(), ctx->hcol.data(), m, n, 2, ctx->K.val);
+      std::vector<int32_t> tp32(n + 1), tcol(ctx->KT.nnz);
+      CK(cudaMemcpy(tp32.data(), ctx->KT.ptr, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      if (ctx->KT.nnz) CK(cudaMemcpy(tcol.data(), ctx->KT.col, ctx->KT.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      std::vector<int64_t> tp(tp32.begin(), tp32.end());
+      ctx->make_tiled(ctx->tKT, tp.data(), tcol.data(), n, m, 1, ctx->KT.val);
+    }
     // scaled data (reading A2): c~ = c/q, h~ = h/r, l~ = q l, u~ = q u
     k_ewise<<<Gn, kThreads, 0, st>>>(n, ctx->c0.p, ctx->q.p, 0, ctx->ct.p);
     k_ewise<<<Gm, kThreads, 0, st>>>(m, ctx->h0.p, ctx->r.p, 0, ctx->ht.p);

@@ -106,7 +106,9 @@ STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e
 SCALAR_KEYS = ["eta", "omega", "beta", "k", "total", "trials", "restarts", "e_anchor", "W", "eta0",
                "cur_err_p", "cur_err_d", "cur_err_gap", "cur_pobj", "cur_dobj",
                "avg_err_p", "avg_err_d", "avg_err_gap", "avg_pobj", "avg_dobj",
-               "e_prev", "best_e", "use_avg", "restart", "last_num", "last_cross"]
+               "e_prev", "best_e", "use_avg", "restart", "last_num", "last_cross",
+               "tiled_K", "tune_K_csr_ms", "tune_K_tiled_ms", "tiled_KT", "tune_KT_csr_ms",
+               "tune_KT_tiled_ms"]
 
 
 def _check(code, ctx=None):

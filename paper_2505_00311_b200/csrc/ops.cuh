@@ -187,6 +187,16 @@ struct EpiStore {
   __device__ void row(int64_t i, double dot, double, Acc<NA>&) { out[i] = dot; }
 };
 
+// Product store of the first component of an interleaved-pair gather (autotune).
+struct EpiStore2 {
+  static constexpr int NA = 1;
+  static constexpr int NX = 3;
+  double* out;
+  __device__ void init(const Ctl*) {}
+  __device__ bool active() const { return true; }
+  __device__ void row(int64_t i, double dot, double, Acc<NA>&) { out[i] = dot; }
+};
+
 // y-side ReflectedHalpern + average: y+, ysum.
 __global__ void __launch_bounds__(kThreads) k_halpern_y(int64_t m, const double* __restrict__ yh,
                                                         const double* __restrict__ y0,

@@ -110,7 +110,7 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
                  TiledHost& H) {
   const int tile_bytes = tiled_tile_bytes();
   const int32_t T = tile_bytes / (8 * elem);
-  const int64_t stage_min = tile_bytes / 32;           // staging beats direct gathers above this
+  const int64_t stage_min = tile_bytes / 16;           // staging must save >= 2x the gather sectors
   // work-item size: enough items to fill the GPU several times over, no more
   // partial groups per chunk than needed (PDCS_TILE_GROUP overrides)
   const int64_t group_nz = std::getenv("PDCS_TILE_GROUP") ? std::atol(std::getenv("PDCS_TILE_GROUP"))
@@ -233,6 +233,7 @@ struct pdcs_ctx {
     DBuf<double> val_s, val_d, scratch;
     int g_partial = 0, g_combine = 0;
     int64_t slot = 0;
+    float tune_csr_ms = 0.f, tune_tiled_ms = 0.f;
   } tK, tKT;
   std::vector<int32_t> hcol;                   // host copy of K's column ids (tiled build)
   DBuf<uint8_t> ek, rk;
@@ -513,6 +514,63 @@ struct pdcs_ctx {
     int64_t slabs = 0;
     for (const TChunk& c : H.chunk) slabs += (c.nrows + kThreads - 1) / kThreads;
     D.g_combine = (int)std::max<int64_t>(1, std::min<int64_t>(slabs, (int64_t)sms * 4));
+    // Setup-time autotune: keep the tiled copy only if it beats the CSR kernel
+    // by >= 10% on this matrix (gather locality decides).
+    if (!env) {
+      const DevCsr& A = elem == 2 ? K : KT;
+      DBuf<double> xin, out;
+      xin.alloc(std::max<int64_t>(nvec * elem, 1));
+      out.alloc(std::max<int64_t>(rows, 1));
+      k_fill<<<grid_for(nvec * elem, sms), kThreads, 0, st>>>(nvec * elem, 1.0, xin.p);
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      auto run_csr = [&] {
+        if (elem == 2) {
+          EpiStore2 e{out.p};
+          spmv_kernel<EpiStore2><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, xin.p, nullptr, A.plan, e, ctl, nullptr, 0);
+        } else {
+          EpiStore e{out.p};
+          spmv_kernel<EpiStore><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, xin.p, nullptr, A.plan, e, ctl, nullptr, 0);
+        }
+      };
+      auto run_tiled = [&] {
+        if (elem == 2) {
+          k_tiled_partial<2><<<D.g_partial, kTThreads, tiled_smem(2), st>>>(M, xin.p, D.scratch.p, ctl, 0);
+          EpiStore2 e{out.p};
+          k_tiled_combine<EpiStore2, 2><<<D.g_combine, kThreads, 0, st>>>(M, D.scratch.p, e, ctl, nullptr, 0);
+        } else {
+          k_tiled_partial<1><<<D.g_partial, kTThreads, tiled_smem(1), st>>>(M, xin.p, D.scratch.p, ctl, 0);
+          EpiStore e{out.p};
+          k_tiled_combine<EpiStore, 1><<<D.g_combine, kThreads, 0, st>>>(M, D.scratch.p, e, ctl, nullptr, 0);
+        }
+      };
+      auto timeit = [&](auto&& f) {   // median of 5 after 2 warm-ups
+        f();
+        f();
+        float v[5];
+        for (int i = 0; i < 5; ++i) {
+          CK(cudaEventRecord(a, st));
+          f();
+          CK(cudaEventRecord(b, st));
+          CK(cudaEventSynchronize(b));
+          CK(cudaEventElapsedTime(&v[i], a, b));
+        }
+        std::sort(v, v + 5);
+        return v[2];
+      };
+      const float tc = timeit(run_csr), tt = timeit(run_tiled);
+      CK(cudaGetLastError());
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      D.tune_csr_ms = tc;
+      D.tune_tiled_ms = tt;
+      if (!(tt < 0.9f * tc)) {
+        D.on = false;
+        D.work.free_(); D.chunk.free_(); D.seg.free_(); D.rowptr.free_(); D.col_d.free_(); D.col_s.free_();
+        D.val_s.free_(); D.val_d.free_(); D.scratch.free_();
+      }
+    }
   }
 
   // products of (x, y) into (kx, kty)
@@ -1295,12 +1353,14 @@ int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
   if (!ctx || !out || !ctx->ctl) return 0;
   if (guard(ctx, [&] { ctx->read_ctl(); }) != PDCS_OK) return 0;
   const Ctl& C = *ctx->hctl;
-  double v[26] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
+  double v[32] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
                   (double)C.restarts, C.e_anchor, C.Wsum, C.eta_init,
                   C.kkt[0][0], C.kkt[0][1], C.kkt[0][2], C.kkt[0][3], C.kkt[0][4],
                   C.kkt[1][0], C.kkt[1][1], C.kkt[1][2], C.kkt[1][3], C.kkt[1][4],
-                  C.e_prev, C.best_e, (double)C.use_avg, (double)C.restart, C.last_num, C.last_cross};
-  const int k = std::min(cap, 26);
+                  C.e_prev, C.best_e, (double)C.use_avg, (double)C.restart, C.last_num, C.last_cross,
+                  (double)ctx->tK.on, ctx->tK.tune_csr_ms, ctx->tK.tune_tiled_ms,
+                  (double)ctx->tKT.on, ctx->tKT.tune_csr_ms, ctx->tKT.tune_tiled_ms};
+  const int k = std::min(cap, 32);
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }

@@ -259,3 +259,46 @@ def test_empty_and_degenerate(P):
     g = P.PdcsSolver(prog, tol=1e-8)
     r = g.solve()
     assert r["status"] == "OPTIMAL" and abs(r["pobj"]) < 1e-8
+
+
+# ------------------------------------------------------------------ tiled SpMV path forced
+@pytest.fixture
+def tiled_env(monkeypatch):
+    """Force the column-tiled SpMV (tiled.cuh) regardless of the setup autotune."""
+    monkeypatch.setenv("PDCS_TILED", "1")
+    monkeypatch.setenv("PDCS_TILE_KB", "1")        # tiny tiles -> many staged segments
+    yield
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_tiled_one_step_and_shadow(P, tiled_env, seed):
+    prog = mixed(40 + seed, m=900, n1=120, n2=500, soc_dims=(3, 120), row_len=(20, 90))
+    rng = np.random.default_rng(seed)
+    g = P.PdcsSolver(prog)
+    sc = g.scalars()
+    assert sc["tiled_K"] == 1.0 and sc["tiled_KT"] == 1.0
+    o = O.OracleSolver(prog)
+    ro, qo = o.get_scaling()
+    x = rng.standard_normal(prog.n) * 3
+    y = rng.standard_normal(prog.m) * 3
+    g.set_iterate(x, y)
+    o.set_iterate(x * qo, y * ro)
+    g.iterate(1)
+    o.iterate(1)
+    xg, yg = g.get_iterate(P.PDHG_OUT)
+    xo, yo = o.get_iterate(1)
+    assert parity(xg, yg, xo, yo) <= 1e-12
+    worst = _shadow(P, prog, 200)
+    assert worst <= TOL, worst
+
+
+def test_tiled_lasso_vanilla_parity(P, tiled_env):
+    prog = gen_lasso(400, 300, 0.2, seed=5)
+    g = P.PdcsSolver(prog, vanilla_pdhg=1)
+    assert g.scalars()["tiled_K"] == 1.0
+    o = O.OracleSolver(prog, vanilla_pdhg=1)
+    g.iterate(300)
+    o.iterate(300)
+    xg, yg = g.get_iterate(P.CURRENT)
+    xo, yo = o.get_iterate(0)
+    assert parity(xg, yg, xo, yo) <= TOL

@@ -82,6 +82,7 @@ struct Ctl {
   int32_t accepted, status, store_kty, need_check;
   int32_t restart, use_avg, best_flag, done;
   int32_t vanilla, ncand;
+  int32_t stop_at_tol, pad2;
   // parameters
   double ls_shrink, ls_grow, beta_max, suff, nec, art;
   int32_t ls_max_rejects, refl_window, check_interval, pad;

@@ -54,9 +54,23 @@ __global__ void __launch_bounds__(kThreads) k_avg_elem(int64_t n, const uint8_t*
 // AdaptiveStepPDHG accept test (reading A7) and
 // AdaptiveReflectionParameter (reading A9), Halpern coefficients
 // (PAPER.md:606).  One CTA; partial sums reduced in a fixed order.
+// In graph mode (h_retry != 0) the decision also drives the graph's WHILE node
+// (repeat the trial while rejected) and IF node (run the Eq. 9 check).
+__device__ __forceinline__ void set_graph_flags(unsigned long long h_retry, unsigned long long h_check,
+                                                unsigned int retry, unsigned int check) {
+  if (h_retry) {
+    cudaGraphSetConditional((cudaGraphConditionalHandle)h_retry, retry);
+    cudaGraphSetConditional((cudaGraphConditionalHandle)h_check, check);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_decide(const double* __restrict__ part, int64_t nslots,
-                                                     Ctl* ctl) {
-  if (ctl->status != ST_RUNNING) return;
+                                                     Ctl* ctl, unsigned long long h_retry,
+                                                     unsigned long long h_check) {
+  if (ctl->status != ST_RUNNING) {
+    if (threadIdx.x == 0) set_graph_flags(h_retry, h_check, 0u, 0u);
+    return;
+  }
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   for (int64_t i = threadIdx.x; i < nslots; i += blockDim.x) {
     s0 += part[i * kAcc + 0];
@@ -122,6 +136,7 @@ __global__ void __launch_bounds__(kThreads) k_decide(const double* __restrict__ 
   }
   C.tau = C.eta / C.omega;
   C.sigma = C.eta * C.omega;
+  set_graph_flags(h_retry, h_check, (!acc && C.status == ST_RUNNING) ? 1u : 0u, C.need_check ? 1u : 0u);
 }
 
 // ---------------------------------------------------------------- SpMV epilogues
@@ -372,7 +387,10 @@ __global__ void __launch_bounds__(kThreads) k_kkt_finalize(const double* __restr
     C.best_flag = 1;
     for (int i = 0; i < 5; ++i) C.best_kkt[i] = C.kkt[use_avg][i];
   }
-  if (ec <= C.tol) C.done = 1;
+  if (ec <= C.tol) {
+    C.done = 1;
+    if (C.stop_at_tol) C.status = ST_OPTIMAL;   // graph mode: later launches become no-ops
+  }
   if (C.vanilla) return;
   const bool rs = ec <= C.suff * C.e_anchor ||
                   (C.e_prev >= 0.0 && ec <= C.nec * C.e_anchor && ec > C.e_prev) ||

@@ -250,6 +250,14 @@ struct pdcs_ctx {
   int64_t slot_pe = 0, slot_spmv = 0, kslot_rows = 0, kslot_cols = 0;
   int g_pe = 0, g_m = 0, g_kr = 0, g_kc = 0, g_grid = 0;
 
+  // CUDA graph of one accepted iteration: WHILE(rejected){trial} -> accept -> IF(check){check}
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_st = nullptr, cap_st2 = nullptr;
+  unsigned long long g_retry = 0, g_check = 0;   // nonzero only while capturing / in the graph
+  bool graph_failed = false;
+  int64_t nodes_trial = 0, nodes_accept = 0, nodes_check = 0;
+
   // timing / counters
   bool timing = false;
   std::map<std::string, std::pair<double, int64_t>> ktimes;
@@ -259,6 +267,10 @@ struct pdcs_ctx {
   int64_t launches = 0;
 
   ~pdcs_ctx() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    if (cap_st) cudaStreamDestroy(cap_st);
+    if (cap_st2) cudaStreamDestroy(cap_st2);
     if (ctl) cudaFree(ctl);
     if (hctl) cudaFreeHost(hctl);
     for (auto e : evpool) cudaEventDestroy(e);
@@ -383,7 +395,7 @@ struct pdcs_ctx {
       spmv("spmv_K_dual", K, reinterpret_cast<const double*>(xx.p), nullptr, e, tpart.p, slot_spmv);
     }
     run_blocks(false, bargs(false, BOP_TRIAL_DUAL), false, 0);
-    launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl); });
+    launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl, g_retry, g_check); });
   }
   // Accepted step: y+ (Halpern/average on y), then K^T y+ with the fused
   // Halpern/average on x.
@@ -463,6 +475,74 @@ struct pdcs_ctx {
     launch("restart_copy", [&] {
       k_restart_copy<<<grid_for(std::max(n, m), sms), kThreads, 0, st>>>(R, ctl);
     });
+  }
+
+  // Add a conditional node (WHILE / IF) at the current capture position of `st`
+  // and capture body() into its body graph on a second stream.
+  template <class F>
+  void capture_conditional(cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type, F&& body,
+                           int64_t& nodes) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &ndeps));
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = type;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, cg, deps, ndeps, &np));
+    CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+    cudaStream_t saved = st;
+    st = cap_st2;
+    const int64_t l0 = launches;
+    CK(cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    body();
+    CK(cudaStreamEndCapture(st, &bodyg));
+    nodes = launches - l0;
+    st = saved;
+  }
+
+  // Build the per-iteration graph once (after setup); on failure fall back to
+  // the host-driven loop.
+  void build_graph() {
+    if (gexec || graph_failed) return;
+    try {
+      if (!cap_st) CK(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
+      if (!cap_st2) CK(cudaStreamCreateWithFlags(&cap_st2, cudaStreamNonBlocking));
+      CK(cudaGraphCreate(&graph, 0));
+      cudaGraphConditionalHandle hr, hc;
+      CK(cudaGraphConditionalHandleCreate(&hr, graph, 1, cudaGraphCondAssignDefault));
+      CK(cudaGraphConditionalHandleCreate(&hc, graph, 0, cudaGraphCondAssignDefault));
+      cudaStream_t saved = st;
+      const bool tsave = timing;
+      timing = false;
+      st = cap_st;
+      g_retry = (unsigned long long)hr;
+      g_check = (unsigned long long)hc;
+      CK(cudaStreamBeginCaptureToGraph(st, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      capture_conditional(hr, cudaGraphCondTypeWhile, [&] { trial(); }, nodes_trial);
+      const int64_t l0 = launches;
+      accept();
+      nodes_accept = launches - l0;
+      capture_conditional(hc, cudaGraphCondTypeIf, [&] { check(); }, nodes_check);
+      cudaGraph_t out;
+      CK(cudaStreamEndCapture(st, &out));
+      st = saved;
+      timing = tsave;
+      g_retry = g_check = 0;
+      CK(cudaGraphInstantiate(&gexec, graph, 0));
+    } catch (const CudaErr& e) {
+      graph_failed = true;
+      g_retry = g_check = 0;
+      cudaGetLastError();
+      if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+      if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
+      err = std::string("graph build failed (host loop used): ") + cudaGetErrorString(e.e) + " at " + e.what;
+    }
   }
 
   static size_t tiled_smem(int elem) { return (size_t)tiled_tile_bytes() + (size_t)kTRows * elem * sizeof(double); }
@@ -1144,8 +1224,45 @@ static void finish_result(pdcs_ctx* ctx, pdcs_result_t* out, double secs) {
   out->solve_seconds = secs;
 }
 
-// Host loop of Alg. 1 (v1: the accept flag is read back after each trial).
+// Graph-driven loop of Alg. 1: one graph launch per accepted iteration; the
+// host synchronises only every check_interval launches (to test termination)
+// or at the end.
+static bool run_steps_graph(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, double time_limit) {
+  if (ctx->timing || std::getenv("PDCS_NO_GRAPH")) return false;
+  ctx->build_graph();
+  if (!ctx->gexec) return false;
+  auto t0 = std::chrono::steady_clock::now();
+  ctx->read_ctl();
+  ctx->hctl->stop_at_tol = stop_at_tol ? 1 : 0;
+  ctx->write_ctl();
+  const Ctl before = *ctx->hctl;
+  const int64_t batch = stop_at_tol ? ctx->prm.check_interval : n_inner;
+  int64_t done = 0;
+  while (done < n_inner) {
+    const int64_t b = std::min(batch, n_inner - done);
+    for (int64_t i = 0; i < b; ++i) CK(cudaGraphLaunch(ctx->gexec, ctx->st));
+    done += b;
+    ctx->read_ctl();
+    if (ctx->hctl->status == ST_NUMERICAL) fail(PDCS_ERR_NUMERICAL, "line search failed (eta underflow / too many rejects)");
+    if (ctx->hctl->status != ST_RUNNING) break;
+    if (stop_at_tol && time_limit > 0 &&
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > time_limit) {
+      ctx->hctl->status = ST_TIME; ctx->write_ctl(); break;
+    }
+  }
+  const Ctl& C = *ctx->hctl;
+  const int64_t trials = C.trials - before.trials, iters = C.total - before.total;
+  ctx->launches += trials * ctx->nodes_trial + iters * ctx->nodes_accept +
+                   (iters / std::max(1, ctx->prm.check_interval)) * ctx->nodes_check;
+  ctx->hctl->stop_at_tol = 0;
+  ctx->write_ctl();
+  return true;
+}
+
+// Host loop of Alg. 1 (the accept flag is read back after each trial); used
+// with per-kernel timing and as the fallback when graphs are unavailable.
 static void run_steps(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, double time_limit) {
+  if (run_steps_graph(ctx, n_inner, stop_at_tol, time_limit)) return;
   auto t0 = std::chrono::steady_clock::now();
   for (int64_t s = 0; s < n_inner; ++s) {
     for (;;) {

@@ -117,18 +117,23 @@ def iter_alg_bytes(prog):
     return 12 * nnz + 4 * (m + 1) + 12 * nnz + 4 * (n + 1) + 8 * 14 * (m + n)
 
 
-def pinned(prog):
+def pinned(prog, rows):
+    """Pinned host copies of this rank's shard (rows [a, b)) and the replicated data."""
     import torch
+    from paper_2505_00311_b200 import dist as D
+    sh = D.shard(prog, *rows)
     def pin(a, dt):
         return torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
-    return dict(row_ptr=pin(prog.row_ptr, np.int64), col=pin(prog.col_idx, np.int32),
-                val=pin(prog.vals, np.float64), c=pin(prog.c, np.float64), h=pin(prog.h, np.float64),
+    return dict(row_ptr=pin(sh["row_ptr"], np.int64), col=pin(sh["col"], np.int32),
+                val=pin(sh["val"], np.float64), c=pin(prog.c, np.float64), h=pin(sh["h"], np.float64),
                 l=pin(prog.l, np.float64), u=pin(prog.u, np.float64))
 
 
-def make_ctx(P, prog, host, params, stream, device):
-    ctx = P.pdcs_create(prog.m, prog.n, prog.n1, 0, prog.m, host["row_ptr"], host["col"], host["val"],
-                        host["c"], host["h"], host["l"], host["u"], params, device, stream)
+def make_ctx(P, prog, host, params, stream, device, rows, uid=None, rank=0, world=1):
+    idbuf = None if uid is None else np.frombuffer(uid, dtype=np.uint8).copy()
+    ctx = P.pdcs_create(prog.m, prog.n, prog.n1, rows[0], rows[1], host["row_ptr"], host["col"],
+                        host["val"], host["c"], host["h"], host["l"], host["u"], params, device, stream,
+                        nccl_unique_id=idbuf, rank=rank, world=world)
     P.pdcs_set_cones(ctx, prog.pk, prog.pdim, prog.rk, prog.rdim)
     return ctx
 
@@ -211,7 +216,8 @@ def _config(prog, args):
     return {"workload": args.config, "instance": prog.name, "m": prog.m, "n": prog.n, "nnz": prog.nnz,
             "cones": {"primal": [int(k) for k in np.unique(prog.pk)], "rows": [int(k) for k in np.unique(prog.rk)]},
             "l2": "inputs larger than L2 (matrix %.2f GB > 126 MB)" % (24 * prog.nnz / 1e9),
-            "parallelism": f"dp{args.gpus}-replica" if args.gpus > 1 else "single-gpu"}
+            "parallelism": f"rows-sharded-x{args.gpus} (NCCL all-reduce, replicated primal)" if args.gpus > 1
+            else "single-gpu"}
 
 
 def main():
@@ -240,17 +246,28 @@ def main():
     import paper_2505_00311_b200 as P
 
     prog, gen_s = build_instance(args.config, args.seed)
-    host = pinned(prog)
+    from paper_2505_00311_b200 import dist as D
+    rows = D.partition_rows(prog.row_ptr, prog.rk, prog.rdim, world)[rank]
+    uid = None
+    if world > 1:
+        # rank 0 creates the ncclUniqueId, torch.distributed broadcasts it
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(P.pdcs_nccl_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(buf, 0)
+        uid = bytes(buf.cpu().numpy().tobytes())
+    host = pinned(prog, rows)
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     params = P.pdcs_default_params()
+    mk = lambda prm: make_ctx(P, prog, host, prm, sh, local, rows, uid, rank, world)
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
     # ---------------- device-timed steps (inputs resident in HBM)
-    ctx = make_ctx(P, prog, host, params, sh, local)
+    ctx = mk(params)
     P.pdcs_iterate(ctx, args.warmup)
     barrier()
     torch.cuda.synchronize()
@@ -279,7 +296,7 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = world * args.steps / (ms / 1e3)
+    value = args.steps / (ms / 1e3)          # iterations of the (one, row-sharded) problem per second
     P.pdcs_destroy(ctx)
 
     # ---------------- roofline of the dominant kernel (an SpMV sweep = its
@@ -317,17 +334,17 @@ def main():
     torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
-    ctx = make_ctx(P, prog, host, params, sh, local)
+    ctx = mk(params)
     P.pdcs_iterate(ctx, args.steps)
     xo = torch.empty(prog.n, dtype=torch.float64).pin_memory()
-    yo = torch.empty(prog.m, dtype=torch.float64).pin_memory()
+    yo = torch.empty(rows[1] - rows[0], dtype=torch.float64).pin_memory()
     P.pdcs_get_iterate(ctx, P.CURRENT, P.ORIGINAL, xo, yo)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     P.pdcs_destroy(ctx)
     h2d = sum(int(t.numel() * t.element_size()) for t in host.values())
-    d2h = (prog.n + prog.m) * 8
-    e2e = {"value": world * args.steps / e2e_s, "unit": "iter/s",
+    d2h = (prog.n + rows[1] - rows[0]) * 8
+    e2e = {"value": args.steps / e2e_s, "unit": "iter/s",
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
            "seconds": e2e_s, "note": "create+set_cones (upload, transpose, Ruiz) + iterate(K) + D2H of (x, y)"}
 
@@ -337,7 +354,7 @@ def main():
         p4 = P.pdcs_default_params(tol=1e-4, time_limit_s=args.tol_time_limit)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctx = make_ctx(P, prog, host, p4, sh, local)
+        ctx = mk(p4)
         torch.cuda.synchronize()
         t_setup = time.perf_counter() - t0
         r = P.pdcs_solve(ctx)
@@ -355,7 +372,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded Philox, PAPER.md:1663 recipe at BASELINE configs[1] size)",
                 "config": _config(prog, args), "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,

@@ -10,8 +10,9 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpdcs.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+NCCL_INC = os.environ.get("NCCL_INC", "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/include")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "550"]
+         "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "550", "-I" + NCCL_INC, "-ldl"]
 
 
 def sources():
@@ -19,7 +20,7 @@ def sources():
 
 
 def deps():
-    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [
+    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [
         os.path.join(HERE, "..", "include", "pdcs.h")]
 
 

@@ -83,6 +83,8 @@ struct Ctl {
   int32_t restart, use_avg, best_flag, done;
   int32_t vanilla, ncand;
   int32_t stop_at_tol, pad2;
+  double red3[3];            // trial sums (dxx, dyy, cross) when reduced outside k_decide
+  double kred[20];           // Eq. 9 reductions (10 per candidate) before the decision
   // parameters
   double ls_shrink, ls_grow, beta_max, suff, nec, art;
   int32_t ls_max_rejects, refl_window, check_interval, pad;

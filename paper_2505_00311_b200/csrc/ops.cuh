@@ -64,13 +64,39 @@ __device__ __forceinline__ void set_graph_flags(unsigned long long h_retry, unsi
   }
 }
 
+// Reduce the trial partial slots into ctl->red3 (row-sharded runs all-reduce
+// red3[1..2] between this kernel and k_decide).
+__global__ void __launch_bounds__(kThreads) k_reduce_trial(const double* __restrict__ part, int64_t nslots,
+                                                           Ctl* ctl) {
+  if (ctl->status != ST_RUNNING) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t i = threadIdx.x; i < nslots; i += blockDim.x) {
+    s0 += part[i * kAcc + 0];
+    s1 += part[i * kAcc + 1];
+    s2 += part[i * kAcc + 2];
+  }
+  __shared__ double red[3][kThreads];
+  red[0][threadIdx.x] = s0; red[1][threadIdx.x] = s1; red[2][threadIdx.x] = s2;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w >= 1; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + w];
+      red[1][threadIdx.x] += red[1][threadIdx.x + w];
+      red[2][threadIdx.x] += red[2][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { ctl->red3[0] = red[0][0]; ctl->red3[1] = red[1][0]; ctl->red3[2] = red[2][0]; }
+}
+
 __global__ void __launch_bounds__(kThreads) k_decide(const double* __restrict__ part, int64_t nslots,
                                                      Ctl* ctl, unsigned long long h_retry,
-                                                     unsigned long long h_check) {
+                                                     unsigned long long h_check, int prereduced) {
   if (ctl->status != ST_RUNNING) {
     if (threadIdx.x == 0) set_graph_flags(h_retry, h_check, 0u, 0u);
     return;
   }
+  if (prereduced) nslots = 0;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   for (int64_t i = threadIdx.x; i < nslots; i += blockDim.x) {
     s0 += part[i * kAcc + 0];
@@ -90,7 +116,9 @@ __global__ void __launch_bounds__(kThreads) k_decide(const double* __restrict__ 
   }
   if (threadIdx.x != 0) return;
   Ctl& C = *ctl;
-  const double dxx = red[0][0], dyy = red[1][0], cross = red[2][0];
+  const double dxx = prereduced ? C.red3[0] : red[0][0];
+  const double dyy = prereduced ? C.red3[1] : red[1][0];
+  const double cross = prereduced ? C.red3[2] : red[2][0];
   C.last_dxx = dxx; C.last_dyy = dyy; C.last_cross = cross;
   const double num = C.omega * dxx + dyy / C.omega;
   C.last_num = num;
@@ -192,6 +220,23 @@ struct EpiHalpernX {
   }
 };
 
+// x-side ReflectedHalpern + average after the all-reduce of K^T y+ (row-sharded
+// path; the single-GPU path fuses this into the K^T sweep as EpiHalpernX).
+__global__ void __launch_bounds__(kThreads) k_halpern_x(int64_t n, const double* __restrict__ xh,
+                                                        const double* __restrict__ x0,
+                                                        const double* __restrict__ ktyp,
+                                                        double* __restrict__ x, double* __restrict__ kty,
+                                                        double* __restrict__ xsum, const Ctl* ctl) {
+  if (ctl->status != ST_RUNNING || !ctl->accepted) return;
+  const double a = ctl->ha, b = ctl->hbeta, c = ctl->hb, eta = ctl->eta_used;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double xn = a * ((1.0 + b) * xh[j] - b * x[j]) + c * x0[j];
+    x[j] = xn;
+    kty[j] = ktyp[j];
+    xsum[j] += eta * xn;
+  }
+}
+
 // Plain product store.
 struct EpiStore {
   static constexpr int NA = 1;
@@ -199,6 +244,17 @@ struct EpiStore {
   double* out;
   __device__ void init(const Ctl*) {}
   __device__ bool active() const { return true; }
+  __device__ void row(int64_t i, double dot, double, Acc<NA>&) { out[i] = dot; }
+};
+
+// Product store only on an accepted step (row-sharded K^T y+ partial).
+struct EpiStoreAcc {
+  static constexpr int NA = 1;
+  static constexpr int NX = 1;
+  double* out;
+  int run;
+  __device__ void init(const Ctl* C) { run = C->status == ST_RUNNING && C->accepted; }
+  __device__ bool active() const { return run; }
   __device__ void row(int64_t i, double dot, double, Acc<NA>&) { out[i] = dot; }
 };
 
@@ -338,13 +394,10 @@ __global__ void __launch_bounds__(kThreads) k_kkt_cols(int64_t n, const uint8_t*
   write_kkt_partials(kv, part, slot0 + blockIdx.x);
 }
 
-// Reduce the KKT partials, form Eq. 9 for each candidate and run
-// GetRestartCandidate / restart condition / PrimalWeightUpdate / termination
-// (readings A10-A15).
-// mode 0: evaluate only (kkt[0..ncand)); mode 1: full check.
-__global__ void __launch_bounds__(kThreads) k_kkt_finalize(const double* __restrict__ part, int64_t nslots,
-                                                           int ncand, int mode, double hnorm, double cnorm,
-                                                           Ctl* ctl) {
+// Reduce the KKT partial slots into ctl->kred (row-sharded runs all-reduce the
+// row-side entries 10c+0..2 (max) and 10c+3..4 (sum) before k_kkt_decide).
+__global__ void __launch_bounds__(kThreads) k_kkt_reduce(const double* __restrict__ part, int64_t nslots,
+                                                         Ctl* ctl) {
   __shared__ double red[kKAcc][kThreads];
   double acc[kKAcc];
   for (int i = 0; i < kKAcc; ++i) acc[i] = 0.0;
@@ -362,11 +415,19 @@ __global__ void __launch_bounds__(kThreads) k_kkt_finalize(const double* __restr
                                             : red[i][threadIdx.x] + red[i][threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x < kKAcc) ctl->kred[threadIdx.x] = red[threadIdx.x][0];
+}
+
+// Form Eq. 9 for each candidate and run GetRestartCandidate / restart
+// condition / PrimalWeightUpdate / termination (
+// SPEC.md:387-413; readings A10-A15).  mode 0: evaluate only; 1: full check.
+__global__ void k_kkt_decide(int ncand, int mode, double hnorm, double cnorm, Ctl* ctl) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double* red = ctl->kred;
   Ctl& C = *ctl;
   double e[2] = {kInf, kInf};
   for (int c = 0; c < ncand; ++c) {
-    auto R = [&](int i) { return red[10 * c + i][0]; };
+    auto R = [&](int i) { return red[10 * c + i]; };
     const double err_p = R(0) / (1.0 + fmax(hnorm, fmax(R(1), R(2))));
     const double err_d = R(5) / (1.0 + fmax(cnorm, R(6)));
     const double pobj = R(7), dobj = R(3) + R(8);

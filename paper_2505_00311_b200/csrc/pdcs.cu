@@ -21,6 +21,7 @@
 #include "../../include/pdcs.h"
 #include "ops.cuh"
 #include "tiled.cuh"
+#include "comm.h"
 
 using namespace pdcs;
 
@@ -221,6 +222,10 @@ struct pdcs_ctx {
   DBuf<double> y, yh, y0, ysum, kxh, kxd, ya, kxa, by, candy, res0, res1, onesm;
   DBuf<double> tmpn, tmpm, scal;
   DBuf<double2> xx;                            // interleaved (x^_j, x_j)
+  // row sharding (comm.h): NCCL communicator over the ranks
+  bool dist = false;
+  ncclComm_t comm = nullptr;
+  DBuf<double> ktyp;                           // local K~^T y partial before the all-reduce
   // column-tiled copies of K~ (pair gather) and K~^T (y gather), tiled.cuh
   struct TiledDev {
     bool on = false;
@@ -267,6 +272,7 @@ struct pdcs_ctx {
   int64_t launches = 0;
 
   ~pdcs_ctx() {
+    if (comm) nccl().CommDestroy(comm);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
     if (cap_st) cudaStreamDestroy(cap_st);
@@ -323,8 +329,13 @@ struct pdcs_ctx {
                                                               part, slot0);
     });
   }
-  void spmv_store(const DevCsr& A, const double* xin, double* out) {
+  void spmv_store(const DevCsr& A, const double* xin, double* out, bool accepted_only = false) {
     EpiStore e{out};
+    if (accepted_only) {
+      EpiStoreAcc ea{out, 0};
+      spmv("spmv_KT_partial", A, xin, nullptr, ea, nullptr, 0);
+      return;
+    }
     spmv("spmv_store", A, xin, nullptr, e, nullptr, 0);
   }
 
@@ -335,6 +346,13 @@ struct pdcs_ctx {
   void write_ctl() {
     CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
+  }
+  // In-place all-reduce over the row shards (no-op on a single rank).
+  void allreduce(double* buf, size_t count, ncclRedOp_t op) {
+    if (!dist || count == 0) return;
+    ++launches;
+    const ncclResult_t r = nccl().AllReduce(buf, buf, count, ncclFloat64, op, comm, st);
+    if (r != ncclSuccess) fail(PDCS_ERR_NCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
   }
 
   // ---------------------------------------------------------------- block kernels
@@ -395,7 +413,13 @@ struct pdcs_ctx {
       spmv("spmv_K_dual", K, reinterpret_cast<const double*>(xx.p), nullptr, e, tpart.p, slot_spmv);
     }
     run_blocks(false, bargs(false, BOP_TRIAL_DUAL), false, 0);
-    launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl, g_retry, g_check); });
+    if (dist) {
+      launch("reduce_trial", [&] { k_reduce_trial<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl); });
+      allreduce(&ctl->red3[1], 2, ncclSum);     // ||dy||^2 and <dy, K dx> over the row shards
+      launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, 0, ctl, g_retry, g_check, 1); });
+    } else {
+      launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl, g_retry, g_check, 0); });
+    }
   }
   // Accepted step: y+ (Halpern/average on y), then K^T y+ with the fused
   // Halpern/average on x.
@@ -403,6 +427,15 @@ struct pdcs_ctx {
     launch("halpern_y", [&] {
       k_halpern_y<<<g_m, kThreads, 0, st>>>(m, yh.p, y0.p, y.p, ysum.p, ctl);
     });
+    if (dist) {
+      // local K~^T y+ partial -> all-reduce -> x-side Halpern
+      spmv_store(KT, y.p, ktyp.p, true);
+      allreduce(ktyp.p, n, ncclSum);
+      launch("halpern_x", [&] {
+        k_halpern_x<<<g_pe, kThreads, 0, st>>>(n, xh.p, x0.p, ktyp.p, x.p, kty.p, xsum.p, ctl);
+      });
+      return;
+    }
     EpiHalpernX e{xh.p, x0.p, x.p, kty.p, xsum.p, 0, 0, 0, 0, 0};
     if (tKT.on) {
       launch("tiled_KT_partial", [&] {
@@ -434,9 +467,12 @@ struct pdcs_ctx {
     }
     // zero the slots of a candidate that was not evaluated
     if (ncand == 1) zero_cand1_kslots();
-    launch("kkt_finalize", [&] {
-      k_kkt_finalize<<<1, kThreads, 0, st>>>(kpart.p, nslot_kkt, ncand, mode, hnorm, cnorm, ctl);
-    });
+    launch("kkt_reduce", [&] { k_kkt_reduce<<<1, kThreads, 0, st>>>(kpart.p, nslot_kkt, ctl); });
+    for (int c = 0; c < ncand; ++c) {             // row-side Eq. 9 terms over the shards
+      allreduce(&ctl->kred[10 * c], 3, ncclMax);
+      allreduce(&ctl->kred[10 * c + 3], 2, ncclSum);
+    }
+    launch("kkt_decide", [&] { k_kkt_decide<<<1, 32, 0, st>>>(ncand, mode, hnorm, cnorm, ctl); });
   }
   void zero_cand1_kslots() {
     for (int side = 0; side < 2; ++side) {
@@ -452,6 +488,7 @@ struct pdcs_ctx {
     KktCand c0{xh.p, yh.p, kxh.p, ktyh.p, res0.p, lam0.p};
     KktCand c1{xa.p, ya.p, kxa.p, ktya.p, res1.p, lam1.p};
     spmv_store(KT, yh.p, ktyh.p);   // K^T y^ of the current candidate (K x^ kept by the K pass)
+    allreduce(ktyh.p, n, ncclSum);
     if (!van) {
       launch("avg_elem", [&] { k_avg_elem<<<g_pe, kThreads, 0, st>>>(n, ek.p, xsum.p, lt.p, ut.p, xa.p, ctl); });
       BlockArgs A = bargs(true, BOP_AVG_PRIMAL);
@@ -463,6 +500,7 @@ struct pdcs_ctx {
       run_blocks(false, B, false, 0);
       spmv_store(K, xa.p, kxa.p);
       spmv_store(KT, ya.p, ktya.p);
+      allreduce(ktya.p, n, ncclSum);
     }
     kkt_launch(c0, c1, van ? 1 : 2, 1);
     RestartArgs R{};
@@ -657,6 +695,7 @@ struct pdcs_ctx {
   void products(const double* xs, const double* ys, double* kxo, double* ktyo) {
     spmv_store(K, xs, kxo);
     spmv_store(KT, ys, ktyo);
+    allreduce(ktyo, n, ncclSum);
   }
 
   // ---------------------------------------------------------------- setup helpers
@@ -815,7 +854,8 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
     if (m_global < 0 || n < 0 || n1 < 0 || n1 > n) fail(PDCS_ERR_DIM, "bad sizes m/n/n1");
     if (row_begin < 0 || row_end < row_begin || row_end > m_global) fail(PDCS_ERR_DIM, "bad row range");
     if (mem_kind != PDCS_MEM_HOST && mem_kind != PDCS_MEM_DEVICE) fail(PDCS_ERR_ARG, "bad mem_kind");
-    if (world != 1 || nccl_unique_id) fail(PDCS_ERR_ARG, "multi-rank contexts are not enabled in this build");
+    if (world < 1 || rank < 0 || rank >= world) fail(PDCS_ERR_ARG, "bad rank / world");
+    if (world > 1 && !nccl_unique_id) fail(PDCS_ERR_ARG, "world > 1 needs an nccl_unique_id");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(PDCS_ERR_CUDA, "no CUDA device");
     if (device < 0 || device >= ndev) fail(PDCS_ERR_ARG, "bad device ordinal");
@@ -826,6 +866,15 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
                                               std::to_string(prop.major * 10 + prop.minor));
     ctx->device = device;
     ctx->sms = prop.multiProcessorCount;
+    if (nccl_unique_id) {                          // row-sharded context (also world == 1, for testing)
+      std::string e;
+      if (!nccl().load(e)) fail(PDCS_ERR_NCCL, e);
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_unique_id, sizeof(id));
+      const ncclResult_t r = nccl().CommInitRank(&ctx->comm, world, id, rank);
+      if (r != ncclSuccess) fail(PDCS_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+      ctx->dist = true;
+    }
     ctx->st = (cudaStream_t)cuda_stream;
     ctx->mem_kind = mem_kind;
     ctx->rank = rank;
@@ -1073,6 +1122,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
                     &ctx->lam1, &ctx->tmpn})
       b->alloc(std::max<int64_t>(n, 1));
     ctx->xx.alloc(std::max<int64_t>(n, 1));
+    ctx->ktyp.alloc(std::max<int64_t>(n, 1));
     ctx->lt.alloc(std::max<int64_t>(n1, 1));
     ctx->ut.alloc(std::max<int64_t>(n1, 1));
     ctx->scal.alloc(8);
@@ -1097,6 +1147,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
                                              ctx->tmpm.p);
         k_row_norms<<<Grn, kThreads, 0, st>>>(n, ctx->KT.ptr, ctx->KT.col, ctx->KT.val, ctx->q.p, ctx->r.p,
                                              mode, ctx->tmpn.p);
+        ctx->allreduce(ctx->tmpn.p, n, mode ? ncclSum : ncclMax);   // column norms over all rows
         k_apply_root<<<Gm, kThreads, 0, st>>>(m, ctx->tmpm.p, ctx->r.p);
         k_apply_root<<<Gn, kThreads, 0, st>>>(n, ctx->tmpn.p, ctx->q.p);
       }
@@ -1143,6 +1194,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
         for (int it = 0; it < 20; ++it) {
           ctx->spmv_store(ctx->K, ctx->tmpn.p, ctx->tmpm.p);
           ctx->spmv_store(ctx->KT, ctx->tmpm.p, ctx->lam0.p);
+          ctx->allreduce(ctx->lam0.p, n, ncclSum);
           k_reduce<<<1, kThreads, 0, st>>>(n, ctx->lam0.p, 1, ctx->scal.p);
           double s2 = 0.0;
           CK(cudaMemcpyAsync(&s2, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1168,6 +1220,8 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
       k_reduce<<<1, kThreads, 0, st>>>(m, ctx->tmpm.p, 2, ctx->scal.p);
       k_reduce<<<1, kThreads, 0, st>>>(n, ctx->ct.p, 0, ctx->scal.p + 1);
       k_reduce<<<1, kThreads, 0, st>>>(m, ctx->ht.p, 0, ctx->scal.p + 2);
+      ctx->allreduce(ctx->scal.p, 1, ncclMax);        // ||K~||_inf over the row shards
+      ctx->allreduce(ctx->scal.p + 2, 1, ncclMax);    // ||h~||_inf
       double hs[3];
       CK(cudaMemcpyAsync(hs, ctx->scal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -1228,7 +1282,7 @@ static void finish_result(pdcs_ctx* ctx, pdcs_result_t* out, double secs) {
 // host synchronises only every check_interval launches (to test termination)
 // or at the end.
 static bool run_steps_graph(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, double time_limit) {
-  if (ctx->timing || std::getenv("PDCS_NO_GRAPH")) return false;
+  if (ctx->timing || ctx->dist || std::getenv("PDCS_NO_GRAPH")) return false;
   ctx->build_graph();
   if (!ctx->gexec) return false;
   auto t0 = std::chrono::steady_clock::now();
@@ -1488,8 +1542,13 @@ void pdcs_destroy(pdcs_ctx* ctx) { delete ctx; }
 
 pdcs_status pdcs_nccl_unique_id(void* out128) {
   if (!out128) return PDCS_ERR_ARG;
-  g_create_error = "NCCL support is not compiled into this build";
-  return PDCS_ERR_NCCL;
+  std::string e;
+  if (!nccl().load(e)) { g_create_error = e; return PDCS_ERR_NCCL; }
+  ncclUniqueId id;
+  const ncclResult_t r = nccl().GetUniqueId(&id);
+  if (r != ncclSuccess) { g_create_error = nccl().GetErrorString(r); return PDCS_ERR_NCCL; }
+  std::memcpy(out128, &id, sizeof(id));
+  return PDCS_OK;
 }
 
 }  // extern "C"

@@ -16,18 +16,29 @@ def _result_dict(r) -> dict:
 class PdcsSolver:
     """create -> set_cones on construction; iterate / solve / kkt / get_iterate after."""
 
-    def __init__(self, prog, device: int = 0, stream=None, **params):
+    def __init__(self, prog, device: int = 0, stream=None, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None, rows=None, **params):
+        """rows=(row_begin, row_end) selects this rank's shard (dist.partition_rows);
+        nccl_id (128 bytes from pdcs_nccl_unique_id on rank 0) enables the
+        NCCL path (also usable with world == 1)."""
+        from . import dist
         self.prog = prog
         self.params = L.pdcs_default_params(**params)
+        r0, r1 = rows if rows is not None else (0, prog.m)
+        self.rows = (r0, r1)
+        sh = dist.shard(prog, r0, r1)
         self._arrays = dict(
-            row_ptr=np.ascontiguousarray(prog.row_ptr, np.int64),
-            col=np.ascontiguousarray(prog.col_idx, np.int32),
-            val=np.ascontiguousarray(prog.vals, np.float64),
-            c=np.ascontiguousarray(prog.c, np.float64), h=np.ascontiguousarray(prog.h, np.float64),
+            row_ptr=sh["row_ptr"], col=np.ascontiguousarray(sh["col"], np.int32),
+            val=np.ascontiguousarray(sh["val"], np.float64),
+            c=np.ascontiguousarray(prog.c, np.float64), h=np.ascontiguousarray(sh["h"], np.float64),
             l=np.ascontiguousarray(prog.l, np.float64), u=np.ascontiguousarray(prog.u, np.float64))
         a = self._arrays
-        self.ctx = L.pdcs_create(prog.m, prog.n, prog.n1, 0, prog.m, a["row_ptr"], a["col"], a["val"],
-                                 a["c"], a["h"], a["l"], a["u"], self.params, device, stream)
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = np.frombuffer(bytes(nccl_id), dtype=np.uint8).copy()
+        self.ctx = L.pdcs_create(prog.m, prog.n, prog.n1, r0, r1, a["row_ptr"], a["col"], a["val"],
+                                 a["c"], a["h"], a["l"], a["u"], self.params, device, stream,
+                                 nccl_unique_id=idbuf, rank=rank, world=world)
         L.pdcs_set_cones(self.ctx, prog.pk, prog.pdim, prog.rk, prog.rdim)
 
     def close(self):
@@ -49,7 +60,7 @@ class PdcsSolver:
 
     def get_iterate(self, which=L.CURRENT, space=L.SCALED):
         x = np.zeros(self.prog.n)
-        y = np.zeros(self.prog.m)
+        y = np.zeros(self.rows[1] - self.rows[0])
         L.pdcs_get_iterate(self.ctx, which, space, x, y)
         return x, y
 
@@ -58,7 +69,7 @@ class PdcsSolver:
                            np.ascontiguousarray(y, np.float64))
 
     def get_scaling(self):
-        r = np.zeros(self.prog.m)
+        r = np.zeros(self.rows[1] - self.rows[0])
         q = np.zeros(self.prog.n)
         L.pdcs_get_scaling(self.ctx, r, q)
         return r, q
@@ -70,7 +81,7 @@ class PdcsSolver:
         return L.pdcs_kernel_times(self.ctx)
 
     def get_state(self):
-        return L.pdcs_get_state(self.ctx, self.prog.n, self.prog.m)
+        return L.pdcs_get_state(self.ctx, self.prog.n, self.rows[1] - self.rows[0])
 
     def set_state(self, st):
         L.pdcs_set_state(self.ctx, st)

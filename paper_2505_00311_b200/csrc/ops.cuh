@@ -610,7 +610,7 @@ __global__ void k_gather_t(int64_t nnz, const int32_t* __restrict__ perm, const 
 __global__ void k_gather_vals(int64_t n, const int32_t* __restrict__ perm, const double* __restrict__ src,
                               double* __restrict__ dst) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
-    dst[p] = src[perm[p]];
+    dst[p] = perm[p] >= 0 ? src[perm[p]] : 0.0;   // -1: quad padding
 }
 __global__ void k_iota(int64_t n, int32_t* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

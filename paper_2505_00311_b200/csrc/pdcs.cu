@@ -81,6 +81,7 @@ int grid_for(int64_t n, int sms, int per_sm = 8) {
 // structure.  perm_* give the CSR position of every entry so that the (scaled)
 // values are gathered on the device afterwards.
 struct TiledHost {
+  std::vector<TBatch> batch;
   std::vector<TWork> work;
   std::vector<TChunk> chunk;
   std::vector<TSeg> seg;
@@ -101,7 +102,7 @@ int tiled_tile_bytes() {
 // lanes per row for a segment with `avg` nonzeros per row: aim for >= ~8 entries
 // per lane so that the unrolled, pipelined loop body is used (PDCS_TILE_LPE overrides)
 int pick_v(double avg) {
-  static const double lpe = std::getenv("PDCS_TILE_LPE") ? std::atof(std::getenv("PDCS_TILE_LPE")) : 4.0;
+  static const double lpe = std::getenv("PDCS_TILE_LPE") ? std::atof(std::getenv("PDCS_TILE_LPE")) : 2.0;
   int v = 1;
   while (v < 32 && avg >= 2.0 * v * lpe) v *= 2;
   return v;
@@ -136,6 +137,7 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
     // segments: direct first (if any), then staged tiles in order
     std::vector<int64_t> staged_tiles;
     int64_t direct_nz = 0;
+    (void)0;
     for (int64_t t : touched) {
       if (cnt[t] >= stage_min) staged_tiles.push_back(t); else direct_nz += cnt[t];
     }
@@ -148,50 +150,101 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
       seg_nz.push_back(cnt[t]);
     }
     const int nseg = (int)seg_nz.size();
-    // row pointers per segment
+    // per-segment per-row counts (staged segments are padded to quads of 4)
+    auto seg_k = [&](int64_t t) { return cnt[t] >= stage_min ? segof[t] : 0; };   // direct is index 0
+    std::vector<int32_t> rc((size_t)nseg * nr, 0);
+    for (int32_t i = 0; i < nr; ++i)
+      for (int64_t p = ptr[r0 + i]; p < ptr[r0 + i + 1]; ++p) rc[(size_t)seg_k(col[p] / T) * nr + i]++;
     std::vector<int64_t> rpbase(nseg);
     for (int k = 0; k < nseg; ++k) {
-      rpbase[k] = (int64_t)H.rowptr.size();
-      H.rowptr.resize(H.rowptr.size() + nr + 1, 0);
       TSeg& S = H.seg[s_begin + k];
+      const bool stg = S.tile >= 0;
+      rpbase[k] = (int64_t)H.rowptr.size();
       S.rp = rpbase[k];
-      S.V = pick_v((double)seg_nz[k] / nr);
-      S.nz = S.tile >= 0 ? (int64_t)H.col_s.size() : (int64_t)H.col_d.size();
-      if (S.tile >= 0) { H.col_s.resize(H.col_s.size() + seg_nz[k]); H.perm_s.resize(H.col_s.size()); }
-      else { H.col_d.resize(H.col_d.size() + seg_nz[k]); H.perm_d.resize(H.col_d.size()); }
+      H.rowptr.resize(H.rowptr.size() + nr + 1, 0);
+      int64_t units = 0;                                  // quads (staged) or entries (direct)
+      for (int32_t i = 0; i < nr; ++i) {
+        const int32_t u = stg ? (rc[(size_t)k * nr + i] + 3) / 4 : rc[(size_t)k * nr + i];
+        H.rowptr[rpbase[k] + i + 1] = H.rowptr[rpbase[k] + i] + u;
+        units += u;
+      }
+      S.V = pick_v(stg ? (double)units / nr : (double)seg_nz[k] / nr);
+      if (stg) {
+        // segments start on an even quad: 16-B aligned TMA sources for the column ids
+        H.col_s.resize((H.col_s.size() + 7) & ~(size_t)7, 0);
+        H.perm_s.resize(H.col_s.size(), -1);
+        S.nz = (int64_t)H.col_s.size();
+        H.col_s.resize(H.col_s.size() + 4 * units, 0);
+        H.perm_s.resize(H.col_s.size(), -1);
+      } else {
+        S.nz = (int64_t)H.col_d.size();
+        H.col_d.resize(H.col_d.size() + units);
+        H.perm_d.resize(H.col_d.size());
+      }
     }
-    auto seg_k = [&](int64_t t) { return cnt[t] >= stage_min ? segof[t] : 0; };   // direct is index 0
-    for (int32_t i = 0; i < nr; ++i)
-      for (int64_t p = ptr[r0 + i]; p < ptr[r0 + i + 1]; ++p) H.rowptr[rpbase[seg_k(col[p] / T)] + i + 1]++;
-    for (int k = 0; k < nseg; ++k)
-      for (int32_t i = 0; i < nr; ++i) H.rowptr[rpbase[k] + i + 1] += H.rowptr[rpbase[k] + i];
-    std::vector<int32_t> fill(nseg * (size_t)nr);
+    std::vector<int32_t> fill((size_t)nseg * nr, 0);
     for (int32_t i = 0; i < nr; ++i)
       for (int64_t p = ptr[r0 + i]; p < ptr[r0 + i + 1]; ++p) {
         const int64_t t = col[p] / T;
         const int k = seg_k(t);
         const TSeg& S = H.seg[s_begin + k];
-        const int64_t q = S.nz + H.rowptr[rpbase[k] + i] + fill[(size_t)k * nr + i]++;
-        if (S.tile >= 0) { H.col_s[q] = (uint16_t)(col[p] - t * T); H.perm_s[q] = (int32_t)p; H.staged++; }
-        else { H.col_d[q] = col[p]; H.perm_d[q] = (int32_t)p; }
+        const int32_t f = fill[(size_t)k * nr + i]++;
+        if (S.tile >= 0) {
+          const int64_t q = S.nz + 4 * (int64_t)H.rowptr[rpbase[k] + i] + f;
+          H.col_s[q] = (uint16_t)(col[p] - t * T);
+          H.perm_s[q] = (int32_t)p;
+          H.staged++;
+        } else {
+          const int64_t q = S.nz + H.rowptr[rpbase[k] + i] + f;
+          H.col_d[q] = col[p];
+          H.perm_d[q] = (int32_t)p;
+        }
       }
-    // work items: consecutive segments up to group_nz nonzeros
+    // work items: consecutive segments up to group_nz nonzeros; the staged
+    // segments of an item are cut into TMA batches of <= kBQ quads
+    auto emit_item = [&](int32_t gg, int32_t sa, int32_t sb) {
+      const int32_t b0 = (int32_t)H.batch.size();
+      int32_t ord = -1;
+      for (int32_t si = sa; si < sb; ++si) {
+        const TSeg& S = H.seg[si];
+        if (S.tile < 0) continue;
+        ++ord;
+        const int32_t* rp = H.rowptr.data() + S.rp;
+        int first = 1;
+        int32_t ra = 0, qa = rp[0];
+        auto emit = [&](int32_t r_a, int32_t r_b, int32_t q_a, int32_t q_b) {
+          if (q_b > q_a) { H.batch.push_back(TBatch{si, r_a, r_b, q_a, q_b, first, ord, 0}); first = 0; }
+        };
+        for (int32_t r = 0; r < nr; ++r) {
+          const int32_t rq0 = rp[r], rq1 = rp[r + 1];
+          while (rq1 - qa > kBQ) {
+            if (rq0 > qa) { emit(ra, r, qa, rq0); qa = rq0; ra = r; }
+            else { emit(r, r + 1, qa, qa + kBQ); qa += kBQ; ra = r; }
+          }
+        }
+        emit(ra, nr, qa, rp[nr]);
+      }
+      H.work.push_back(TWork{(int32_t)H.chunk.size(), gg, sa, sb, b0, (int32_t)H.batch.size()});
+    };
     int32_t g = 0;
     int64_t acc = 0;
     int32_t ws = s_begin;
     for (int k = 0; k < nseg; ++k) {
       acc += seg_nz[k];
       if (acc >= group_nz || k == nseg - 1) {
-        H.work.push_back(TWork{(int32_t)H.chunk.size(), g++, ws, s_begin + k + 1});
+        emit_item(g++, ws, s_begin + k + 1);
         ws = s_begin + k + 1;
         acc = 0;
       }
     }
-    if (nseg == 0) H.work.push_back(TWork{(int32_t)H.chunk.size(), g++, s_begin, s_begin});
+    if (nseg == 0) emit_item(g++, s_begin, s_begin);
     H.chunk.push_back(TChunk{r0, nr, g, H.scratch});
     H.scratch += (int64_t)g * nr * elem;
     for (int64_t t : touched) { cnt[t] = 0; segof[t] = -1; }
   }
+  H.col_s.resize(H.col_s.size() + 8, 0);      // TMA column-id copies may read one quad past the end
+  H.rowptr.resize(H.rowptr.size() + 8, 0);    // TMA row-pointer slices are rounded up to 16 B
+  H.perm_s.resize(H.col_s.size(), -1);
 }
 
 }  // namespace
@@ -231,6 +284,8 @@ struct pdcs_ctx {
     bool on = false;
     TiledMat M;
     DBuf<TWork> work;
+    DBuf<TBatch> batch;
+    bool tma = true;
     DBuf<TChunk> chunk;
     DBuf<TSeg> seg;
     DBuf<int32_t> rowptr, col_d;
@@ -401,10 +456,7 @@ struct pdcs_ctx {
     run_blocks(true, bargs(true, BOP_TRIAL_PRIMAL), false, 0);
     EpiDualTrial e{y.p, ht.p, rk.p, kxh.p, kxd.p, yh.p, 0.0, 0};
     if (tK.on) {
-      launch("tiled_K_partial", [&] {
-        k_tiled_partial<2><<<tK.g_partial, kTThreads, tiled_smem(2), st>>>(
-            tK.M, reinterpret_cast<const double*>(xx.p), tK.scratch.p, ctl, 1);
-      });
+      tiled_partial("tiled_K_partial", tK, 2, reinterpret_cast<const double*>(xx.p), 1);
       launch("spmv_K_dual", [&] {
         k_tiled_combine<EpiDualTrial, 2><<<tK.g_combine, kThreads, 0, st>>>(tK.M, tK.scratch.p, e, ctl, tpart.p,
                                                                           slot_spmv);
@@ -438,9 +490,7 @@ struct pdcs_ctx {
     }
     EpiHalpernX e{xh.p, x0.p, x.p, kty.p, xsum.p, 0, 0, 0, 0, 0};
     if (tKT.on) {
-      launch("tiled_KT_partial", [&] {
-        k_tiled_partial<1><<<tKT.g_partial, kTThreads, tiled_smem(1), st>>>(tKT.M, y.p, tKT.scratch.p, ctl, 2);
-      });
+      tiled_partial("tiled_KT_partial", tKT, 1, y.p, 2);
       launch("spmv_KT_halpern", [&] {
         k_tiled_combine<EpiHalpernX, 1><<<tKT.g_combine, kThreads, 0, st>>>(tKT.M, tKT.scratch.p, e, ctl, nullptr, 0);
       });
@@ -583,6 +633,22 @@ struct pdcs_ctx {
     }
   }
 
+  static size_t tma_smem(int elem) {
+    return 2 * (size_t)tiled_tile_bytes() + (size_t)kNST * kBQ * 32 + (size_t)kNST * (kBQ + 2) * 8 +
+           (size_t)kNST * kBR * 4 + (size_t)kTRows * elem * sizeof(double);
+  }
+  // launch the partial products of a tiled matrix (TMA pipeline or the plain kernel)
+  void tiled_partial(const char* name, TiledDev& D, int elem, const double* xin, int guard) {
+    launch(name, [&] {
+      if (elem == 2) {
+        if (D.tma) k_tiled_tma<2><<<D.g_partial, kTThreads, tma_smem(2), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        else k_tiled_partial<2><<<D.g_partial, kTThreads, tiled_smem(2), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+      } else {
+        if (D.tma) k_tiled_tma<1><<<D.g_partial, kTThreads, tma_smem(1), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        else k_tiled_partial<1><<<D.g_partial, kTThreads, tiled_smem(1), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+      }
+    });
+  }
   static size_t tiled_smem(int elem) { return (size_t)tiled_tile_bytes() + (size_t)kTRows * elem * sizeof(double); }
 
   // Build the tiled copy of a CSR (structure on the host, scaled values on the device).
@@ -596,6 +662,7 @@ struct pdcs_ctx {
     D.on = want && H.nnz > 0;
     if (!D.on) return;
     upload(D.work, H.work, st);
+    upload(D.batch, H.batch, st);
     upload(D.chunk, H.chunk, st);
     upload(D.seg, H.seg, st);
     upload(D.rowptr, H.rowptr, st);
@@ -620,13 +687,21 @@ struct pdcs_ctx {
     M.T = H.T; M.elem = elem;
     M.work = D.work.p; M.chunk = D.chunk.p; M.seg = D.seg.p; M.rowptr = D.rowptr.p;
     M.val_s = D.val_s.p; M.col_s = D.col_s.p; M.val_d = D.val_d.p; M.col_d = D.col_d.p;
+    M.batch = D.batch.p;
+    // TMA-pipelined variant (k_tiled_tma) is opt-in: on B200 it measured slower than
+    // the 4-CTA/SM register-streaming kernel, PDCS_TMA=1 enables it.
+    D.tma = std::getenv("PDCS_TMA") && std::atoi(std::getenv("PDCS_TMA")) != 0;
     int occ = 1;
     if (elem == 2) {
       CK(cudaFuncSetAttribute(k_tiled_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(2)));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<2>, kTThreads, tiled_smem(2)));
+      CK(cudaFuncSetAttribute(k_tiled_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(2)));
+      if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<2>, kTThreads, tma_smem(2)));
+      else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<2>, kTThreads, tiled_smem(2)));
     } else {
       CK(cudaFuncSetAttribute(k_tiled_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(1)));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<1>, kTThreads, tiled_smem(1)));
+      CK(cudaFuncSetAttribute(k_tiled_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(1)));
+      if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<1>, kTThreads, tma_smem(1)));
+      else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<1>, kTThreads, tiled_smem(1)));
     }
     D.g_partial = (int)std::max<int64_t>(1, std::min<int64_t>(M.nwork, (int64_t)sms * std::max(occ, 1)));
     int64_t slabs = 0;
@@ -637,7 +712,7 @@ struct pdcs_ctx {
     if (!env) {
       const DevCsr& A = elem == 2 ? K : KT;
       DBuf<double> xin, out;
-      xin.alloc(std::max<int64_t>(nvec * elem, 1));
+      xin.alloc(std::max<int64_t>(nvec * elem, 1) + 2);
       out.alloc(std::max<int64_t>(rows, 1));
       k_fill<<<grid_for(nvec * elem, sms), kThreads, 0, st>>>(nvec * elem, 1.0, xin.p);
       cudaEvent_t a, b;
@@ -654,11 +729,11 @@ struct pdcs_ctx {
       };
       auto run_tiled = [&] {
         if (elem == 2) {
-          k_tiled_partial<2><<<D.g_partial, kTThreads, tiled_smem(2), st>>>(M, xin.p, D.scratch.p, ctl, 0);
+          tiled_partial("autotune", D, 2, xin.p, 0);
           EpiStore2 e{out.p};
           k_tiled_combine<EpiStore2, 2><<<D.g_combine, kThreads, 0, st>>>(M, D.scratch.p, e, ctl, nullptr, 0);
         } else {
-          k_tiled_partial<1><<<D.g_partial, kTThreads, tiled_smem(1), st>>>(M, xin.p, D.scratch.p, ctl, 0);
+          tiled_partial("autotune", D, 1, xin.p, 0);
           EpiStore e{out.p};
           k_tiled_combine<EpiStore, 1><<<D.g_combine, kThreads, 0, st>>>(M, D.scratch.p, e, ctl, nullptr, 0);
         }
@@ -1113,7 +1188,8 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     CK(cudaMemsetAsync(ctx->kpart.p, 0, ks * kKAcc * sizeof(double), st));
     ctx->gbuf.alloc(4 * (size_t)ctx->sms * 8);
     // ---- vectors
-    for (auto* b : {&ctx->r, &ctx->onesm, &ctx->ht, &ctx->y, &ctx->yh, &ctx->y0, &ctx->ysum,
+    ctx->y.alloc(m + 2);   // +pad: TMA tile copies round up to 16 B
+    for (auto* b : {&ctx->r, &ctx->onesm, &ctx->ht, &ctx->yh, &ctx->y0, &ctx->ysum,
                     &ctx->kxh, &ctx->kxd, &ctx->ya, &ctx->kxa, &ctx->by, &ctx->candy, &ctx->res0,
                     &ctx->res1, &ctx->tmpm})
       b->alloc(std::max<int64_t>(m, 1));
@@ -1121,7 +1197,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
                     &ctx->ktyh, &ctx->xa, &ctx->ktya, &ctx->bx, &ctx->candx, &ctx->lam0,
                     &ctx->lam1, &ctx->tmpn})
       b->alloc(std::max<int64_t>(n, 1));
-    ctx->xx.alloc(std::max<int64_t>(n, 1));
+    ctx->xx.alloc(std::max<int64_t>(n, 1) + 1);
     ctx->ktyp.alloc(std::max<int64_t>(n, 1));
     ctx->lt.alloc(std::max<int64_t>(n1, 1));
     ctx->ut.alloc(std::max<int64_t>(n1, 1));

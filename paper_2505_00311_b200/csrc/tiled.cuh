@@ -9,7 +9,8 @@
 // Format (built at setup): rows are cut into chunks of <= kTRows
 // rows; the gathered vector into tiles of T elements (64 KB).  For every
 // (chunk, tile) pair with enough nonzeros the entries form a *staged segment*
-// (tile-local uint16 column ids, 10 bytes per nonzero instead of 12); the rest
+// (tile-local uint16 column ids, 10 bytes per nonzero instead of 12, stored in
+// zero-padded quads of 4 entries with row pointers counted in quads); the rest
 // of a chunk's entries form one *direct segment* (int32 global ids, gathered
 // from L2).  Each segment is a small CSR over the chunk's rows.  A work item is
 // (chunk, group of consecutive segments); it stages each tile in shared memory,
@@ -30,7 +31,7 @@ struct TSeg {
   int32_t tile;      // >= 0: staged tile index; -1: direct segment
   int32_t V;         // lanes per row (1, 2, 4, 8, 16, 32)
   int64_t rp;        // offset of the segment's row pointers (nrows + 1 entries)
-  int64_t nz;        // offset of the segment's entries in its pool
+  int64_t nz;        // offset of the segment's entries in its pool (staged: in entries, = 4 * quads)
 };
 struct TChunk {
   int64_t row0;
@@ -39,8 +40,17 @@ struct TChunk {
   int64_t scratch;   // offset (in doubles) of the chunk's partials: ngroups * nrows * ELEM
 };
 struct TWork {
-  int32_t chunk, group, s0, s1;
+  int32_t chunk, group, s0, s1;   // segments [s0, s1): direct ones run first, staged via batches
+  int32_t b0, b1;                 // TMA batches [b0, b1) of the staged segments
 };
+// A TMA batch: quads [qa, qb) (segment-relative, qb - qa <= kBQ) of rows [ra, rb)
+// of segment `seg`; `first` marks the first batch of that segment in the item.
+struct TBatch {
+  int32_t seg, ra, rb, qa, qb, first, ord, pad;   // ord: segment ordinal within the work item
+};
+constexpr int kBQ = 1024;             // quads per TMA batch (32 KB values + 8 KB column ids)
+constexpr int kBR = kTRows + 8;       // row pointers per TMA batch (16-B aligned slice)
+constexpr int kNST = 3;               // TMA pipeline stages
 struct TiledMat {
   int64_t m = 0, nvec = 0, nwork = 0, nchunk = 0;
   int32_t T = 0, elem = 1;
@@ -52,48 +62,112 @@ struct TiledMat {
   const uint16_t* col_s = nullptr;
   const double* val_d = nullptr;
   const int32_t* col_d = nullptr;
+  const TBatch* batch = nullptr;
 };
 
-// Dot of one segment row with V lanes; xs is the gathered source (shared tile or
-// global vector), ELEM 1 or 2 (interleaved pairs).
-template <int V, int ELEM, bool STAGED>
-__device__ __forceinline__ void seg_row_dot(const double* __restrict__ val, const uint16_t* __restrict__ c16,
-                                            const int32_t* __restrict__ c32, const double* xs, int32_t b,
-                                            int32_t e, int lane, double& s1, double& s2) {
-  constexpr int U = 4;
+// Shared-memory loads with 32-bit shared addresses (the tile pointer would
+// otherwise reach the loop as a generic pointer: 64-bit generic loads).
+__device__ __forceinline__ double2 lds_v2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+// Streaming 16-byte loads of the matrix (no L1 allocation).
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+// Staged segment row, quad layout: the row's entries are packed in quads of 4
+// (32 B of values, 8 B of uint16 tile-local column ids, zero padded), so every
+// load a lane issues is a full 16/8-byte vector and a warp touches whole
+// sectors.  Lane l of the V-lane group takes quads qb+l, qb+l+V, ...
+template <int V, int ELEM>
+__device__ __forceinline__ void seg_row_dot_quad(const double* __restrict__ val4, const uint16_t* __restrict__ col4,
+                                                 uint32_t xs_s, int32_t qb, int32_t qe, int lane, double& s1,
+                                                 double& s2) {
+  constexpr int U = 2;   // quads per lane per batch
   s1 = 0.0;
   s2 = 0.0;
-  int32_t p = b + lane;
-  for (; p + (U - 1) * V < e; p += U * V) {
+  for (int32_t q0 = qb + lane; q0 < qe; q0 += U * V) {
+    double a[U][4];
+    uint32_t c[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t q = q0 + u * V;
+      if (q < qe) {
+        const double2 v01 = ld_stream2(val4 + 4 * (int64_t)q);
+        const double2 v23 = ld_stream2(val4 + 4 * (int64_t)q + 2);
+        const uint2 cc = ld_stream_u2(col4 + 4 * (int64_t)q);
+        a[u][0] = v01.x; a[u][1] = v01.y; a[u][2] = v23.x; a[u][3] = v23.y;
+        c[u][0] = cc.x & 0xffffu; c[u][1] = cc.x >> 16; c[u][2] = cc.y & 0xffffu; c[u][3] = cc.y >> 16;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { a[u][k] = 0.0; c[u][k] = 0u; }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (ELEM == 2) {
+          const double2 v = lds_v2(xs_s + c[u][k] * 16u);
+          s1 += a[u][k] * v.x;
+          s2 += a[u][k] * v.y;
+        } else {
+          s1 += a[u][k] * lds_f64(xs_s + c[u][k] * 8u);
+        }
+      }
+  }
+  if (V > 1) {
+#pragma unroll
+    for (int o = V / 2; o >= 1; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o, V);
+      if (ELEM == 2) s2 += __shfl_xor_sync(0xffffffffu, s2, o, V);
+    }
+  }
+}
+
+// Direct segment row (global gathers, int32 column ids): predicated batches of
+// U entries per lane, all loads of a batch issued before any gather.
+template <int V, int ELEM>
+__device__ __forceinline__ void seg_row_dot_direct(const double* __restrict__ val, const int32_t* __restrict__ c32,
+                                                   const double* __restrict__ xs, int32_t b, int32_t e, int lane,
+                                                   double& s1, double& s2) {
+  constexpr int U = 8;
+  s1 = 0.0;
+  s2 = 0.0;
+  for (int32_t p = b + lane; p < e; p += U * V) {
     int32_t c[U];
     double a[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      a[k] = ld_stream(val + p + k * V);
-      c[k] = STAGED ? (int32_t)__ldg(c16 + p + k * V) : ld_stream(c32 + p + k * V);
+      const int32_t q = p + k * V;
+      const bool ok = q < e;
+      a[k] = ok ? ld_stream(val + q) : 0.0;
+      c[k] = ok ? ld_stream(c32 + q) : 0;
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       if (ELEM == 2) {
-        const double2 v = STAGED ? reinterpret_cast<const double2*>(xs)[c[k]]
-                                 : __ldg(reinterpret_cast<const double2*>(xs) + c[k]);
+        const double2 v = __ldg(reinterpret_cast<const double2*>(xs) + c[k]);
         s1 += a[k] * v.x;
         s2 += a[k] * v.y;
       } else {
-        s1 += a[k] * (STAGED ? xs[c[k]] : __ldg(xs + c[k]));
+        s1 += a[k] * __ldg(xs + c[k]);
       }
-    }
-  }
-  for (; p < e; p += V) {
-    const double a = ld_stream(val + p);
-    const int32_t c = STAGED ? (int32_t)__ldg(c16 + p) : ld_stream(c32 + p);
-    if (ELEM == 2) {
-      const double2 v = STAGED ? reinterpret_cast<const double2*>(xs)[c]
-                               : __ldg(reinterpret_cast<const double2*>(xs) + c);
-      s1 += a * v.x;
-      s2 += a * v.y;
-    } else {
-      s1 += a * (STAGED ? xs[c] : __ldg(xs + c));
     }
   }
   if (V > 1) {
@@ -107,7 +181,7 @@ __device__ __forceinline__ void seg_row_dot(const double* __restrict__ val, cons
 
 template <int V, int ELEM>
 __device__ __forceinline__ void seg_rows(const TiledMat& M, const TSeg& S, const TChunk& C,
-                                         const double* xs, bool staged, double* acc) {
+                                         const double* xs, uint32_t xs_s, bool staged, double* acc) {
   const int G = blockDim.x / V;
   const int g = threadIdx.x / V, lane = threadIdx.x % V;
   const int32_t* rp = M.rowptr + S.rp;
@@ -116,8 +190,8 @@ __device__ __forceinline__ void seg_rows(const TiledMat& M, const TSeg& S, const
     double s1 = 0.0, s2 = 0.0;
     int32_t b = 0, e = 0;
     if (r < C.nrows) { b = __ldg(rp + r); e = __ldg(rp + r + 1); }
-    if (staged) seg_row_dot<V, ELEM, true>(M.val_s + S.nz, M.col_s + S.nz, nullptr, xs, b, e, lane, s1, s2);
-    else seg_row_dot<V, ELEM, false>(M.val_d + S.nz, nullptr, M.col_d + S.nz, xs, b, e, lane, s1, s2);
+    if (staged) seg_row_dot_quad<V, ELEM>(M.val_s + S.nz, M.col_s + S.nz, xs_s, b, e, lane, s1, s2);
+    else seg_row_dot_direct<V, ELEM>(M.val_d + S.nz, M.col_d + S.nz, xs, b, e, lane, s1, s2);
     if (lane == 0 && r < C.nrows) {
       acc[r * ELEM] += s1;
       if (ELEM == 2) acc[r * ELEM + 1] += s2;
@@ -153,16 +227,199 @@ __global__ void __launch_bounds__(kTThreads) k_tiled_partial(TiledMat M, const d
         if ((len & 1) && threadIdx.x == 0) tile[len - 1] = __ldg(x + base * ELEM + len - 1);
         __syncthreads();
       }
-      const double* xs = staged ? tile : x;
+      const uint32_t xs_s = (uint32_t)__cvta_generic_to_shared(tile);
       switch (S.V) {
-        case 1: seg_rows<1, ELEM>(M, S, C, xs, staged, acc); break;
-        case 2: seg_rows<2, ELEM>(M, S, C, xs, staged, acc); break;
-        case 4: seg_rows<4, ELEM>(M, S, C, xs, staged, acc); break;
-        case 8: seg_rows<8, ELEM>(M, S, C, xs, staged, acc); break;
-        case 16: seg_rows<16, ELEM>(M, S, C, xs, staged, acc); break;
-        default: seg_rows<32, ELEM>(M, S, C, xs, staged, acc); break;
+        case 1: seg_rows<1, ELEM>(M, S, C, x, xs_s, staged, acc); break;
+        case 2: seg_rows<2, ELEM>(M, S, C, x, xs_s, staged, acc); break;
+        case 4: seg_rows<4, ELEM>(M, S, C, x, xs_s, staged, acc); break;
+        case 8: seg_rows<8, ELEM>(M, S, C, x, xs_s, staged, acc); break;
+        case 16: seg_rows<16, ELEM>(M, S, C, x, xs_s, staged, acc); break;
+        default: seg_rows<32, ELEM>(M, S, C, x, xs_s, staged, acc); break;
       }
       __syncthreads();
+    }
+    double* out = scratch + C.scratch + (int64_t)W.group * C.nrows * ELEM;
+    for (int i = threadIdx.x; i < C.nrows * ELEM; i += blockDim.x) out[i] = acc[i];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ TMA pipeline
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA), completion counted on `bar` (bytes % 16 == 0)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int V, int ELEM>
+__device__ __forceinline__ void batch_rows(const TiledMat& M, const TSeg& S, const TBatch& B, uint32_t tile_s,
+                                           const double* sval, const uint16_t* scol, int32_t qcopy,
+                                           const int32_t* rp, double* acc) {
+  const int G = blockDim.x / V;
+  const int g = threadIdx.x / V, lane = threadIdx.x % V;
+  for (int rb = B.ra; rb < B.rb; rb += G) {              // uniform trip count per warp
+    const int r = rb + g;
+    double s1 = 0.0, s2 = 0.0;
+    if (r < B.rb) {
+      const int32_t qb = max(rp[r], B.qa), qe = min(rp[r + 1], B.qb);
+      for (int32_t q = qb + lane; q < qe; q += V) {
+        const int32_t l = q - qcopy;
+        const double2 v01 = *reinterpret_cast<const double2*>(sval + 4 * l);
+        const double2 v23 = *reinterpret_cast<const double2*>(sval + 4 * l + 2);
+        const uint2 cc = *reinterpret_cast<const uint2*>(scol + 4 * l);
+        const uint32_t c0 = cc.x & 0xffffu, c1 = cc.x >> 16, c2 = cc.y & 0xffffu, c3 = cc.y >> 16;
+        if (ELEM == 2) {
+          const double2 x0 = lds_v2(tile_s + c0 * 16u), x1 = lds_v2(tile_s + c1 * 16u);
+          const double2 x2 = lds_v2(tile_s + c2 * 16u), x3 = lds_v2(tile_s + c3 * 16u);
+          s1 += v01.x * x0.x; s2 += v01.x * x0.y;
+          s1 += v01.y * x1.x; s2 += v01.y * x1.y;
+          s1 += v23.x * x2.x; s2 += v23.x * x2.y;
+          s1 += v23.y * x3.x; s2 += v23.y * x3.y;
+        } else {
+          s1 += v01.x * lds_f64(tile_s + c0 * 8u);
+          s1 += v01.y * lds_f64(tile_s + c1 * 8u);
+          s1 += v23.x * lds_f64(tile_s + c2 * 8u);
+          s1 += v23.y * lds_f64(tile_s + c3 * 8u);
+        }
+      }
+    }
+    if (V > 1) {
+#pragma unroll
+      for (int o = V / 2; o >= 1; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o, V);
+        if (ELEM == 2) s2 += __shfl_xor_sync(0xffffffffu, s2, o, V);
+      }
+    }
+    if (lane == 0 && r < B.rb) {
+      acc[r * ELEM] += s1;
+      if (ELEM == 2) acc[r * ELEM + 1] += s2;
+    }
+  }
+}
+
+// Partial products with the staged segments streamed by TMA: thread 0 keeps
+// kNST batches (values + column ids, and the segment's vector tile) in flight;
+// all warps consume from shared memory.  Direct segments run first from global.
+template <int ELEM>
+__global__ void __launch_bounds__(kTThreads) k_tiled_tma(TiledMat M, const double* __restrict__ x,
+                                                         double* __restrict__ scratch, const Ctl* ctl, int guard) {
+  if (guard >= 1 && ctl->status != 4) return;
+  if (guard == 2 && !ctl->accepted) return;
+  extern __shared__ __align__(128) double smem[];
+  const int tile_doubles = M.T * ELEM;
+  double* tiles = smem;                                       // 2 * tile_doubles
+  double* vals = tiles + 2 * tile_doubles;                    // kNST * kBQ * 4
+  uint16_t* cols = reinterpret_cast<uint16_t*>(vals + kNST * kBQ * 4);   // kNST * kBQ * 4 (+ 8 pad)
+  int32_t* rps = reinterpret_cast<int32_t*>(cols + kNST * (kBQ + 2) * 4);  // kNST * kBR
+  double* acc = reinterpret_cast<double*>(rps + kNST * kBR);               // kTRows * ELEM
+  __shared__ __align__(8) uint64_t full[kNST];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kNST; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t uses[kNST] = {0, 0, 0};   // completed phases per stage (thread 0 and consumers agree)
+  for (int64_t w = blockIdx.x; w < M.nwork; w += gridDim.x) {
+    const TWork W = M.work[w];
+    const TChunk C = M.chunk[W.chunk];
+    for (int i = threadIdx.x; i < C.nrows * ELEM; i += blockDim.x) acc[i] = 0.0;
+    __syncthreads();
+    // direct segments (global gathers)
+    for (int s = W.s0; s < W.s1; ++s) {
+      const TSeg S = M.seg[s];
+      if (S.tile >= 0) continue;
+      switch (S.V) {
+        case 1: seg_rows<1, ELEM>(M, S, C, x, 0u, false, acc); break;
+        case 2: seg_rows<2, ELEM>(M, S, C, x, 0u, false, acc); break;
+        case 4: seg_rows<4, ELEM>(M, S, C, x, 0u, false, acc); break;
+        case 8: seg_rows<8, ELEM>(M, S, C, x, 0u, false, acc); break;
+        case 16: seg_rows<16, ELEM>(M, S, C, x, 0u, false, acc); break;
+        default: seg_rows<32, ELEM>(M, S, C, x, 0u, false, acc); break;
+      }
+      __syncthreads();
+    }
+    const int nb = W.b1 - W.b0;
+    auto issue = [&](int j) {
+      const TBatch B = M.batch[W.b0 + j];
+      const TSeg S = M.seg[B.seg];
+      const int st = j % kNST;
+      const int32_t qc = B.qa & ~1;                        // 16-B aligned column-id copy
+      const uint32_t vbytes = (uint32_t)(B.qb - B.qa) * 32u;
+      const uint32_t cbytes = (uint32_t)(((B.qb - qc + 1) & ~1) * 8);
+      uint32_t tbytes = 0;
+      if (B.first) {
+        const int64_t base = (int64_t)S.tile * M.T;
+        const int64_t len = (M.nvec - base < M.T ? M.nvec - base : M.T) * ELEM * 8;
+        tbytes = (uint32_t)((len + 15) & ~15);
+      }
+      const int64_t r0 = (S.rp + B.ra) & ~(int64_t)3;      // 16-B aligned row-pointer slice
+      const uint32_t rbytes = (uint32_t)(((S.rp + B.rb + 1 - r0) * 4 + 15) & ~15);
+      mbar_expect_tx(&full[st], vbytes + cbytes + tbytes + rbytes);
+      tma_load_1d(rps + (size_t)st * kBR, M.rowptr + r0, rbytes, &full[st]);
+      tma_load_1d(vals + (size_t)st * kBQ * 4, M.val_s + S.nz + 4 * (int64_t)B.qa, vbytes, &full[st]);
+      tma_load_1d(cols + (size_t)st * (kBQ + 2) * 4, M.col_s + S.nz + 4 * (int64_t)qc, cbytes, &full[st]);
+      if (B.first)
+        tma_load_1d(tiles + (size_t)(B.ord & 1) * tile_doubles, x + (int64_t)S.tile * M.T * ELEM, tbytes,
+                    &full[st]);
+    };
+    // thread 0 issues batch j when a stage is free (j <= i + kNST) and the tile
+    // buffer it opens is free: segment ordinal ord_j <= ord(oldest unfinished) + 1
+    int next = 0;
+    auto pump = [&](int oldest) {
+      if (threadIdx.x != 0) return;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int oord = oldest < nb ? M.batch[W.b0 + oldest].ord : 0x7fffffff;
+      while (next < nb && next < oldest + kNST) {
+        const TBatch Bn = M.batch[W.b0 + next];
+        if (Bn.first && Bn.ord > oord + 1) break;
+        issue(next);
+        ++next;
+      }
+    };
+    pump(0);
+    for (int i = 0; i < nb; ++i) {
+      const TBatch B = M.batch[W.b0 + i];
+      const int st = i % kNST;
+      mbar_wait(&full[st], uses[st] & 1u);
+      ++uses[st];
+      const TSeg S = M.seg[B.seg];
+      const uint32_t tile_s = smem_u32(tiles + (size_t)(B.ord & 1) * tile_doubles);
+      const double* sv = vals + (size_t)st * kBQ * 4;
+      const uint16_t* sc = cols + (size_t)st * (kBQ + 2) * 4;
+      const int32_t qc = B.qa & ~1;
+      const double* svb = sv - 4 * (B.qa - qc);            // values were copied from qa
+      // row pointers were copied from (S.rp + ra) & ~3: index them by chunk row
+      const int32_t* rpb = rps + (size_t)st * kBR - ((S.rp + B.ra) & ~(int64_t)3) + S.rp;
+      switch (S.V) {
+        case 1: batch_rows<1, ELEM>(M, S, B, tile_s, svb, sc, qc, rpb, acc); break;
+        case 2: batch_rows<2, ELEM>(M, S, B, tile_s, svb, sc, qc, rpb, acc); break;
+        case 4: batch_rows<4, ELEM>(M, S, B, tile_s, svb, sc, qc, rpb, acc); break;
+        case 8: batch_rows<8, ELEM>(M, S, B, tile_s, svb, sc, qc, rpb, acc); break;
+        case 16: batch_rows<16, ELEM>(M, S, B, tile_s, svb, sc, qc, rpb, acc); break;
+        default: batch_rows<32, ELEM>(M, S, B, tile_s, svb, sc, qc, rpb, acc); break;
+      }
+      __syncthreads();                       // stage st (and a finished segment's tile) is free
+      pump(i + 1);
     }
     double* out = scratch + C.scratch + (int64_t)W.group * C.nrows * ELEM;
     for (int i = threadIdx.x; i < C.nrows * ELEM; i += blockDim.x) out[i] = acc[i];

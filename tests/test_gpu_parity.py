@@ -292,6 +292,22 @@ def test_tiled_one_step_and_shadow(P, tiled_env, seed):
     assert worst <= TOL, worst
 
 
+def test_tiled_tma_pipeline_parity(P, tiled_env, monkeypatch):
+    """The TMA-pipelined tiled kernel (cp.async.bulk + mbarrier ring, opt-in)."""
+    monkeypatch.setenv("PDCS_TMA", "1")
+    prog = mixed(45, m=900, n1=120, n2=500, soc_dims=(3, 120), row_len=(20, 90))
+    worst = _shadow(P, prog, 120)
+    assert worst <= TOL, worst
+    prog = gen_lasso(400, 300, 0.2, seed=6)
+    g = P.PdcsSolver(prog, vanilla_pdhg=1)
+    o = O.OracleSolver(prog, vanilla_pdhg=1)
+    g.iterate(200)
+    o.iterate(200)
+    xg, yg = g.get_iterate(P.CURRENT)
+    xo, yo = o.get_iterate(0)
+    assert parity(xg, yg, xo, yo) <= TOL
+
+
 def test_tiled_lasso_vanilla_parity(P, tiled_env):
     prog = gen_lasso(400, 300, 0.2, seed=5)
     g = P.PdcsSolver(prog, vanilla_pdhg=1)

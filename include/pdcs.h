@@ -207,8 +207,11 @@ void pdcs_enable_timing(pdcs_ctx *ctx, int on);
 
 /* Control-state snapshot (diagnostics / decision-trace comparison).  Fills up
  * to cap doubles: eta, omega, beta, k, total, trials, restarts, e_anchor, W,
- * eta_init, kkt_cur[5], kkt_avg[5], e_prev, best_e, use_avg, restart flag.
- * Returns the number of values written. */
+ * eta_init, kkt_cur[5], kkt_avg[5], e_prev, best_e, use_avg, restart flag,
+ * last line-search numerator and cross term, then setup diagnostics: tiled_K
+ * (0/1), autotune ms (CSR, tiled) for K, the same three for K^T, host build
+ * ms of the tiled K and K^T formats, wall ms of pdcs_create and of
+ * pdcs_set_cones.  Returns the number of values written (<= 36). */
 int pdcs_get_scalars(pdcs_ctx *ctx, double *out, int cap);
 
 /* Number of kernel launches issued by the last pdcs_iterate call. */

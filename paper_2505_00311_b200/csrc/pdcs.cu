@@ -16,6 +16,7 @@
 #include <functional>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pdcs.h"
@@ -108,25 +109,91 @@ int pick_v(double avg) {
   return v;
 }
 
-void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
-                 TiledHost& H) {
+// Shared-memory bank balancing of one staged segment (in place).  A warp of
+// k_tiled_partial serves 32/V rows; at time step t lane l of a row's V-lane
+// group reads quad l + t*V, and position k of all those quads is one warp-wide
+// ld.shared (v2.f64 for the pair tile, f64 otherwise).  That load costs as many
+// shared-memory wavefronts as the largest number of distinct addresses falling
+// in one bank group (16-B groups of a 128-B line: col % 8 for pairs, col % 16
+// for doubles).  Within a row the entry order is free (its partial dot product
+// is one sum), so every row's entries are redistributed over its own quads,
+// greedily keeping each (time step, position) histogram of bank groups flat.
+// Lanes whose second unrolled quad (U = 2 in seg_row_dot_quad) is past the
+// row's end read column 0; pads take the emptiest group.
+void balance_banks(uint16_t* cols, int32_t* perm, const int32_t* rp, int32_t nr, int V, int elem, int32_t valid) {
+  constexpr int U = 2;
+  const int G = elem == 2 ? 8 : 16;
+  const int rpw = 32 / V;                                     // rows per warp
+  std::vector<std::vector<std::pair<uint16_t, int32_t>>> bucket((size_t)rpw * G);
+  std::vector<int32_t> left(rpw);
+  std::vector<std::pair<uint16_t, int32_t>> out;
+  for (int32_t i0 = 0; i0 < nr; i0 += rpw) {
+    const int R = (int)std::min<int32_t>(rpw, nr - i0);
+    int32_t tmax = 0;
+    for (int a = 0; a < R; ++a) {
+      const int32_t q0 = rp[i0 + a], q1 = rp[i0 + a + 1];
+      tmax = std::max(tmax, (q1 - q0 + V - 1) / V);
+      left[a] = 0;
+      for (int g = 0; g < G; ++g) bucket[(size_t)a * G + g].clear();
+      for (int64_t s = 4 * (int64_t)q0; s < 4 * (int64_t)q1; ++s)
+        if (perm[s] >= 0) { bucket[(size_t)a * G + cols[s] % G].push_back({cols[s], perm[s]}); ++left[a]; }
+    }
+    // new contents of each row's slots, written after the row's quads are assigned
+    out.assign(4 * (size_t)(rp[i0 + R] - rp[i0]), {0, -1});
+    for (int32_t t = 0; t < tmax; ++t) {
+      bool zero_read = false;
+      if (t % U)
+        for (int a = 0; a < R && !zero_read; ++a) {
+          const int32_t nq = rp[i0 + a + 1] - rp[i0 + a];
+          // some lane l < V has quad l + (t-1)V in the row but l + tV past its end
+          zero_read = nq > (t - 1) * V && nq < (t + 1) * V;
+        }
+      for (int k = 0; k < 4; ++k) {
+        int hist[16] = {0};
+        if (zero_read) hist[0] = 1;
+        for (int a = 0; a < R; ++a) {
+          const int32_t q0 = rp[i0 + a], nq = rp[i0 + a + 1] - q0;
+          for (int l = 0; l < V; ++l) {
+            const int32_t q = l + t * V;
+            if (q >= nq) break;
+            const size_t slot = 4 * (size_t)(q0 - rp[i0] + q) + k;
+            int best = -1;
+            for (int g = 0; g < G; ++g)
+              if ((left[a] == 0 || !bucket[(size_t)a * G + g].empty()) && (best < 0 || hist[g] < hist[best])) best = g;
+            if (left[a] > 0) {
+              auto& b = bucket[(size_t)a * G + best];
+              out[slot] = b.back();
+              b.pop_back();
+              --left[a];
+            } else {
+              out[slot] = {(uint16_t)(best < valid ? best : 0), -1};   // pad: value 0, emptiest group
+            }
+            ++hist[best];
+          }
+        }
+      }
+    }
+    const size_t base = 4 * (size_t)rp[i0];
+    for (size_t s = 0; s < out.size(); ++s) { cols[base + s] = out[s].first; perm[base + s] = out[s].second; }
+  }
+}
+
+// Chunks [row_a, row_b) (row_a a multiple of kTRows) into H, offsets local to H.
+void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, int64_t row_b, int64_t nvec,
+                       int elem, int64_t group_nz, TiledHost& H) {
   const int tile_bytes = tiled_tile_bytes();
   const int32_t T = tile_bytes / (8 * elem);
   const int64_t stage_min = tile_bytes / 16;           // staging must save >= 2x the gather sectors
-  // work-item size: enough items to fill the GPU several times over, no more
-  // partial groups per chunk than needed (PDCS_TILE_GROUP overrides)
-  const int64_t group_nz = std::getenv("PDCS_TILE_GROUP") ? std::atol(std::getenv("PDCS_TILE_GROUP"))
-                                                          : std::max<int64_t>(32768, ptr[rows] / 3000);
   const int64_t ntiles = (nvec + T - 1) / T;
   H.T = T;
   H.elem = elem;
-  H.nnz = ptr[rows];
-  H.perm_s.reserve(H.nnz);
-  H.col_s.reserve(H.nnz);
+  H.perm_s.reserve(ptr[row_b] - ptr[row_a]);
+  H.col_s.reserve(ptr[row_b] - ptr[row_a]);
   std::vector<int64_t> cnt(ntiles, 0);
   std::vector<int32_t> segof(ntiles, -1);
   std::vector<int64_t> touched;
-  for (int64_t r0 = 0; r0 < rows; r0 += kTRows) {
+  const int64_t rows = row_b;
+  for (int64_t r0 = row_a; r0 < rows; r0 += kTRows) {
     const int32_t nr = (int32_t)std::min<int64_t>(kTRows, rows - r0);
     touched.clear();
     for (int64_t p = ptr[r0]; p < ptr[r0 + nr]; ++p) {
@@ -200,6 +267,15 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
           H.perm_d[q] = (int32_t)p;
         }
       }
+    static const bool balance = !std::getenv("PDCS_TILE_BALANCE") || std::atoi(std::getenv("PDCS_TILE_BALANCE"));
+    if (balance)
+      for (int k = 0; k < nseg; ++k) {
+        const TSeg& S = H.seg[s_begin + k];
+        if (S.tile < 0 || S.V > 32) continue;
+        const int32_t valid = (int32_t)std::min<int64_t>(T, nvec - (int64_t)S.tile * T);
+        balance_banks(H.col_s.data() + S.nz, H.perm_s.data() + S.nz, H.rowptr.data() + rpbase[k], nr, S.V, elem,
+                      valid);
+      }
     // work items: consecutive segments up to group_nz nonzeros; the staged
     // segments of an item are cut into TMA batches of <= kBQ quads
     auto emit_item = [&](int32_t gg, int32_t sa, int32_t sb) {
@@ -241,6 +317,63 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
     H.chunk.push_back(TChunk{r0, nr, g, H.scratch});
     H.scratch += (int64_t)g * nr * elem;
     for (int64_t t : touched) { cnt[t] = 0; segof[t] = -1; }
+  }
+}
+
+// Tiled format of a whole CSR: contiguous chunk ranges of about equal nnz are
+// built on host threads (build_tiled_range) and concatenated in order with
+// their offsets rebased, so the result does not depend on the thread count.
+void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
+                 TiledHost& H) {
+  // work-item size: enough items to fill the GPU several times over, no more
+  // partial groups per chunk than needed (PDCS_TILE_GROUP overrides)
+  const int64_t group_nz = std::getenv("PDCS_TILE_GROUP") ? std::atol(std::getenv("PDCS_TILE_GROUP"))
+                                                          : std::max<int64_t>(32768, ptr[rows] / 3000);
+  const int64_t nchunk = (rows + kTRows - 1) / kTRows;
+  int nth = (int)std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()), 32,
+                                    std::max<int64_t>(1, nchunk / 4)});
+  if (const char* e = std::getenv("PDCS_BUILD_THREADS")) nth = std::max(1, std::atoi(e));
+  // chunk-aligned range starts at equal shares of nnz
+  std::vector<int64_t> cut(nth + 1, rows);
+  cut[0] = 0;
+  for (int w = 1; w < nth; ++w) {
+    const int64_t target = ptr[rows] / nth * w;
+    const int64_t r = std::lower_bound(ptr, ptr + rows + 1, target) - ptr;
+    cut[w] = std::max(cut[w - 1], std::min(rows, r / kTRows * kTRows));
+  }
+  std::vector<TiledHost> part(nth);
+  std::vector<std::thread> th;
+  for (int w = 0; w < nth; ++w)
+    th.emplace_back([&, w] { build_tiled_range(ptr, col, cut[w], cut[w + 1], nvec, elem, group_nz, part[w]); });
+  for (auto& t : th) t.join();
+  H.T = tiled_tile_bytes() / (8 * elem);
+  H.elem = elem;
+  H.nnz = ptr[rows];
+  size_t ns = 0, nd = 0, nrp = 0;
+  for (const auto& P : part) { ns += P.col_s.size() + 8; nd += P.col_d.size(); nrp += P.rowptr.size(); }
+  H.col_s.reserve(ns + 8); H.perm_s.reserve(ns + 8); H.col_d.reserve(nd); H.perm_d.reserve(nd);
+  H.rowptr.reserve(nrp + 8);
+  for (auto& P : part) {
+    H.col_s.resize((H.col_s.size() + 7) & ~(size_t)7, 0);    // keep segment starts 16-B aligned
+    H.perm_s.resize(H.col_s.size(), -1);
+    const int64_t sbase = (int64_t)H.seg.size(), bbase = (int64_t)H.batch.size(), cbase = (int64_t)H.chunk.size();
+    const int64_t rpb = (int64_t)H.rowptr.size(), nzs = (int64_t)H.col_s.size(), nzd = (int64_t)H.col_d.size();
+    for (TSeg S : P.seg) { S.rp += rpb; S.nz += S.tile >= 0 ? nzs : nzd; H.seg.push_back(S); }
+    for (TBatch B : P.batch) { B.seg += (int32_t)sbase; H.batch.push_back(B); }
+    for (TWork W : P.work) {
+      W.chunk += (int32_t)cbase; W.s0 += (int32_t)sbase; W.s1 += (int32_t)sbase;
+      W.b0 += (int32_t)bbase; W.b1 += (int32_t)bbase;
+      H.work.push_back(W);
+    }
+    for (TChunk C : P.chunk) { C.scratch += H.scratch; H.chunk.push_back(C); }
+    H.scratch += P.scratch;
+    H.staged += P.staged;
+    H.rowptr.insert(H.rowptr.end(), P.rowptr.begin(), P.rowptr.end());
+    H.col_s.insert(H.col_s.end(), P.col_s.begin(), P.col_s.end());
+    H.perm_s.insert(H.perm_s.end(), P.perm_s.begin(), P.perm_s.end());
+    H.col_d.insert(H.col_d.end(), P.col_d.begin(), P.col_d.end());
+    H.perm_d.insert(H.perm_d.end(), P.perm_d.begin(), P.perm_d.end());
+    P = TiledHost();
   }
   H.col_s.resize(H.col_s.size() + 8, 0);      // TMA column-id copies may read one quad past the end
   H.rowptr.resize(H.rowptr.size() + 8, 0);    // TMA row-pointer slices are rounded up to 16 B
@@ -294,7 +427,9 @@ struct pdcs_ctx {
     int g_partial = 0, g_combine = 0;
     int64_t slot = 0;
     float tune_csr_ms = 0.f, tune_tiled_ms = 0.f;
+    double build_ms = 0.0;                     // host build of the format
   } tK, tKT;
+  double t_create_ms = 0.0, t_cones_ms = 0.0;  // wall time of pdcs_create / pdcs_set_cones
   std::vector<int32_t> hcol;                   // host copy of K's column ids (tiled build)
   DBuf<uint8_t> ek, rk;
   DBuf<Block> pblocks, rblocks;
@@ -655,7 +790,9 @@ struct pdcs_ctx {
   void make_tiled(TiledDev& D, const int64_t* hp, const int32_t* hc, int64_t rows, int64_t nvec, int elem,
                   const double* dval) {
     TiledHost H;
+    const auto t0 = std::chrono::steady_clock::now();
     build_tiled(hp, hc, rows, nvec, elem, H);
+    D.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     const double frac = H.nnz ? (double)H.staged / (double)H.nnz : 0.0;
     const char* env = std::getenv("PDCS_TILED");
     const bool want = env ? std::atoi(env) != 0 : frac >= 0.3;
@@ -781,10 +918,13 @@ struct pdcs_ctx {
     // row-length bounds per class (PDCS_SPMV_BINS="b1,b4,b8,b16,b32" overrides).
     const int Vs[kMaxClasses] = {1, 4, 8, 16, 32, 0};
     int64_t bound[5] = {2, 12, 48, 96, (int64_t)1 << 40};   // measured on B200 (profiles/)
+    bool fixed_bins = false;
     if (const char* env = std::getenv("PDCS_SPMV_BINS")) {
       int64_t b[5];
-      if (std::sscanf(env, "%ld,%ld,%ld,%ld,%ld", &b[0], &b[1], &b[2], &b[3], &b[4]) == 5)
+      if (std::sscanf(env, "%ld,%ld,%ld,%ld,%ld", &b[0], &b[1], &b[2], &b[3], &b[4]) == 5) {
         for (int i = 0; i < 5; ++i) bound[i] = b[i];
+        fixed_bins = true;
+      }
     }
     std::vector<int64_t> lists[kMaxClasses];
     for (int64_t i = 0; i < rows; ++i) {
@@ -793,6 +933,15 @@ struct pdcs_ctx {
       for (int k = 0; k < 5; ++k)
         if (L <= bound[k]) { c = k; break; }
       lists[c].push_back(i);
+    }
+    // Few long rows (fewer than 16 warps per SM in the warp-per-row class):
+    // one warp per row leaves the SMs idle and each warp walks a long serial
+    // chain of gathers, so rows of > 1024 nnz get a CTA each instead.  With
+    // many long rows (Lasso K^T) warp-per-row is faster (profiles/r1_sweep_v0.txt).
+    if (!fixed_bins && (int64_t)lists[4].size() < (int64_t)sms * 16) {
+      std::vector<int64_t> keep;
+      for (int64_t r_ : lists[4]) (ptr[r_ + 1] - ptr[r_] > 1024 ? lists[5] : keep).push_back(r_);
+      lists[4].swap(keep);
     }
     SpmvPlan P{};
     P.ncls = 0;
@@ -925,6 +1074,7 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
   if (!out) return PDCS_ERR_ARG;
   *out = nullptr;
   pdcs_ctx* ctx = new pdcs_ctx();
+  const auto t_start = std::chrono::steady_clock::now();
   pdcs_status s = guard(nullptr, [&] {
     if (m_global < 0 || n < 0 || n1 < 0 || n1 > n) fail(PDCS_ERR_DIM, "bad sizes m/n/n1");
     if (row_begin < 0 || row_end < row_begin || row_end > m_global) fail(PDCS_ERR_DIM, "bad row range");
@@ -1066,6 +1216,7 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
     CK(cudaMallocHost(&ctx->hctl, sizeof(Ctl)));
     std::memset(ctx->hctl, 0, sizeof(Ctl));
     CK(cudaStreamSynchronize(st));
+    ctx->t_create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   });
   if (s != PDCS_OK) {
     delete ctx;
@@ -1078,6 +1229,7 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
 pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim, int64_t npc,
                            const int32_t* rkind, const int64_t* rdim, int64_t nrc) {
   if (!ctx) return PDCS_ERR_ARG;
+  const auto t_start = std::chrono::steady_clock::now();
   return guard(ctx, [&] {
     if (ctx->cones_set) fail(PDCS_ERR_STATE, "cones already set");
     if (npc < 0 || nrc < 0 || (npc && (!pk || !pdim)) || (nrc && (!rkind || !rdim)))
@@ -1319,6 +1471,8 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     CK(cudaGetLastError());
     // anchor / products / e_anchor
     reset_from_current(ctx);
+    CK(cudaStreamSynchronize(st));
+    ctx->t_cones_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   });
 }
 
@@ -1600,14 +1754,15 @@ int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
   if (!ctx || !out || !ctx->ctl) return 0;
   if (guard(ctx, [&] { ctx->read_ctl(); }) != PDCS_OK) return 0;
   const Ctl& C = *ctx->hctl;
-  double v[32] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
+  double v[36] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
                   (double)C.restarts, C.e_anchor, C.Wsum, C.eta_init,
                   C.kkt[0][0], C.kkt[0][1], C.kkt[0][2], C.kkt[0][3], C.kkt[0][4],
                   C.kkt[1][0], C.kkt[1][1], C.kkt[1][2], C.kkt[1][3], C.kkt[1][4],
                   C.e_prev, C.best_e, (double)C.use_avg, (double)C.restart, C.last_num, C.last_cross,
                   (double)ctx->tK.on, ctx->tK.tune_csr_ms, ctx->tK.tune_tiled_ms,
-                  (double)ctx->tKT.on, ctx->tKT.tune_csr_ms, ctx->tKT.tune_tiled_ms};
-  const int k = std::min(cap, 32);
+                  (double)ctx->tKT.on, ctx->tKT.tune_csr_ms, ctx->tKT.tune_tiled_ms,
+                  ctx->tK.build_ms, ctx->tKT.build_ms, ctx->t_create_ms, ctx->t_cones_ms};
+  const int k = std::min(cap, 36);
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }

@@ -318,3 +318,29 @@ def test_tiled_lasso_vanilla_parity(P, tiled_env):
     xg, yg = g.get_iterate(P.CURRENT)
     xo, yo = o.get_iterate(0)
     assert parity(xg, yg, xo, yo) <= TOL
+
+
+def test_tiled_build_threads_and_bank_balance(P, tiled_env, monkeypatch):
+    """The tiled format is built on host threads (one contiguous chunk range
+    each) and concatenated: the result must not depend on the thread count
+    (bit-identical iterates).  Bank balancing only permutes entries within a
+    row, so it changes nothing but the summation order."""
+    monkeypatch.setenv("PDCS_TILE_KB", "4")
+    prog = gen_lasso(12000, 400, 0.05, seed=8)
+    runs = {}
+    for key, env in {"t1": {"PDCS_BUILD_THREADS": "1"}, "t5": {"PDCS_BUILD_THREADS": "5"},
+                     "nobal": {"PDCS_BUILD_THREADS": "3", "PDCS_TILE_BALANCE": "0"}}.items():
+        for k in ("PDCS_BUILD_THREADS", "PDCS_TILE_BALANCE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        g = P.PdcsSolver(prog, vanilla_pdhg=1)
+        assert g.scalars()["tiled_K"] == 1.0 and g.scalars()["tiled_KT"] == 1.0
+        g.iterate(60)
+        runs[key] = g.get_iterate(P.CURRENT)
+        g.close()
+    assert np.array_equal(runs["t1"][0], runs["t5"][0]) and np.array_equal(runs["t1"][1], runs["t5"][1])
+    assert parity(*runs["t1"], *runs["nobal"]) <= 1e-12
+    o = O.OracleSolver(prog, vanilla_pdhg=1)
+    o.iterate(60)
+    assert parity(*runs["t1"], *o.get_iterate(0)) <= TOL

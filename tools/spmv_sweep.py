@@ -28,6 +28,6 @@ for b in bins:
     out = {k: round(v[0] / v[1], 4) for k, v in kt.items() if v[1]}
     tot = sum(v[0] for v in kt.values()) / a.iters
     sc = g.scalars()
-    tune = {k: sc[k] for k in sc if k.startswith("tune") or k.startswith("tiled")}
+    tune = {k: sc[k] for k in sc if k.startswith(("tune", "tiled", "setup"))}
     print(json.dumps({"bins": b, **tune, "ms_per_iter_kernels": round(tot, 4), "wall_ms_per_iter": round(1e3 * el / a.iters, 4), **out}), flush=True)
     g.close()

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpdcs.so")
+LIB_PATH = os.environ.get("PDCS_LIB") or os.path.join(_HERE, "libpdcs.so")   # PDCS_LIB: tuning builds
 
 P_D = C.POINTER(C.c_double)
 P_I64 = C.POINTER(C.c_int64)

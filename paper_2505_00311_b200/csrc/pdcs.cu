@@ -92,6 +92,7 @@ struct TiledHost {
   std::vector<int32_t> perm_s, perm_d;
   int64_t scratch = 0, staged = 0, nnz = 0;
   int32_t T = 0, elem = 1;
+  double build_ms = 0.0;
 };
 
 // shared-memory tile size in bytes (PDCS_TILE_KB overrides; default 32 KB)
@@ -100,10 +101,13 @@ int tiled_tile_bytes() {
   return b;
 }
 
-// lanes per row for a segment with `avg` nonzeros per row: aim for >= ~8 entries
-// per lane so that the unrolled, pipelined loop body is used (PDCS_TILE_LPE overrides)
-int pick_v(double avg) {
-  static const double lpe = std::getenv("PDCS_TILE_LPE") ? std::atof(std::getenv("PDCS_TILE_LPE")) : 2.0;
+// lanes per row for a segment with `avg` quads (staged) or entries (direct) per
+// row: at least 2*lpe units per lane so that the unrolled loop body is used.
+// Measured on B200 (profiles/r1_sweep_lpe.txt): lpe 4 for the pair gather,
+// 2 for the single gather (PDCS_TILE_LPE overrides both).
+int pick_v(double avg, int elem) {
+  static const double env = std::getenv("PDCS_TILE_LPE") ? std::atof(std::getenv("PDCS_TILE_LPE")) : 0.0;
+  const double lpe = env > 0 ? env : elem == 2 ? 4.0 : 2.0;
   int v = 1;
   while (v < 32 && avg >= 2.0 * v * lpe) v *= 2;
   return v;
@@ -235,7 +239,7 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
         H.rowptr[rpbase[k] + i + 1] = H.rowptr[rpbase[k] + i] + u;
         units += u;
       }
-      S.V = pick_v(stg ? (double)units / nr : (double)seg_nz[k] / nr);
+      S.V = pick_v(stg ? (double)units / nr : (double)seg_nz[k] / nr, elem);
       if (stg) {
         // segments start on an even quad: 16-B aligned TMA sources for the column ids
         H.col_s.resize((H.col_s.size() + 7) & ~(size_t)7, 0);
@@ -325,6 +329,7 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
 // their offsets rebased, so the result does not depend on the thread count.
 void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
                  TiledHost& H) {
+  const auto t_start = std::chrono::steady_clock::now();
   // work-item size: enough items to fill the GPU several times over, no more
   // partial groups per chunk than needed (PDCS_TILE_GROUP overrides)
   const int64_t group_nz = std::getenv("PDCS_TILE_GROUP") ? std::atol(std::getenv("PDCS_TILE_GROUP"))
@@ -378,6 +383,35 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
   H.col_s.resize(H.col_s.size() + 8, 0);      // TMA column-id copies may read one quad past the end
   H.rowptr.resize(H.rowptr.size() + 8, 0);    // TMA row-pointer slices are rounded up to 16 B
   H.perm_s.resize(H.col_s.size(), -1);
+  H.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+// Input checks of the CSR on host threads: column ids in
+// range and strictly increasing per row, finite values.  Reports the first
+// offending row (and, within it, the first offending entry's check).
+void validate_csr(const int64_t* ptr, const int32_t* col, const double* val, int64_t m, int64_t n) {
+  const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(16, ptr[m] / 4000000 + 1));
+  std::vector<int64_t> bad(nth, INT64_MAX);
+  std::vector<std::thread> th;
+  for (int w = 0; w < nth; ++w)
+    th.emplace_back([&, w] {
+      const int64_t a = m * w / nth, b = m * (w + 1) / nth;
+      for (int64_t i = a; i < b; ++i)
+        for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q) {
+          int why = 0;
+          if (col[q] < 0 || col[q] >= n) why = 1;
+          else if (q > ptr[i] && col[q] <= col[q - 1]) why = 2;
+          else if (!std::isfinite(val[q])) why = 3;
+          if (why) { bad[w] = i * 4 + why; return; }
+        }
+    });
+  for (auto& t : th) t.join();
+  const int64_t b = *std::min_element(bad.begin(), bad.end());
+  if (b == INT64_MAX) return;
+  const std::string row = std::to_string(b / 4);
+  if (b % 4 == 1) fail(PDCS_ERR_DIM, "column index out of range in row " + row);
+  if (b % 4 == 2) fail(PDCS_ERR_DIM, "column indices not strictly increasing in row " + row);
+  fail(PDCS_ERR_NONFINITE, "non-finite matrix entry in row " + row);
 }
 
 }  // namespace
@@ -430,7 +464,11 @@ struct pdcs_ctx {
     double build_ms = 0.0;                     // host build of the format
   } tK, tKT;
   double t_create_ms = 0.0, t_cones_ms = 0.0;  // wall time of pdcs_create / pdcs_set_cones
-  std::vector<int32_t> hcol;                   // host copy of K's column ids (tiled build)
+  // host builds of the tiled formats (build_tiled), started in pdcs_create
+  TiledHost hK, hKT;
+  std::thread thK, thKT;
+  std::vector<int64_t> hKTptr;                 // K~^T structure for the background build
+  std::vector<int32_t> hKTcol;
   DBuf<uint8_t> ek, rk;
   DBuf<Block> pblocks, rblocks;
   DBuf<int64_t> rsoc_offs_p, rsoc_offs_r;
@@ -462,6 +500,8 @@ struct pdcs_ctx {
   int64_t launches = 0;
 
   ~pdcs_ctx() {
+    if (thK.joinable()) thK.join();
+    if (thKT.joinable()) thKT.join();
     if (comm) nccl().CommDestroy(comm);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
@@ -787,17 +827,12 @@ struct pdcs_ctx {
   static size_t tiled_smem(int elem) { return (size_t)tiled_tile_bytes() + (size_t)kTRows * elem * sizeof(double); }
 
   // Build the tiled copy of a CSR (structure on the host, scaled values on the device).
-  void make_tiled(TiledDev& D, const int64_t* hp, const int32_t* hc, int64_t rows, int64_t nvec, int elem,
-                  const double* dval) {
-    TiledHost H;
-    const auto t0 = std::chrono::steady_clock::now();
-    build_tiled(hp, hc, rows, nvec, elem, H);
-    D.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  void make_tiled(TiledDev& D, TiledHost& H, int64_t rows, int64_t nvec, int elem, const double* dval) {
     const double frac = H.nnz ? (double)H.staged / (double)H.nnz : 0.0;
     const char* env = std::getenv("PDCS_TILED");
     const bool want = env ? std::atoi(env) != 0 : frac >= 0.3;
     D.on = want && H.nnz > 0;
-    if (!D.on) return;
+    if (!D.on) { H = TiledHost(); return; }
     upload(D.work, H.work, st);
     upload(D.batch, H.batch, st);
     upload(D.chunk, H.chunk, st);
@@ -843,6 +878,7 @@ struct pdcs_ctx {
     D.g_partial = (int)std::max<int64_t>(1, std::min<int64_t>(M.nwork, (int64_t)sms * std::max(occ, 1)));
     int64_t slabs = 0;
     for (const TChunk& c : H.chunk) slabs += (c.nrows + kThreads - 1) / kThreads;
+    H = TiledHost();                           // host copy no longer needed
     D.g_combine = (int)std::max<int64_t>(1, std::min<int64_t>(slabs, (int64_t)sms * 4));
     // Setup-time autotune: keep the tiled copy only if it beats the CSR kernel
     // by >= 10% on this matrix (gather locality decides).
@@ -934,14 +970,19 @@ struct pdcs_ctx {
         if (L <= bound[k]) { c = k; break; }
       lists[c].push_back(i);
     }
-    // Few long rows (fewer than 16 warps per SM in the warp-per-row class):
-    // one warp per row leaves the SMs idle and each warp walks a long serial
-    // chain of gathers, so rows of > 1024 nnz get a CTA each instead.  With
-    // many long rows (Lasso K^T) warp-per-row is faster (profiles/r1_sweep_v0.txt).
-    if (!fixed_bins && (int64_t)lists[4].size() < (int64_t)sms * 16) {
-      std::vector<int64_t> keep;
-      for (int64_t r_ : lists[4]) (ptr[r_ + 1] - ptr[r_] > 1024 ? lists[5] : keep).push_back(r_);
-      lists[4].swap(keep);
+    // Few very long rows (> 1024 nnz; fewer than 16 per SM): one warp per row
+    // leaves the SMs idle while each warp walks a long serial chain of gathers
+    // (Fisher's 1000 supply rows of 1e4 nnz), so they get a CTA each.  With
+    // many of them (Lasso K^T: 1e4 rows) warp-per-row is faster
+    // (profiles/r1_sweep_v0.txt).
+    if (!fixed_bins) {
+      int64_t nlong = 0;
+      for (int64_t r_ : lists[4]) nlong += ptr[r_ + 1] - ptr[r_] > 1024;
+      if (nlong && nlong < (int64_t)sms * 16) {
+        std::vector<int64_t> keep;
+        for (int64_t r_ : lists[4]) (ptr[r_ + 1] - ptr[r_] > 1024 ? lists[5] : keep).push_back(r_);
+        lists[4].swap(keep);
+      }
     }
     SpmvPlan P{};
     P.ncls = 0;
@@ -1119,16 +1160,29 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
       if (ctx->hptr[i + 1] < ctx->hptr[i]) fail(PDCS_ERR_DIM, "row_ptr not monotone at row " + std::to_string(i));
     const int64_t nnz = ctx->hptr[m];
     if (nnz >= ((int64_t)1 << 31)) fail(PDCS_ERR_DIM, "local nnz must be < 2^31 (shard the rows)");
-    std::vector<int32_t>& hcol = ctx->hcol;
-    hcol = to_host(col_idx, nnz, mem_kind);
-    std::vector<double> hval = to_host(vals, nnz, mem_kind);
-    for (int64_t i = 0; i < m; ++i)
-      for (int64_t q_ = ctx->hptr[i]; q_ < ctx->hptr[i + 1]; ++q_) {
-        if (hcol[q_] < 0 || hcol[q_] >= n) fail(PDCS_ERR_DIM, "column index out of range in row " + std::to_string(i));
-        if (q_ > ctx->hptr[i] && hcol[q_] <= hcol[q_ - 1])
-          fail(PDCS_ERR_DIM, "column indices not strictly increasing in row " + std::to_string(i));
-        if (!std::isfinite(hval[q_])) fail(PDCS_ERR_NONFINITE, "non-finite matrix entry in row " + std::to_string(i));
-      }
+    // host view of the matrix: the caller's buffers (host) or copies (device)
+    std::vector<int32_t> colcopy;
+    std::vector<double> valcopy;
+    const int32_t* hcolp = col_idx;
+    const double* hvalp = vals;
+    if (mem_kind == PDCS_MEM_DEVICE) {
+      colcopy = to_host(col_idx, nnz, mem_kind);
+      valcopy = to_host(vals, nnz, mem_kind);
+      hcolp = colcopy.data();
+      hvalp = valcopy.data();
+    } else if (nnz && (!col_idx || !vals)) {
+      fail(PDCS_ERR_ARG, "null input pointer");
+    }
+    validate_csr(ctx->hptr.data(), hcolp, hvalp, m, n);
+    // tiled format of K~ (structure only) on host threads, overlapping the uploads
+    // and the device transpose below; joined before this call returns
+    ctx->thK = std::thread([ctx, hcolp, m, n] {
+      build_tiled(ctx->hptr.data(), hcolp, m, n, 2, ctx->hK);
+    });
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() { if (t.joinable()) t.join(); }
+    } join_k{ctx->thK};
     std::vector<double> hc = to_host(c, n, mem_kind), hh = to_host(h, m, mem_kind);
     ctx->hl = to_host(l, n1, mem_kind);
     ctx->hu = to_host(u, n1, mem_kind);
@@ -1149,8 +1203,12 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
     std::vector<int32_t> p32(m + 1);
     for (int64_t i = 0; i <= m; ++i) p32[i] = (int32_t)ctx->hptr[i];
     upload(ctx->Kptr, p32, st);
-    upload(ctx->Kcol, hcol, st);
-    upload(ctx->Kval, hval, st);
+    ctx->Kcol.alloc(nnz);
+    ctx->Kval.alloc(nnz);
+    if (nnz) {
+      CK(cudaMemcpyAsync(ctx->Kcol.p, col_idx, nnz * sizeof(int32_t), cudaMemcpyDefault, st));
+      CK(cudaMemcpyAsync(ctx->Kval.p, vals, nnz * sizeof(double), cudaMemcpyDefault, st));
+    }
     upload(ctx->c0, hc, st);
     upload(ctx->h0, hh, st);
     upload(ctx->l0, ctx->hl, st);
@@ -1201,6 +1259,14 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
     std::vector<size_t> offs;
     ctx->build_plan(ctx->K, ctx->hptr, rowstore, offs);
     ctx->build_plan(ctx->KT, tptr, rowstore, offs);
+    // tiled format of K~^T from the transposed structure, in the background
+    // (joined in pdcs_set_cones, which uses it after the Ruiz scaling)
+    ctx->hKTptr = std::move(tptr);
+    ctx->hKTcol.resize(nnz);
+    if (nnz) CK(cudaMemcpy(ctx->hKTcol.data(), ctx->KTcol.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    ctx->thKT = std::thread([ctx, m, n] {
+      build_tiled(ctx->hKTptr.data(), ctx->hKTcol.data(), n, m, 1, ctx->hKT);
+    });
     upload(ctx->planrows, rowstore, st);
     ctx->patch_plan(ctx->K);
     ctx->patch_plan(ctx->KT);
@@ -1216,6 +1282,8 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
     CK(cudaMallocHost(&ctx->hctl, sizeof(Ctl)));
     std::memset(ctx->hctl, 0, sizeof(Ctl));
     CK(cudaStreamSynchronize(st));
+    ctx->thK.join();
+    ctx->tK.build_ms = ctx->hK.build_ms;
     ctx->t_create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   });
   if (s != PDCS_OK) {
@@ -1387,12 +1455,12 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     CK(cudaGetLastError());
     // column-tiled copies of K~ and K~^T for the hot SpMVs (tiled.cuh)
     {
-      ctx->make_tiled(ctx->tK, ctx->hptr.data(), ctx->hcol.data(), m, n, 2, ctx->K.val);
-      std::vector<int32_t> tp32(n + 1), tcol(ctx->KT.nnz);
-      CK(cudaMemcpy(tp32.data(), ctx->KT.ptr, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
-      if (ctx->KT.nnz) CK(cudaMemcpy(tcol.data(), ctx->KT.col, ctx->KT.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
-      std::vector<int64_t> tp(tp32.begin(), tp32.end());
-      ctx->make_tiled(ctx->tKT, tp.data(), tcol.data(), n, m, 1, ctx->KT.val);
+      ctx->make_tiled(ctx->tK, ctx->hK, m, n, 2, ctx->K.val);
+      if (ctx->thKT.joinable()) ctx->thKT.join();
+      ctx->tKT.build_ms = ctx->hKT.build_ms;
+      ctx->make_tiled(ctx->tKT, ctx->hKT, n, m, 1, ctx->KT.val);
+      ctx->hKTptr = std::vector<int64_t>();
+      ctx->hKTcol = std::vector<int32_t>();
     }
     // scaled data (reading A2): c~ = c/q, h~ = h/r, l~ = q l, u~ = q u
     k_ewise<<<Gn, kThreads, 0, st>>>(n, ctx->c0.p, ctx->q.p, 0, ctx->ct.p);

@@ -23,6 +23,12 @@
 
 namespace pdcs {
 
+#ifndef PDCS_TP_MINB
+#define PDCS_TP_MINB 2                // min resident CTAs/SM of k_tiled_partial<2>: caps registers at 64
+#endif
+#ifndef PDCS_TP_MINB1
+#define PDCS_TP_MINB1 3               // k_tiled_partial<1>: 40 registers, 3 CTAs/SM (-10% time on Lasso)
+#endif
 constexpr int kTRows = 1024;          // rows per chunk (shared accumulator size)
 constexpr int kTThreads = 512;        // CTA size of the partial kernel
 constexpr int kTileBytes = 65536;     // one vector tile in shared memory
@@ -84,6 +90,14 @@ __device__ __forceinline__ double2 ld_stream2(const double* p) {
   asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
+// 32-byte load (sm_100: LDG.256): one quad of values, one L2 sector, one request
+__device__ __forceinline__ double4 ld_stream4(const double* p) {
+  double4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
   uint2 v;
   asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
@@ -108,10 +122,9 @@ __device__ __forceinline__ void seg_row_dot_quad(const double* __restrict__ val4
     for (int u = 0; u < U; ++u) {
       const int32_t q = q0 + u * V;
       if (q < qe) {
-        const double2 v01 = ld_stream2(val4 + 4 * (int64_t)q);
-        const double2 v23 = ld_stream2(val4 + 4 * (int64_t)q + 2);
+        const double4 v = ld_stream4(val4 + 4 * (int64_t)q);
         const uint2 cc = ld_stream_u2(col4 + 4 * (int64_t)q);
-        a[u][0] = v01.x; a[u][1] = v01.y; a[u][2] = v23.x; a[u][3] = v23.y;
+        a[u][0] = v.x; a[u][1] = v.y; a[u][2] = v.z; a[u][3] = v.w;
         c[u][0] = cc.x & 0xffffu; c[u][1] = cc.x >> 16; c[u][2] = cc.y & 0xffffu; c[u][3] = cc.y >> 16;
       } else {
 #pragma unroll
@@ -202,7 +215,7 @@ __device__ __forceinline__ void seg_rows(const TiledMat& M, const TSeg& S, const
 // Partial dot products of every work item -> scratch.
 // guard: 0 always run, 1 only while running, 2 only on an accepted step
 template <int ELEM>
-__global__ void __launch_bounds__(kTThreads) k_tiled_partial(TiledMat M, const double* __restrict__ x,
+__global__ void __launch_bounds__(kTThreads, ELEM == 1 ? PDCS_TP_MINB1 : PDCS_TP_MINB) k_tiled_partial(TiledMat M, const double* __restrict__ x,
                                                              double* __restrict__ scratch, const Ctl* ctl,
                                                              int guard) {
   if (guard >= 1 && ctl->status != 4) return;

@@ -220,6 +220,20 @@ int64_t pdcs_launch_count(const pdcs_ctx *ctx);
 const char *pdcs_last_error(const pdcs_ctx *ctx);
 void pdcs_destroy(pdcs_ctx *ctx);
 
+/* Host-only diagnostic, no GPU needed: build the column-tiled layout
+ * of a CSR structure (row_ptr[rows+1], col[nnz], valid and
+ * sorted; elem = 2 for the (x^, x) pair gather of K, 1 for the y gather of
+ * K^T) and model the shared-memory gathers of its partial kernel.  Writes up to
+ * cap doubles: nnz, staged nnz, quads, pad entries, staged segments, work
+ * items, modeled ld.shared instructions, modeled shared-memory wavefronts,
+ * host build ms, a lower bound on those wavefronts for the layout's row
+ * grouping (per phase: max(active slots, entries of the most loaded bank
+ * group)), and the number of structure errors (entries stored under a wrong
+ * column, twice, or not at all; 0 for a correct layout).  Returns the number
+ * written (0 on bad arguments). */
+int pdcs_tiled_layout_stats(const int64_t *row_ptr, const int32_t *col, int64_t rows, int64_t nvec, int elem,
+                            double *out, int cap);
+
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 broadcasts it). */
 pdcs_status pdcs_nccl_unique_id(void *out128);
 

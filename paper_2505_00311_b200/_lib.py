@@ -90,6 +90,9 @@ def lib():
         L.pdcs_launch_count.restype = C.c_int64
         L.pdcs_destroy.argtypes = [C.c_void_p]
         L.pdcs_nccl_unique_id.argtypes = [C.c_void_p]
+        L.pdcs_tiled_layout_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                              C.c_void_p, C.c_int]
+        L.pdcs_tiled_layout_stats.restype = C.c_int
         _lib = L
     return _lib
 
@@ -98,7 +101,7 @@ EXPORTED = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterat
             "pdcs_solve", "pdcs_get_iterate", "pdcs_set_iterate", "pdcs_get_scaling",
             "pdcs_kernel_times", "pdcs_enable_timing", "pdcs_launch_count", "pdcs_last_error",
             "pdcs_destroy", "pdcs_nccl_unique_id", "pdcs_get_scalars", "pdcs_get_state",
-            "pdcs_set_state"]
+            "pdcs_set_state", "pdcs_tiled_layout_stats"]
 
 STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e_prev", "best_e", "k",
               "total", "trials", "restarts"]
@@ -241,3 +244,19 @@ def pdcs_nccl_unique_id():
     buf = (C.c_char * 128)()
     _check(lib().pdcs_nccl_unique_id(buf))
     return bytes(buf)
+
+
+TILED_STAT_KEYS = ["nnz", "staged", "quads", "pads", "segments", "work_items", "lds_inst", "lds_wavefronts",
+                   "build_ms", "lds_wavefront_bound", "structure_errors"]
+
+
+def pdcs_tiled_layout_stats(row_ptr, col, nvec: int, elem: int) -> dict:
+    """Host-only model of the tiled layout (no GPU): see include/pdcs.h."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cc = np.ascontiguousarray(col, np.int32)
+    out = np.zeros(len(TILED_STAT_KEYS))
+    k = lib().pdcs_tiled_layout_stats(rp.ctypes.data, cc.ctypes.data, rp.shape[0] - 1, int(nvec), int(elem),
+                                      out.ctypes.data, len(TILED_STAT_KEYS))
+    if k == 0:
+        raise PdcsError(-1, "pdcs_tiled_layout_stats: bad arguments")
+    return dict(zip(TILED_STAT_KEYS[:k], out[:k]))

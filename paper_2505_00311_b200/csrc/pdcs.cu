@@ -87,6 +87,7 @@ struct TiledHost {
   std::vector<TChunk> chunk;
   std::vector<TSeg> seg;
   std::vector<int32_t> rowptr;
+  std::vector<uint16_t> srow;      // per segment position: chunk-local row (rows sorted by length)
   std::vector<uint16_t> col_s;
   std::vector<int32_t> col_d;
   std::vector<int32_t> perm_s, perm_d;
@@ -113,73 +114,123 @@ int pick_v(double avg, int elem) {
   return v;
 }
 
-// Shared-memory bank balancing of one staged segment (in place).  A warp of
-// k_tiled_partial serves 32/V rows; at time step t lane l of a row's V-lane
-// group reads quad l + t*V, and position k of all those quads is one warp-wide
-// ld.shared (v2.f64 for the pair tile, f64 otherwise).  That load costs as many
-// shared-memory wavefronts as the largest number of distinct addresses falling
-// in one bank group (16-B groups of a 128-B line: col % 8 for pairs, col % 16
-// for doubles).  Within a row the entry order is free (its partial dot product
-// is one sum), so every row's entries are redistributed over its own quads,
-// greedily keeping each (time step, position) histogram of bank groups flat.
-// Lanes whose second unrolled quad (U = 2 in seg_row_dot_quad) is past the
-// row's end read column 0; pads take the emptiest group.
-void balance_banks(uint16_t* cols, int32_t* perm, const int32_t* rp, int32_t nr, int V, int elem, int32_t valid) {
-  constexpr int U = 2;
-  const int G = elem == 2 ? 8 : 16;
-  const int rpw = 32 / V;                                     // rows per warp
-  std::vector<std::vector<std::pair<uint16_t, int32_t>>> bucket((size_t)rpw * G);
-  std::vector<int32_t> left(rpw);
-  std::vector<std::pair<uint16_t, int32_t>> out;
-  for (int32_t i0 = 0; i0 < nr; i0 += rpw) {
-    const int R = (int)std::min<int32_t>(rpw, nr - i0);
-    int32_t tmax = 0;
+// Gather schedule of k_tiled_partial (seg_rows) over one staged segment: warp
+// block `blk` is the 32/V consecutive positions i0 = blk * 32/V ...; lane
+// a*V + l reads quads l, l + V, ... of position i0 + a, one per time step.
+// lanes[lane] lists (local row, quad) in time order; rows[] maps local rows to
+// segment positions.
+int tiled_blocks(int32_t nr, int V) { return (nr + 32 / V - 1) / (32 / V); }
+void tiled_block_schedule(const int32_t* rp, int32_t nr, int V, int blk, std::vector<int32_t>& rows,
+                          std::vector<std::vector<std::pair<int32_t, int32_t>>>& lanes) {
+  rows.clear();
+  lanes.assign(32, {});
+  const int rpw = 32 / V;
+  const int32_t i0 = blk * rpw;
+  for (int a = 0; a < rpw && i0 + a < nr; ++a) {
+    rows.push_back(i0 + a);
+    const int32_t nq = rp[i0 + a + 1] - rp[i0 + a];
+    for (int l = 0; l < V; ++l)
+      for (int32_t q = l; q < nq; q += V) lanes[a * V + l].push_back({a, q});
+  }
+}
+
+// Shared-memory bank balancing of one staged segment (in place).  At every
+// time step each lane of a warp reads one quad (tiled_block_schedule), and
+// position k of those quads is one warp-wide ld.shared: v2.f64 for the pair
+// tile, served in 4 phases of 8 lanes, f64 otherwise, 2 phases of 16 lanes
+// (measured: tools/lds_probe.cu).  A phase costs as many wavefronts as the
+// largest number of distinct addresses in one bank group (16-B groups: col % 8
+// for pairs; 8-B groups: col % 16).  Within a row the entry order is free (its
+// partial dot product is one sum), so each row's entries are redistributed over
+// its own quads.  Per slot, lanes with the fewest choices go first and take the
+// free bank group with the most entries left in the block (a phase needs at
+// least as many wavefronts as its most loaded group has entries, so those are
+// drained first); a lane that would conflict uses one of its row's pads if it
+// has one, reading an address another lane already reads (a broadcast).
+void balance_banks(uint16_t* cols, int32_t* perm, const int32_t* rp, int32_t nr, int V, int elem) {
+  const int G = elem == 2 ? 8 : 16;                           // bank groups = lanes per phase
+  std::vector<std::vector<std::pair<uint16_t, int32_t>>> bucket;
+  std::vector<int32_t> left, slots, rows;
+  std::vector<uint32_t> mask;
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> lanes;
+  const int64_t nslot = 4 * (int64_t)rp[nr];
+  std::vector<uint16_t> ncol(nslot, 0);
+  std::vector<int32_t> nperm(nslot, -1);
+  const int nblk = tiled_blocks(nr, V);
+  for (int blk = 0; blk < nblk; ++blk) {
+    tiled_block_schedule(rp, nr, V, blk, rows, lanes);
+    const int R = (int)rows.size();
+    bucket.assign((size_t)R * G, {});
+    left.assign(R, 0);
+    slots.assign(R, 0);
+    mask.assign(R, 0);
+    int rem[16] = {0};
+    size_t tmax = 0;
+    for (const auto& ln : lanes) tmax = std::max(tmax, ln.size());
     for (int a = 0; a < R; ++a) {
-      const int32_t q0 = rp[i0 + a], q1 = rp[i0 + a + 1];
-      tmax = std::max(tmax, (q1 - q0 + V - 1) / V);
-      left[a] = 0;
-      for (int g = 0; g < G; ++g) bucket[(size_t)a * G + g].clear();
-      for (int64_t s = 4 * (int64_t)q0; s < 4 * (int64_t)q1; ++s)
-        if (perm[s] >= 0) { bucket[(size_t)a * G + cols[s] % G].push_back({cols[s], perm[s]}); ++left[a]; }
-    }
-    // new contents of each row's slots, written after the row's quads are assigned
-    out.assign(4 * (size_t)(rp[i0 + R] - rp[i0]), {0, -1});
-    for (int32_t t = 0; t < tmax; ++t) {
-      bool zero_read = false;
-      if (t % U)
-        for (int a = 0; a < R && !zero_read; ++a) {
-          const int32_t nq = rp[i0 + a + 1] - rp[i0 + a];
-          // some lane l < V has quad l + (t-1)V in the row but l + tV past its end
-          zero_read = nq > (t - 1) * V && nq < (t + 1) * V;
+      const int32_t q0 = rp[rows[a]], q1 = rp[rows[a] + 1];
+      slots[a] = 4 * (q1 - q0);
+      for (int64_t e = 4 * (int64_t)q0; e < 4 * (int64_t)q1; ++e)
+        if (perm[e] >= 0) {
+          const int g = cols[e] % G;
+          bucket[(size_t)a * G + g].push_back({cols[e], perm[e]});
+          mask[a] |= 1u << g;
+          ++rem[g];
+          ++left[a];
         }
-      for (int k = 0; k < 4; ++k) {
-        int hist[16] = {0};
-        if (zero_read) hist[0] = 1;
-        for (int a = 0; a < R; ++a) {
-          const int32_t q0 = rp[i0 + a], nq = rp[i0 + a + 1] - q0;
-          for (int l = 0; l < V; ++l) {
-            const int32_t q = l + t * V;
-            if (q >= nq) break;
-            const size_t slot = 4 * (size_t)(q0 - rp[i0] + q) + k;
-            int best = -1;
-            for (int g = 0; g < G; ++g)
-              if ((left[a] == 0 || !bucket[(size_t)a * G + g].empty()) && (best < 0 || hist[g] < hist[best])) best = g;
-            if (left[a] > 0) {
-              auto& b = bucket[(size_t)a * G + best];
-              out[slot] = b.back();
-              b.pop_back();
-              --left[a];
-            } else {
-              out[slot] = {(uint16_t)(best < valid ? best : 0), -1};   // pad: value 0, emptiest group
+    }
+    int unit_a[16];
+    int64_t unit_slot[16];
+    for (size_t t = 0; t < tmax; ++t)
+      for (int k = 0; k < 4; ++k)
+        for (int ph = 0; ph < 32 / G; ++ph) {
+          int nu = 0;
+          for (int lane = ph * G; lane < ph * G + G; ++lane) {
+            if (t >= lanes[lane].size()) continue;
+            const int a = lanes[lane][t].first;
+            unit_a[nu] = a;
+            unit_slot[nu] = 4 * (int64_t)(rp[rows[a]] + lanes[lane][t].second) + k;
+            ++nu;
+          }
+          // fewest choices first (insertion sort on the popcount of the row's groups)
+          for (int x = 1; x < nu; ++x)
+            for (int y = x; y > 0 && __builtin_popcount(mask[unit_a[y]]) < __builtin_popcount(mask[unit_a[y - 1]]); --y) {
+              std::swap(unit_a[y], unit_a[y - 1]);
+              std::swap(unit_slot[y], unit_slot[y - 1]);
             }
-            ++hist[best];
+          uint32_t used = 0;
+          int any_col = -1;
+          for (int x = 0; x < nu; ++x) {
+            const int a = unit_a[x];
+            const int64_t slot = unit_slot[x];
+            const uint32_t avail = mask[a] & ~used;
+            int g = -1;
+            if (avail || (left[a] > 0 && slots[a] == left[a])) {
+              const uint32_t from = avail ? avail : mask[a];        // forced: a conflict
+              for (int h = 0; h < G; ++h)
+                if ((from >> h & 1u) && (g < 0 || rem[h] > rem[g])) g = h;
+            }
+            if (g >= 0) {
+              auto& b = bucket[(size_t)a * G + g];
+              ncol[slot] = b.back().first;
+              nperm[slot] = b.back().second;
+              b.pop_back();
+              if (b.empty()) mask[a] &= ~(1u << g);
+              --rem[g];
+              --left[a];
+              used |= 1u << g;
+              if (any_col < 0) any_col = ncol[slot];
+            } else {                                                // pad: re-read an address
+              ncol[slot] = (uint16_t)(any_col >= 0 ? any_col : 0);
+              nperm[slot] = -1;
+              if (any_col < 0) any_col = 0;
+            }
+            --slots[a];
           }
         }
-      }
-    }
-    const size_t base = 4 * (size_t)rp[i0];
-    for (size_t s = 0; s < out.size(); ++s) { cols[base + s] = out[s].first; perm[base + s] = out[s].second; }
   }
+  std::copy(ncol.begin(), ncol.end(), cols);
+  std::copy(nperm.begin(), nperm.end(), perm);
 }
 
 // Chunks [row_a, row_b) (row_a a multiple of kTRows) into H, offsets local to H.
@@ -227,16 +278,26 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
     for (int32_t i = 0; i < nr; ++i)
       for (int64_t p = ptr[r0 + i]; p < ptr[r0 + i + 1]; ++p) rc[(size_t)seg_k(col[p] / T) * nr + i]++;
     std::vector<int64_t> rpbase(nseg);
+    // staged segments hold their rows longest first (stable), so that the
+    // lanes of a warp run rows of about equal length; pos_of maps row -> position
+    std::vector<int32_t> pos_of((size_t)nseg * nr), order(nr);
     for (int k = 0; k < nseg; ++k) {
       TSeg& S = H.seg[s_begin + k];
       const bool stg = S.tile >= 0;
+      const int32_t* rck = rc.data() + (size_t)k * nr;
+      for (int32_t i = 0; i < nr; ++i) order[i] = i;
+      if (stg) std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return rck[a] > rck[b]; });
       rpbase[k] = (int64_t)H.rowptr.size();
       S.rp = rpbase[k];
       H.rowptr.resize(H.rowptr.size() + nr + 1, 0);
+      H.srow.resize(H.rowptr.size(), 0);
       int64_t units = 0;                                  // quads (staged) or entries (direct)
-      for (int32_t i = 0; i < nr; ++i) {
-        const int32_t u = stg ? (rc[(size_t)k * nr + i] + 3) / 4 : rc[(size_t)k * nr + i];
-        H.rowptr[rpbase[k] + i + 1] = H.rowptr[rpbase[k] + i] + u;
+      for (int32_t pos = 0; pos < nr; ++pos) {
+        const int32_t i = order[pos];
+        const int32_t u = stg ? (rck[i] + 3) / 4 : rck[i];
+        H.rowptr[rpbase[k] + pos + 1] = H.rowptr[rpbase[k] + pos] + u;
+        H.srow[rpbase[k] + pos] = (uint16_t)i;
+        pos_of[(size_t)k * nr + i] = pos;
         units += u;
       }
       S.V = pick_v(stg ? (double)units / nr : (double)seg_nz[k] / nr, elem);
@@ -260,25 +321,24 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
         const int k = seg_k(t);
         const TSeg& S = H.seg[s_begin + k];
         const int32_t f = fill[(size_t)k * nr + i]++;
+        const int32_t pos = pos_of[(size_t)k * nr + i];
         if (S.tile >= 0) {
-          const int64_t q = S.nz + 4 * (int64_t)H.rowptr[rpbase[k] + i] + f;
+          const int64_t q = S.nz + 4 * (int64_t)H.rowptr[rpbase[k] + pos] + f;
           H.col_s[q] = (uint16_t)(col[p] - t * T);
           H.perm_s[q] = (int32_t)p;
           H.staged++;
         } else {
-          const int64_t q = S.nz + H.rowptr[rpbase[k] + i] + f;
+          const int64_t q = S.nz + H.rowptr[rpbase[k] + pos] + f;
           H.col_d[q] = col[p];
           H.perm_d[q] = (int32_t)p;
         }
       }
-    static const bool balance = !std::getenv("PDCS_TILE_BALANCE") || std::atoi(std::getenv("PDCS_TILE_BALANCE"));
+    const bool balance = !std::getenv("PDCS_TILE_BALANCE") || std::atoi(std::getenv("PDCS_TILE_BALANCE"));
     if (balance)
       for (int k = 0; k < nseg; ++k) {
         const TSeg& S = H.seg[s_begin + k];
         if (S.tile < 0 || S.V > 32) continue;
-        const int32_t valid = (int32_t)std::min<int64_t>(T, nvec - (int64_t)S.tile * T);
-        balance_banks(H.col_s.data() + S.nz, H.perm_s.data() + S.nz, H.rowptr.data() + rpbase[k], nr, S.V, elem,
-                      valid);
+        balance_banks(H.col_s.data() + S.nz, H.perm_s.data() + S.nz, H.rowptr.data() + rpbase[k], nr, S.V, elem);
       }
     // work items: consecutive segments up to group_nz nonzeros; the staged
     // segments of an item are cut into TMA batches of <= kBQ quads
@@ -374,6 +434,7 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
     H.scratch += P.scratch;
     H.staged += P.staged;
     H.rowptr.insert(H.rowptr.end(), P.rowptr.begin(), P.rowptr.end());
+    H.srow.insert(H.srow.end(), P.srow.begin(), P.srow.end());
     H.col_s.insert(H.col_s.end(), P.col_s.begin(), P.col_s.end());
     H.perm_s.insert(H.perm_s.end(), P.perm_s.begin(), P.perm_s.end());
     H.col_d.insert(H.col_d.end(), P.col_d.begin(), P.col_d.end());
@@ -382,6 +443,7 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
   }
   H.col_s.resize(H.col_s.size() + 8, 0);      // TMA column-id copies may read one quad past the end
   H.rowptr.resize(H.rowptr.size() + 8, 0);    // TMA row-pointer slices are rounded up to 16 B
+  H.srow.resize(H.rowptr.size(), 0);
   H.perm_s.resize(H.col_s.size(), -1);
   H.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
 }
@@ -456,7 +518,7 @@ struct pdcs_ctx {
     DBuf<TChunk> chunk;
     DBuf<TSeg> seg;
     DBuf<int32_t> rowptr, col_d;
-    DBuf<uint16_t> col_s;
+    DBuf<uint16_t> col_s, srow;
     DBuf<double> val_s, val_d, scratch;
     int g_partial = 0, g_combine = 0;
     int64_t slot = 0;
@@ -838,6 +900,7 @@ struct pdcs_ctx {
     upload(D.chunk, H.chunk, st);
     upload(D.seg, H.seg, st);
     upload(D.rowptr, H.rowptr, st);
+    upload(D.srow, H.srow, st);
     upload(D.col_s, H.col_s, st);
     upload(D.col_d, H.col_d, st);
     DBuf<int32_t> perm;
@@ -857,7 +920,7 @@ struct pdcs_ctx {
     TiledMat& M = D.M;
     M.m = rows; M.nvec = nvec; M.nwork = (int64_t)H.work.size(); M.nchunk = (int64_t)H.chunk.size();
     M.T = H.T; M.elem = elem;
-    M.work = D.work.p; M.chunk = D.chunk.p; M.seg = D.seg.p; M.rowptr = D.rowptr.p;
+    M.work = D.work.p; M.chunk = D.chunk.p; M.seg = D.seg.p; M.rowptr = D.rowptr.p; M.srow = D.srow.p;
     M.val_s = D.val_s.p; M.col_s = D.col_s.p; M.val_d = D.val_d.p; M.col_d = D.col_d.p;
     M.batch = D.batch.p;
     // TMA-pipelined variant (k_tiled_tma) is opt-in: on B200 it measured slower than
@@ -933,7 +996,7 @@ struct pdcs_ctx {
       D.tune_tiled_ms = tt;
       if (!(tt < 0.9f * tc)) {
         D.on = false;
-        D.work.free_(); D.chunk.free_(); D.seg.free_(); D.rowptr.free_(); D.col_d.free_(); D.col_s.free_();
+        D.work.free_(); D.chunk.free_(); D.seg.free_(); D.rowptr.free_(); D.srow.free_(); D.col_d.free_(); D.col_s.free_();
         D.val_s.free_(); D.val_d.free_(); D.scratch.free_();
       }
     }
@@ -1838,6 +1901,88 @@ int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
 int64_t pdcs_launch_count(const pdcs_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 void pdcs_destroy(pdcs_ctx* ctx) { delete ctx; }
+
+int pdcs_tiled_layout_stats(const int64_t* row_ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
+                            double* out, int cap) {
+  if (!row_ptr || (!col && row_ptr[rows] > 0) || rows < 0 || nvec <= 0 || (elem != 1 && elem != 2) || !out)
+    return 0;
+  TiledHost H;
+  build_tiled(row_ptr, col, rows, nvec, elem, H);
+  // simulate the shared-memory gathers of k_tiled_partial along the schedule
+  // of tiled_block_schedule: per (block, time step, quad position) one
+  // ld.shared; a phase of P lanes costs the largest number of distinct
+  // addresses in one bank group
+  const int P = elem == 2 ? 8 : 16;
+  double quads = 0, pads = 0, inst = 0, wav = 0, segs = 0, bound = 0;
+  std::vector<int32_t> brows;
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> lanes;
+  for (size_t si = 0; si < H.seg.size(); ++si) {
+    const TSeg& S = H.seg[si];
+    if (S.tile < 0) continue;
+    segs += 1;
+    const int32_t* rp = H.rowptr.data() + S.rp;
+    int32_t nr = 0;
+    for (const TWork& W : H.work)
+      if ((int64_t)si >= W.s0 && (int64_t)si < W.s1) { nr = H.chunk[W.chunk].nrows; break; }
+    quads += rp[nr] - rp[0];
+    for (int64_t e = 4 * (int64_t)rp[0]; e < 4 * (int64_t)rp[nr]; ++e) pads += H.perm_s[S.nz + e] < 0;
+    const int nblk = tiled_blocks(nr, S.V);
+    for (int blk = 0; blk < nblk; ++blk) {
+      tiled_block_schedule(rp, nr, S.V, blk, brows, lanes);
+      size_t tmax = 0;
+      for (const auto& ln : lanes) tmax = std::max(tmax, ln.size());
+      for (int ph = 0; ph < 32 / P; ++ph) {
+        int load[16] = {0};
+        double active_slots = 0;
+        for (size_t t = 0; t < tmax; ++t)
+          for (int k = 0; k < 4; ++k) {
+            int cnt[16] = {0};
+            int seen[16][16];
+            int active = 0;
+            for (int lane = ph * P; lane < ph * P + P; ++lane) {
+              if (t >= lanes[lane].size()) continue;
+              ++active;
+              const int64_t e = S.nz + 4 * (int64_t)(rp[brows[lanes[lane][t].first]] + lanes[lane][t].second) + k;
+              const int c = H.col_s[e];
+              const int g = c % P;
+              if (H.perm_s[e] >= 0) ++load[g];
+              bool dup = false;
+              for (int z = 0; z < cnt[g]; ++z) dup |= seen[g][z] == c;
+              if (!dup) seen[g][cnt[g]++] = c;
+            }
+            if (active) { wav += *std::max_element(cnt, cnt + P); active_slots += 1; }
+          }
+        bound += std::max<double>(active_slots, (double)*std::max_element(load, load + P));
+      }
+      inst += 4.0 * (double)tmax;
+    }
+  }
+  // structure check: every CSR entry stored exactly once, under its own column
+  const int64_t nnz = H.nnz;
+  std::vector<uint8_t> hit(nnz, 0);
+  double bad = 0;
+  for (size_t si = 0; si < H.seg.size(); ++si) {
+    const TSeg& S = H.seg[si];
+    int32_t nr = 0;
+    for (const TWork& W : H.work)
+      if ((int64_t)si >= W.s0 && (int64_t)si < W.s1) { nr = H.chunk[W.chunk].nrows; break; }
+    const int32_t* rp = H.rowptr.data() + S.rp;
+    const int64_t ne = S.tile >= 0 ? 4 * (int64_t)rp[nr] : rp[nr];
+    for (int64_t e = 0; e < ne; ++e) {
+      const int32_t pp = S.tile >= 0 ? H.perm_s[S.nz + e] : H.perm_d[S.nz + e];
+      if (pp < 0) continue;
+      const int64_t c = S.tile >= 0 ? (int64_t)S.tile * H.T + H.col_s[S.nz + e] : H.col_d[S.nz + e];
+      if (pp >= nnz || hit[pp] || c != col[pp]) { bad += 1; continue; }
+      hit[pp] = 1;
+    }
+  }
+  for (int64_t q = 0; q < nnz; ++q) bad += hit[q] == 0;
+  const double v[11] = {(double)H.nnz, (double)H.staged, quads, pads, segs, (double)H.work.size(), inst, wav,
+                        H.build_ms, bound, bad};
+  const int k = std::min(cap, 11);
+  for (int i = 0; i < k; ++i) out[i] = v[i];
+  return k;
+}
 
 pdcs_status pdcs_nccl_unique_id(void* out128) {
   if (!out128) return PDCS_ERR_ARG;

@@ -64,6 +64,7 @@ struct TiledMat {
   const TChunk* chunk = nullptr;
   const TSeg* seg = nullptr;
   const int32_t* rowptr = nullptr;
+  const uint16_t* srow = nullptr;     // segment position -> chunk-local row (parallel to rowptr)
   const double* val_s = nullptr;
   const uint16_t* col_s = nullptr;
   const double* val_d = nullptr;
@@ -133,16 +134,17 @@ __device__ __forceinline__ void seg_row_dot_quad(const double* __restrict__ val4
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
+      if (q0 + u * V < qe)                 // no shared-memory wavefronts for slots past the row
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (ELEM == 2) {
-          const double2 v = lds_v2(xs_s + c[u][k] * 16u);
-          s1 += a[u][k] * v.x;
-          s2 += a[u][k] * v.y;
-        } else {
-          s1 += a[u][k] * lds_f64(xs_s + c[u][k] * 8u);
+        for (int k = 0; k < 4; ++k) {
+          if (ELEM == 2) {
+            const double2 v = lds_v2(xs_s + c[u][k] * 16u);
+            s1 += a[u][k] * v.x;
+            s2 += a[u][k] * v.y;
+          } else {
+            s1 += a[u][k] * lds_f64(xs_s + c[u][k] * 8u);
+          }
         }
-      }
   }
   if (V > 1) {
 #pragma unroll
@@ -206,8 +208,9 @@ __device__ __forceinline__ void seg_rows(const TiledMat& M, const TSeg& S, const
     if (staged) seg_row_dot_quad<V, ELEM>(M.val_s + S.nz, M.col_s + S.nz, xs_s, b, e, lane, s1, s2);
     else seg_row_dot_direct<V, ELEM>(M.val_d + S.nz, M.col_d + S.nz, xs, b, e, lane, s1, s2);
     if (lane == 0 && r < C.nrows) {
-      acc[r * ELEM] += s1;
-      if (ELEM == 2) acc[r * ELEM + 1] += s2;
+      const int rr = __ldg(M.srow + S.rp + r);
+      acc[rr * ELEM] += s1;
+      if (ELEM == 2) acc[rr * ELEM + 1] += s2;
     }
   }
 }
@@ -324,8 +327,9 @@ __device__ __forceinline__ void batch_rows(const TiledMat& M, const TSeg& S, con
       }
     }
     if (lane == 0 && r < B.rb) {
-      acc[r * ELEM] += s1;
-      if (ELEM == 2) acc[r * ELEM + 1] += s2;
+      const int rr = __ldg(M.srow + S.rp + r);
+      acc[rr * ELEM] += s1;
+      if (ELEM == 2) acc[rr * ELEM + 1] += s2;
     }
   }
 }

@@ -1,0 +1,102 @@
+"""Host-side tests of the column-tiled SpMV layout builder,
+through the host-only diagnostic pdcs_tiled_layout_stats (no GPU needed).
+
+The builder decides which entries are staged through shared-memory tiles,
+packs them into zero-padded quads, sorts each segment's rows by length and
+permutes entries inside rows to balance shared-memory banks.  None of that may
+lose, duplicate or relabel an entry (structure_errors == 0), the result must
+not depend on the number of host build threads, and the bank balancing must
+lower the modeled wavefront count without going below its lower bound.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_2505_00311_b200 import _lib
+from instances import gen_lasso, gen_mpo, gen_fisher
+
+
+def _csr(prog):
+    K = sp.csr_matrix((prog.vals, prog.col_idx, prog.row_ptr), shape=(prog.m, prog.n))
+    KT = K.T.tocsr()
+    KT.sort_indices()
+    return K, KT
+
+
+def _stats(A, nvec, elem):
+    return _lib.pdcs_tiled_layout_stats(A.indptr.astype(np.int64), A.indices.astype(np.int32), nvec, elem)
+
+
+def _random_csr(rng, rows, cols, row_len):
+    ptr = [0]
+    idx = []
+    for _ in range(rows):
+        k = int(rng.integers(row_len[0], row_len[1] + 1))
+        c = np.sort(rng.choice(cols, size=min(k, cols), replace=False))
+        idx.append(c)
+        ptr.append(ptr[-1] + len(c))
+    idx = np.concatenate(idx) if idx else np.zeros(0, np.int64)
+    return sp.csr_matrix((np.ones(len(idx)), idx, ptr), shape=(rows, cols))
+
+
+@pytest.mark.parametrize("kb", ["1", "4", "32"])
+def test_layout_structure_lasso(monkeypatch, kb):
+    monkeypatch.setenv("PDCS_TILE_KB", kb)
+    prog = gen_lasso(6000, 700, 0.03, seed=2)
+    K, KT = _csr(prog)
+    for A, nvec, elem in [(K, prog.n, 2), (KT, prog.m, 1)]:
+        st = _stats(A, nvec, elem)
+        assert st["nnz"] == A.nnz
+        assert st["structure_errors"] == 0
+        assert st["quads"] * 4 == st["staged"] + st["pads"]
+        assert st["lds_wavefronts"] >= st["lds_wavefront_bound"] - 1e-9
+
+
+def test_layout_structure_ragged_and_degenerate(monkeypatch):
+    """Ragged rows (0 .. 300 entries), empty rows, a single row, a single column."""
+    monkeypatch.setenv("PDCS_TILE_KB", "1")
+    rng = np.random.default_rng(5)
+    cases = [_random_csr(rng, 3000, 900, (0, 300)), _random_csr(rng, 1, 5000, (4000, 4000)),
+             _random_csr(rng, 2500, 1, (0, 1)), _random_csr(rng, 1500, 3000, (0, 0))]
+    for A in cases:
+        for elem, nvec in [(2, A.shape[1]), (1, A.shape[1])]:
+            st = _stats(A, nvec, elem)
+            assert st["nnz"] == A.nnz and st["structure_errors"] == 0
+
+
+def test_layout_other_configs(monkeypatch):
+    monkeypatch.setenv("PDCS_TILE_KB", "4")
+    for prog in [gen_mpo(4, 60, seed=1), gen_fisher(300, 40, 0.2, seed=1)]:
+        K, KT = _csr(prog)
+        assert _stats(K, prog.n, 2)["structure_errors"] == 0
+        assert _stats(KT, prog.m, 1)["structure_errors"] == 0
+
+
+def test_layout_independent_of_build_threads(monkeypatch):
+    monkeypatch.setenv("PDCS_TILE_KB", "2")
+    prog = gen_lasso(9000, 500, 0.04, seed=3)
+    K, _ = _csr(prog)
+    out = []
+    for nth in ["1", "3", "8"]:
+        monkeypatch.setenv("PDCS_BUILD_THREADS", nth)
+        st = _stats(K, prog.n, 2)
+        st.pop("build_ms")
+        out.append(st)
+    assert out[0] == out[1] == out[2]
+
+
+def test_bank_balancing_lowers_wavefronts(monkeypatch):
+    """The model charges each 8-lane (pairs) / 16-lane (doubles) phase the
+    largest number of distinct addresses in one bank group (tools/lds_probe.cu
+    measured this rule on B200).  Balancing must beat the unbalanced layout and
+    come within 30% of the per-phase lower bound."""
+    prog = gen_lasso(20000, 10000, 0.01, seed=0)
+    K, KT = _csr(prog)
+    for A, nvec, elem in [(K, prog.n, 2), (KT, prog.m, 1)]:
+        monkeypatch.setenv("PDCS_TILE_BALANCE", "0")
+        raw = _stats(A, nvec, elem)
+        monkeypatch.setenv("PDCS_TILE_BALANCE", "1")
+        bal = _stats(A, nvec, elem)
+        assert raw["structure_errors"] == 0 and bal["structure_errors"] == 0
+        assert bal["lds_wavefronts"] < 0.85 * raw["lds_wavefronts"], (raw, bal)
+        assert bal["lds_wavefronts"] <= 1.3 * bal["lds_wavefront_bound"], bal

@@ -469,3 +469,176 @@ def gen_mixed(m: int, n1: int, n2: int, seed: int = 0, row_len=(3, 12),
 def rows_of(row_ptr: np.ndarray) -> np.ndarray:
     m = row_ptr.shape[0] - 1
     return np.repeat(np.arange(m, dtype=np.int64), np.diff(row_ptr))
+
+
+# --------------------------------------------------------------------------
+# Mixed-cone planted instance at scale (SURVEY §8(d) cfg 5), vectorised
+# --------------------------------------------------------------------------
+def _blocks_of_kind(rng, kind: int, total: int, dims_fn, min_dim: int):
+    """Blocks of one kind whose dims sum to exactly `total` (a short last block
+    becomes NonNeg)."""
+    if total <= 0:
+        return np.zeros(0, np.int32), np.zeros(0, np.int64)
+    d = dims_fn(max(16, int(2 * total / 3) + 16))
+    while d.sum() < total:
+        d = np.concatenate([d, dims_fn(max(16, d.shape[0]))])
+    cs = np.cumsum(d)
+    nb = int(np.searchsorted(cs, total)) + 1
+    d = d[:nb].copy()
+    d[-1] -= cs[nb - 1] - total
+    k = np.full(nb, kind, np.int32)
+    if d[-1] < min_dim:
+        k[-1] = NONNEG
+    return k, d.astype(np.int64)
+
+
+def _mixed_cones(rng, total: int, shares, giant=()):
+    """Cone list over `total` coordinates: kind shares of the coordinates,
+    SOC dims log-uniform in [3, 4096] (+ giant SOC blocks), RSOC in [3, 256],
+    exp / dual exp 3, Zero / NonNeg runs U{1..64}; blocks in random order."""
+    def logu(lo, hi):
+        return lambda k: np.floor(np.exp(rng.uniform(math.log(lo), math.log(hi + 1), k))).astype(np.int64)
+    dims = {ZERO: lambda k: rng.integers(1, 65, k), NONNEG: lambda k: rng.integers(1, 65, k),
+            SOC: logu(3, 4096), RSOC: logu(3, 256), EXP: lambda k: np.full(k, 3), DUAL_EXP: lambda k: np.full(k, 3)}
+    mins = {ZERO: 1, NONNEG: 1, SOC: 2, RSOC: 3, EXP: 3, DUAL_EXP: 3}
+    kinds, ds = [], []
+    used = 0
+    for g in giant:
+        kinds.append(np.array([SOC], np.int32)); ds.append(np.array([g], np.int64)); used += g
+    order = list(shares.items())
+    for i, (kind, f) in enumerate(order):
+        t = int(round(f * total)) if i < len(order) - 1 else total - used
+        if kind == SOC:
+            t -= sum(giant)
+        t = max(t, 0)
+        if kind in (EXP, DUAL_EXP):
+            t -= t % 3
+        k, d = _blocks_of_kind(rng, kind, t, dims[kind], mins[kind])
+        kinds.append(k); ds.append(d); used += int(d.sum())
+    k = np.concatenate(kinds); d = np.concatenate(ds)
+    if used < total:                      # rounding remainder
+        k = np.concatenate([k, [NONNEG]]).astype(np.int32); d = np.concatenate([d, [total - used]])
+    p = rng.permutation(k.shape[0])
+    return k[p].astype(np.int32), d[p].astype(np.int64)
+
+
+def _planted_pairs(rng, kinds, dims):
+    """Complementary (s in K, y in K*, <s, y> = 0) for every block, vectorised
+    per kind (same construction as _cone_pair)."""
+    total = int(dims.sum())
+    s = np.zeros(total); y = np.zeros(total)
+    off = np.concatenate([[0], np.cumsum(dims)[:-1]]).astype(np.int64)
+    elem = np.repeat(kinds, dims)
+    zr = elem == ZERO
+    y[zr] = rng.standard_normal(int(zr.sum()))
+    nn = elem == NONNEG
+    a = rng.uniform(0.0, 1.0, int(nn.sum())); b = rng.uniform(0.0, 1.0, int(nn.sum()))
+    pick = rng.uniform(size=a.shape[0]) < 0.5
+    s[nn] = np.where(pick, 0.0, a); y[nn] = np.where(pick, b, 0.0)
+    for kind in (SOC, RSOC):
+        sel = np.nonzero(kinds == kind)[0]
+        if not sel.size:
+            continue
+        o, d = off[sel], dims[sel]
+        idx = np.concatenate([np.arange(oo, oo + dd) for oo, dd in zip(o, d)]) if sel.size < 20000 else \
+            np.repeat(o, d) + (np.arange(int(d.sum())) - np.repeat(np.cumsum(d) - d, d))
+        v = rng.standard_normal(idx.shape[0])
+        head = np.repeat(np.cumsum(d) - d, 1)               # block starts within idx
+        v[head] = 0.0
+        nv = np.sqrt(np.add.reduceat(v * v, head))
+        v[head] = nv
+        ab = rng.uniform(0.0, 1.0, (sel.size, 2))
+        mode = rng.integers(0, 3, sel.size)
+        ab[mode == 1, 0] = 0.0
+        ab[mode == 2, 1] = 0.0
+        sa = np.repeat(ab[:, 0], d); sb = np.repeat(ab[:, 1], d)
+        sv = sa * v
+        yv = -sb * v
+        yv[head] = sb[head] * nv
+        if kind == RSOC:                                    # rotate the leading pair
+            for z in (sv, yv):
+                t0, t1 = z[head].copy(), z[head + 1].copy()
+                z[head] = (t0 + t1) / math.sqrt(2.0)
+                z[head + 1] = (t0 - t1) / math.sqrt(2.0)
+        s[idx] = sv; y[idx] = yv
+    for kind in (EXP, DUAL_EXP):
+        sel = np.nonzero(kinds == kind)[0]
+        if not sel.size:
+            continue
+        o = off[sel]
+        rho = rng.uniform(-2.0, 2.0, sel.size)
+        ab = rng.uniform(0.1, 1.0, (sel.size, 2))
+        mode = rng.integers(0, 4, sel.size)
+        ab[mode == 1, 0] = 0.0
+        ab[mode == 2, 1] = 0.0
+        pe = ab[:, :1] * np.stack([rho, np.ones_like(rho), np.exp(rho)], 1)
+        de = ab[:, 1:] * np.stack([-np.ones_like(rho), rho - 1.0, np.exp(-rho)], 1)
+        if kind == DUAL_EXP:
+            pe, de = de, pe
+        for j in range(3):
+            s[o + j] = pe[:, j]; y[o + j] = de[:, j]
+    return s, y
+
+
+def gen_mixed_large(scale: float = 0.125, seed: int = 0) -> ConicProgram:
+    """SURVEY §8(d) cfg 5 at `scale` (1.0: m = 2e7, n = 1e7, nnz ~ 2e9; the
+    default 1/8 is one GPU's share of the 8-GPU job).  Rows of U{20..180}
+    distinct uniform columns; values N(0,1) 10^U[-2,2] (row) 10^U[-2,2] (col).
+    Row cones: 30% Zero, 30% NonNeg, 25% SOC (log-uniform dims in [3, 4096]
+    plus 4 blocks of 2.5e5*scale), 5% RSOC ([3, 256]), 7.5% Exp, 2.5% DualExp.
+    Columns: 40% box (1/4 each free, [l,inf), (-inf,u], [l,u]), 60% primal
+    cones: Zero 1%, NonNeg 20%, SOC 40%, RSOC 15%, Exp 20%, DualExp 4%.
+    Planted KKT pair as gen_mixed: h = G x* - s*, c = G^T y* + lam*."""
+    rng = _rng(seed)
+    m = int(round(2e7 * scale)); n = int(round(1e7 * scale))
+    n1 = int(round(0.4 * n)); n2 = n - n1
+    lens = rng.integers(20, 181, size=m).astype(np.int64)
+    lens = np.minimum(lens, n)
+    row_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(row_ptr[-1])
+    rows = np.repeat(np.arange(m, dtype=np.int64), lens)
+    key = rows * n + rng.integers(0, n, nnz)
+    while True:                                            # distinct columns within each row
+        key.sort()
+        dup = np.nonzero(key[1:] == key[:-1])[0] + 1
+        if dup.size == 0:
+            break
+        key[dup] = (key[dup] // n) * n + rng.integers(0, n, dup.size)
+    col = (key % n).astype(np.int32)
+    del key
+    rf = 10.0 ** rng.uniform(-2.0, 2.0, m)
+    cf = 10.0 ** rng.uniform(-2.0, 2.0, n)
+    val = rng.standard_normal(nnz) * rf[rows] * cf[col]
+    giant = tuple([max(3, int(2.5e5 * scale))] * 4)
+    rk, rdim = _mixed_cones(rng, m, {ZERO: .30, NONNEG: .30, SOC: .25, RSOC: .05, EXP: .075, DUAL_EXP: .025},
+                            giant=giant)
+    pk, pdim = _mixed_cones(rng, n2, {ZERO: .01, NONNEG: .20, SOC: .40, RSOC: .15, EXP: .20, DUAL_EXP: .04})
+    # box part and its planted (x, lam): interior, at lower, at upper
+    btype = rng.integers(0, 4, size=n1)
+    lo = rng.uniform(-1.0, 0.0, n1)
+    hi = rng.uniform(0.0, 1.0, n1) + lo + 0.5
+    l = np.where((btype == 1) | (btype == 3), lo, -INF)
+    u = np.where((btype == 2) | (btype == 3), hi, INF)
+    status = rng.integers(0, 3, size=n1)
+    fl, fu = np.isfinite(l), np.isfinite(u)
+    atl = (status == 1) & fl
+    atu = (status == 2) & fu & ~atl
+    inter = ~(atl | atu)
+    x1 = np.where(fl & fu, rng.uniform(0.0, 1.0, n1) * (np.where(fu, u, 0) - np.where(fl, l, 0)) + np.where(fl, l, 0),
+                  np.where(fl, np.where(fl, l, 0) + rng.uniform(0.0, 1.0, n1),
+                           np.where(fu, np.where(fu, u, 0) - rng.uniform(0.0, 1.0, n1), rng.standard_normal(n1))))
+    x1 = np.where(atl, l, np.where(atu, u, x1))
+    lam1 = np.where(atl, rng.uniform(0.0, 1.0, n1), np.where(atu, -rng.uniform(0.0, 1.0, n1), 0.0))
+    lam1[inter] = 0.0
+    x2, lam2 = _planted_pairs(rng, pk, pdim)
+    s_star, y_star = _planted_pairs(rng, rk, rdim)
+    x_star = np.concatenate([x1, x2]); lam = np.concatenate([lam1, lam2])
+    Gx = np.bincount(rows, weights=val * x_star[col], minlength=m)
+    GTy = np.bincount(col, weights=val * y_star[rows], minlength=n)
+    del rows
+    prog = ConicProgram(m=m, n=n, n1=n1, row_ptr=row_ptr, col_idx=col, vals=val,
+                        c=GTy + lam, h=Gx - s_star, l=l, u=u, pk=pk, pdim=pdim, rk=rk, rdim=rdim,
+                        name=f"mixed_cfg5_scale{scale:g}_s{seed}")
+    prog.x_star, prog.y_star = x_star, y_star
+    prog.obj_star = float(prog.c @ x_star)
+    return prog

@@ -61,6 +61,32 @@ struct CtaTeam {
   }
 };
 
+// Cluster team: the kClusterCtas CTAs of a thread-block cluster.  Each pass's
+// CTA sums are exchanged through distributed shared memory and added in rank
+// order, so every CTA gets the same bits.  sm holds 2 * (blockDim/32) + 2 doubles.
+struct ClusterTeam {
+  double* sm;
+  __device__ int rank() const { return (int)cooperative_groups::this_cluster().block_rank() * blockDim.x + threadIdx.x; }
+  __device__ int size() const { return (int)cooperative_groups::this_cluster().num_blocks() * blockDim.x; }
+  __device__ void sum2(double& a, double& b) {
+    CtaTeam c{sm};
+    c.sum2(a, b);
+    auto cl = cooperative_groups::this_cluster();
+    const int slot = 2 * (blockDim.x >> 5);
+    if (threadIdx.x == 0) { sm[slot] = a; sm[slot + 1] = b; }
+    cl.sync();
+    double sa = 0.0, sb = 0.0;
+    for (unsigned int r = 0; r < cl.num_blocks(); ++r) {
+      const double* p = cl.map_shared_rank(sm, r);
+      sa += p[slot];
+      sb += p[slot + 1];
+    }
+    cl.sync();                       // the slots may be rewritten by the next pass
+    a = sa;
+    b = sb;
+  }
+};
+
 // Whole-grid team (cooperative launch).  gbuf holds 2 buffers x 2 x gridDim doubles.
 struct GridTeam {
   double* sm;      // >= 2*(blockDim/32) + 2 doubles of shared memory
@@ -159,8 +185,8 @@ __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool un
       for (int64_t i = 1 + r; i < d; i += S) {
         const double x = X(i), h = H(i), h2 = h * h;
         double p, w;
-        if (mode == SM_LAM) { const double den = h2 + 2.0 * par; p = h * x / den; w = p * p / den; }
-        else { const double den = 1.0 + par * h2; p = h * x / den; w = p * p * h2 / den; }
+        if (mode == SM_LAM) { const double rd = 1.0 / (h2 + 2.0 * par); p = h * x * rd; w = p * p * rd; }
+        else { const double rd = 1.0 / (1.0 + par * h2); p = h * x * rd; w = p * p * h2 * rd; }
         S0 += p * p;
         S1 += w;
       }
@@ -226,17 +252,24 @@ __device__ __forceinline__ bool d_in_exp_dual(double r, double s, double t, doub
 // magnitude of its terms.  u = (dr rho, ds, dt e^rho), w = (1/dr, (1-rho)/ds,
 // -e^-rho/dt) span the Moreau pair of Eq. 17, <u, w> = 0.
 struct ExpDet { double g, dg, mag; };
-__device__ __forceinline__ ExpDet exp_det(double r0, double s0, double t0, double dr, double ds,
-                                          double dt, double rho) {
+// Ratios of the divisors, computed once per cone (the same quotients as
+// inline: bit-identical, 6 fp64 divisions fewer per determinant evaluation).
+struct ExpRatios {
+  double dr, ds, sd_t, dt_s, dt_r, dr_t, dr_s, ds_r;   // ds/dt, dt/ds, dt/dr, dr/dt, dr/ds, ds/dr
+  __device__ ExpRatios(double dr_, double ds_, double dt_)
+      : dr(dr_), ds(ds_), sd_t(ds_ / dt_), dt_s(dt_ / ds_), dt_r(dt_ / dr_), dr_t(dr_ / dt_), dr_s(dr_ / ds_),
+        ds_r(ds_ / dr_) {}
+};
+__device__ __forceinline__ ExpDet exp_det(double r0, double s0, double t0, const ExpRatios& q, double rho) {
   const double e0 = exp(-fabs(rho));
   const double ep = rho >= 0.0 ? 1.0 : e0 * e0;     // e^{rho - |rho|}
   const double em = rho >= 0.0 ? e0 * e0 : 1.0;     // e^{-rho - |rho|}
-  const double cr = -(ds / dt) * em - (dt / ds) * (1.0 - rho) * ep;
-  const double cs = (dt / dr) * ep + (dr / dt) * rho * em;
-  const double ct = (dr * rho * (1.0 - rho) / ds - ds / dr) * e0;
-  const double dcr = (ds / dt) * em + (dt / ds) * rho * ep;
-  const double dcs = (dt / dr) * ep + (dr / dt) * (1.0 - rho) * em;
-  const double dct = dr * (1.0 - 2.0 * rho) / ds * e0;
+  const double cr = -q.sd_t * em - q.dt_s * (1.0 - rho) * ep;
+  const double cs = q.dt_r * ep + q.dr_t * rho * em;
+  const double ct = (q.dr * rho * (1.0 - rho) / q.ds - q.ds_r) * e0;
+  const double dcr = q.sd_t * em + q.dt_s * rho * ep;
+  const double dcs = q.dt_r * ep + q.dr_t * (1.0 - rho) * em;
+  const double dct = q.dr * (1.0 - 2.0 * rho) / q.ds * e0;
   ExpDet o;
   o.g = r0 * cr + s0 * cs + t0 * ct;
   o.dg = r0 * dcr + s0 * dcs + t0 * dct;
@@ -262,6 +295,7 @@ __device__ __noinline__ void proj_exp_d(double r0, double s0, double t0, double 
     if (d_in_exp_dual(w0, w1, w2, tol)) { o0 = 0.0; o1 = 0.0; o2 = 0.0; return; }
   }
   if (r0 <= 0.0 && s0 <= 0.0) { o0 = r0; o1 = 0.0; o2 = fmax(t0, 0.0); return; }   // case 3
+  const ExpRatios q(dr, ds, dt);
   // case 4: bracket (Eq. 16); an end whose det is rounding
   // noise is the root.
   double rho = __builtin_nan("");
@@ -273,30 +307,30 @@ __device__ __noinline__ void proj_exp_d(double r0, double s0, double t0, double 
     lo = fmin(a3, a4); hi = fmax(a3, a4);
     if (lo == hi) { rho = lo; found = true; }
     else {
-      slo = det_sign(exp_det(r0, s0, t0, dr, ds, dt, lo));
-      shi = det_sign(exp_det(r0, s0, t0, dr, ds, dt, hi));
+      slo = det_sign(exp_det(r0, s0, t0, q, lo));
+      shi = det_sign(exp_det(r0, s0, t0, q, hi));
       if (slo == 0) { rho = lo; found = true; } else if (shi == 0) { rho = hi; found = true; }
     }
   } else if (s0 > 0.0) {          // r0 <= 0 < s0: (-inf, a3)
     hi = r0 * ds / (s0 * dr);
-    shi = det_sign(exp_det(r0, s0, t0, dr, ds, dt, hi));
+    shi = det_sign(exp_det(r0, s0, t0, q, hi));
     if (shi == 0) { rho = hi; found = true; }
     else {
       for (int j = 0; j < 200; ++j) {      // doubling, cap 200 (A19)
         lo = hi - ldexp(1.0, j);
-        slo = det_sign(exp_det(r0, s0, t0, dr, ds, dt, lo));
+        slo = det_sign(exp_det(r0, s0, t0, q, lo));
         if (slo != shi) break;
       }
       if (slo == 0) { rho = lo; found = true; }
     }
   } else {                        // s0 <= 0 < r0: (a4, inf)
     lo = 1.0 - s0 * ds / (r0 * dr);
-    slo = det_sign(exp_det(r0, s0, t0, dr, ds, dt, lo));
+    slo = det_sign(exp_det(r0, s0, t0, q, lo));
     if (slo == 0) { rho = lo; found = true; }
     else {
       for (int j = 0; j < 200; ++j) {
         hi = lo + ldexp(1.0, j);
-        shi = det_sign(exp_det(r0, s0, t0, dr, ds, dt, hi));
+        shi = det_sign(exp_det(r0, s0, t0, q, hi));
         if (shi != slo) break;
       }
       if (shi == 0) { rho = hi; found = true; }
@@ -310,7 +344,7 @@ __device__ __noinline__ void proj_exp_d(double r0, double s0, double t0, double 
     rho = 0.5 * (lo + hi);
     double dxold = hi - lo, dx = dxold;
     for (int it = 0; it < 200; ++it) {
-      const ExpDet e = exp_det(r0, s0, t0, dr, ds, dt, rho);
+      const ExpDet e = exp_det(r0, s0, t0, q, rho);
       const int s = det_sign(e);
       if (s == 0) break;
       if (s == slo) lo = rho; else hi = rho;

@@ -12,6 +12,9 @@
 namespace pdcs {
 
 constexpr int kThreads = 256;          // CTA size of the streaming kernels
+constexpr int kThreadsSmall = 64;
+constexpr int kNClass = 5;             // cone block size classes: thread, warp, cta, cluster, grid
+constexpr int kClusterCtas = 8;        // CTAs per thread-block cluster of the cluster class      // CTA size of the thread-per-cone kernel (spreads cones over all SMs)
 constexpr int kCtaPerSm = 4;           // resident CTAs per SM targeted by grid sizing
 constexpr double kRsqrt2 = 0.70710678118654752440;  // 1/sqrt(2), RSOC rotation
 

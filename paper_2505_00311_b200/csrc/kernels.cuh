@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads) k_blocks_thread(BlockArgs A, const C
   finish_block_partials(A, acc, kv);
 }
 
-// One block per warp (SOC/RSOC of dim 33..2048).
+// One block per warp (SOC/RSOC of dim 33..512).
 __global__ void __launch_bounds__(kThreads) k_blocks_warp(BlockArgs A, const Ctl* ctl) {
   if (!block_op_active(A, ctl)) return;
   Acc<kAcc> acc; acc.zero();
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) k_blocks_warp(BlockArgs A, const Ctl
   finish_block_partials(A, acc, kv);
 }
 
-// One block per CTA (SOC/RSOC of dim > 2048).
+// One block per CTA (SOC/RSOC of dim 513..4096).
 __global__ void __launch_bounds__(kThreads) k_blocks_cta(BlockArgs A, const Ctl* ctl) {
   if (!block_op_active(A, ctl)) return;
   __shared__ double sm[2 * (kThreads / 32) + 2];
@@ -251,6 +251,23 @@ __global__ void __launch_bounds__(kThreads) k_blocks_cta(BlockArgs A, const Ctl*
   double kv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   CtaTeam tm{sm};
   for (int64_t bi = blockIdx.x; bi < A.nblocks; bi += gridDim.x) {
+    const Block b = A.blocks[bi];
+    run_block(tm, A, ctl, b, acc, kv);
+  }
+  finish_block_partials(A, acc, kv);
+}
+
+// One block per thread-block cluster of kClusterCtas CTAs (SOC/RSOC of dim
+// 4097..131072): per-pass reductions through distributed shared memory.
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
+    k_blocks_cluster(BlockArgs A, const Ctl* ctl) {
+  if (!block_op_active(A, ctl)) return;
+  __shared__ double sm[2 * (kThreads / 32) + 2];
+  Acc<kAcc> acc; acc.zero();
+  double kv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  ClusterTeam tm{sm};
+  const int64_t cid = blockIdx.x / kClusterCtas, ncl = gridDim.x / kClusterCtas;
+  for (int64_t bi = cid; bi < A.nblocks; bi += ncl) {
     const Block b = A.blocks[bi];
     run_block(tm, A, ctl, b, acc, kv);
   }

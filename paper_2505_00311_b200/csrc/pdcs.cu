@@ -540,7 +540,7 @@ struct pdcs_ctx {
 
   // block classes per side: [thread, warp, cta, grid] ranges into the block arrays
   struct BClass { int64_t begin = 0, count = 0; int grid = 0; int64_t slot = 0; int64_t kslot[2] = {0, 0}; };
-  BClass pcls[4], rcls[4];
+  BClass pcls[kNClass], rcls[kNClass];   // thread, warp, cta, cluster, grid
   int64_t nslot_trial = 0, nslot_kkt = 0;
   int64_t slot_pe = 0, slot_spmv = 0, kslot_rows = 0, kslot_cols = 0;
   int g_pe = 0, g_m = 0, g_kr = 0, g_kc = 0, g_grid = 0;
@@ -659,7 +659,7 @@ struct pdcs_ctx {
   }
   void run_blocks(bool primal, BlockArgs A, bool kkt, int cand) {
     BClass* cl = primal ? pcls : rcls;
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < kNClass; ++c) {
       if (cl[c].count == 0) continue;
       BlockArgs B = A;
       B.blocks = A.blocks + cl[c].begin;
@@ -668,10 +668,12 @@ struct pdcs_ctx {
       B.part = kkt ? kpart.p : tpart.p;
       B.slot0 = kkt ? cl[c].kslot[cand] : cl[c].slot;
       const int g = cl[c].grid;
-      if (c == 0) launch("blocks_thread", [&] { k_blocks_thread<<<g, kThreads, 0, st>>>(B, ctl); });
+      if (c == 0) launch("blocks_thread", [&] { k_blocks_thread<<<g, kThreadsSmall, 0, st>>>(B, ctl); });
       else if (c == 1) launch("blocks_warp", [&] { k_blocks_warp<<<g, kThreads, 0, st>>>(B, ctl); });
       else if (c == 2) {
         launch("blocks_cta", [&] { k_blocks_cta<<<g, kThreads, 0, st>>>(B, ctl); });
+      } else if (c == 3) {
+        launch("blocks_cluster", [&] { k_blocks_cluster<<<g, kThreads, 0, st>>>(B, ctl); });
       } else {
         double* gb = gbuf.p;
         const Ctl* cp = ctl;
@@ -764,7 +766,7 @@ struct pdcs_ctx {
   void zero_cand1_kslots() {
     for (int side = 0; side < 2; ++side) {
       BClass* cl = side ? pcls : rcls;
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < kNClass; ++c)
         if (cl[c].count)
           CK(cudaMemsetAsync(kpart.p + cl[c].kslot[1] * kKAcc, 0, (size_t)cl[c].grid * kKAcc * sizeof(double), st));
     }
@@ -1409,22 +1411,34 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
       off += rdim[b];
     }
     if (off != mg) fail(PDCS_ERR_CONE, "row cone dims do not sum to m");
-    // size classes: thread (exp, soc <= 32), warp (<= 2048), cta (<= 131072), grid
+    // Size classes: thread (exp, soc <= 32), warp (<= 512), cta (<= 4096),
+    // cluster of kClusterCtas CTAs (<= 131072), grid.  Within a class blocks are
+    // ordered by (kind, dim) so that the lanes / warps of a launch run the same
+    // code path with similar trip counts.
     auto classify = [&](std::vector<Block>& v, pdcs_ctx::BClass* cl) {
-      auto cls = [](const Block& b) { return (b.kind == C_EXP || b.kind == C_DEXP || b.dim <= 32) ? 0 : b.dim <= 2048 ? 1 : b.dim <= 131072 ? 2 : 3; };
-      std::stable_sort(v.begin(), v.end(), [&](const Block& a, const Block& b) { return cls(a) < cls(b); });
-      for (int c = 0; c < 4; ++c) cl[c] = pdcs_ctx::BClass{};
+      auto cls = [](const Block& b) {
+        return (b.kind == C_EXP || b.kind == C_DEXP || b.dim <= 32) ? 0 : b.dim <= 512 ? 1 : b.dim <= 4096 ? 2
+               : b.dim <= 131072 ? 3 : 4;
+      };
+      std::stable_sort(v.begin(), v.end(), [&](const Block& a, const Block& b) {
+        const int ca = cls(a), cb = cls(b);
+        if (ca != cb) return ca < cb;
+        if (a.kind != b.kind) return a.kind < b.kind;
+        return a.dim < b.dim;
+      });
+      for (int c = 0; c < kNClass; ++c) cl[c] = pdcs_ctx::BClass{};
       for (size_t i = 0; i < v.size(); ++i) {
         const int c = cls(v[i]);
         if (cl[c].count == 0) cl[c].begin = (int64_t)i;
         cl[c].count++;
       }
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < kNClass; ++c) {
         const int64_t cnt = cl[c].count;
         if (!cnt) continue;
-        if (c == 0) cl[c].grid = grid_for(cnt, ctx->sms, 8);
+        if (c == 0) cl[c].grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + kThreadsSmall - 1) / kThreadsSmall, (int64_t)ctx->sms * 32));
         else if (c == 1) cl[c].grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 7) / 8, (int64_t)ctx->sms * 8));
         else if (c == 2) cl[c].grid = (int)std::min<int64_t>(cnt, (int64_t)ctx->sms * 4);
+        else if (c == 3) cl[c].grid = kClusterCtas * (int)std::min<int64_t>(cnt, (int64_t)ctx->sms * 2 / kClusterCtas);
         else {
           int nb = 0;
           CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_blocks_grid, kThreads, 0));
@@ -1448,9 +1462,9 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     ctx->g_kc = grid_for(n, ctx->sms, 4);
     int64_t s = 0;
     ctx->slot_pe = s; s += ctx->g_pe;
-    for (int c = 0; c < 4; ++c) if (ctx->pcls[c].count) { ctx->pcls[c].slot = s; s += ctx->pcls[c].grid; }
+    for (int c = 0; c < kNClass; ++c) if (ctx->pcls[c].count) { ctx->pcls[c].slot = s; s += ctx->pcls[c].grid; }
     ctx->slot_spmv = s; s += std::max<int64_t>(ctx->K.plan.total_cta, (int64_t)ctx->sms * 4);
-    for (int c = 0; c < 4; ++c) if (ctx->rcls[c].count) { ctx->rcls[c].slot = s; s += ctx->rcls[c].grid; }
+    for (int c = 0; c < kNClass; ++c) if (ctx->rcls[c].count) { ctx->rcls[c].slot = s; s += ctx->rcls[c].grid; }
     ctx->nslot_trial = s;
     int64_t ks = 0;
     ctx->kslot_rows = ks; ks += ctx->g_kr;
@@ -1458,7 +1472,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     for (int cand = 0; cand < 2; ++cand)
       for (int side = 0; side < 2; ++side) {
         pdcs_ctx::BClass* cl = side ? ctx->pcls : ctx->rcls;
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < kNClass; ++c)
           if (cl[c].count) {
             cl[c].kslot[cand] = ks;
             ks += cl[c].grid;

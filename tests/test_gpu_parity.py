@@ -344,3 +344,62 @@ def test_tiled_build_threads_and_bank_balance(P, tiled_env, monkeypatch):
     o = O.OracleSolver(prog, vanilla_pdhg=1)
     o.iterate(60)
     assert parity(*runs["t1"], *o.get_iterate(0)) <= TOL
+
+
+def test_cfg5_recipe_parity(P):
+    """SURVEY §8(d) cfg 5 recipe (row lengths 20..180, values over 8 decades,
+    all six cone kinds, log-uniform SOC dims up to 4096 -> thread/warp/CTA
+    teams, planted optimum) at a size the oracle runs in seconds: one Eq. 5
+    step from random points at 1e-12, then checkpoint shadowing."""
+    from instances import gen_mixed_large
+    prog = gen_mixed_large(0.0003, seed=4)
+    rng = np.random.default_rng(4)
+    g = P.PdcsSolver(prog)
+    o = O.OracleSolver(prog)
+    ro, qo = o.get_scaling()
+    rg, qg = g.get_scaling()
+    np.testing.assert_allclose(rg, ro, rtol=1e-13)
+    np.testing.assert_allclose(qg, qo, rtol=1e-13)
+    for _ in range(2):
+        x = rng.standard_normal(prog.n) * 3
+        y = rng.standard_normal(prog.m) * 3
+        g.set_iterate(x, y)
+        o.set_iterate(x * qo, y * ro)
+        g.iterate(1)
+        o.iterate(1)
+        assert parity(*g.get_iterate(P.PDHG_OUT), *o.get_iterate(1)) <= 1e-12
+    g.close()
+    worst = _shadow(P, prog, 120)
+    assert worst <= TOL, worst
+
+
+def test_cta_and_grid_teams_one_step(P):
+    """Rescaled SOC / RSOC blocks on the CTA team (513..4096 entries), the
+    thread-block-cluster team (4097..131072, DSMEM reductions) and the
+    whole-grid cooperative team (> 131072): one Eq. 5 step from random points
+    against the oracle's projection (Thm 1)."""
+    prog = gen_mixed(3000, 100, 150000, seed=11, soc_dims=(600, 2000), scale_spread=1.5,
+                     col_mix=[(SOC, 1.0)], row_len=(3, 12))
+    assert prog.pdim.max() > 131072 or (prog.rdim.max() > 512)
+    big = [d for k, d in zip(prog.pk, prog.pdim) if k == SOC]
+    prog2 = gen_mixed(3000, 100, 150000, seed=12, soc_dims=(140000, 150000), scale_spread=1.5,
+                      col_mix=[(SOC, 1.0)], row_len=(3, 12))
+    assert max(d for k, d in zip(prog2.pk, prog2.pdim) if k == SOC) > 131072
+    assert max(big) > 512
+    prog3 = gen_mixed(3000, 100, 150000, seed=13, soc_dims=(5000, 40000), scale_spread=1.5,
+                      col_mix=[(SOC, 0.7), (RSOC, 0.3)], row_len=(3, 12))
+    assert any(4096 < d <= 131072 for d in prog3.pdim)            # cluster team
+    for pr in (prog, prog2, prog3):
+        rng = np.random.default_rng(7)
+        g = P.PdcsSolver(pr)
+        o = O.OracleSolver(pr)
+        ro, qo = o.get_scaling()
+        for _ in range(2):
+            x = rng.standard_normal(pr.n) * 3
+            y = rng.standard_normal(pr.m) * 3
+            g.set_iterate(x, y)
+            o.set_iterate(x * qo, y * ro)
+            g.iterate(1)
+            o.iterate(1)
+            assert parity(*g.get_iterate(P.PDHG_OUT), *o.get_iterate(1)) <= 1e-12
+        g.close()

@@ -1,0 +1,32 @@
+"""Input generators (instances/): recipe properties and planted optima.
+
+The planted mixed-cone instance of SURVEY §8(d) cfg 5 must be an exact KKT
+point of Eq. 1-2: Eq. 9 at (x*, y*), evaluated by the
+oracle, is zero up to rounding, and c^T x* is the optimal value.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from instances import gen_mixed_large, ZERO, NONNEG, SOC, RSOC, EXP, DUAL_EXP
+
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_cfg5_recipe_and_planted_kkt(seed):
+    p = gen_mixed_large(0.0003, seed=seed)
+    assert p.m == 6000 and p.n == 3000 and p.n1 == 1200
+    lens = np.diff(p.row_ptr)
+    assert lens.min() >= 20 and lens.max() <= 180
+    for i in range(0, p.m, 97):                                 # distinct sorted columns per row
+        c = p.col_idx[p.row_ptr[i]:p.row_ptr[i + 1]]
+        assert np.all(np.diff(c) > 0)
+    assert p.rdim.sum() == p.m and p.pdim.sum() == p.n - p.n1
+    share = np.bincount(np.repeat(p.rk, p.rdim), minlength=6) / p.m
+    assert np.allclose(share, [.30, .30, .25, .05, .075, .025], atol=0.002)
+    pshare = np.bincount(np.repeat(p.pk, p.pdim), minlength=6) / (p.n - p.n1)
+    assert np.allclose(pshare, [.01, .20, .40, .15, .20, .04], atol=0.003)
+    assert np.all(p.rdim[(p.rk == EXP) | (p.rk == DUAL_EXP)] == 3)
+    assert np.all(p.rdim[p.rk == SOC] >= 2) and np.all(p.rdim[p.rk == RSOC] >= 3)
+    e = O.OracleSolver(p).kkt_point(p.x_star, p.y_star)
+    assert e["err_p"] < 1e-13 and e["err_d"] < 1e-13 and e["err_gap"] < 1e-12
+    assert abs(e["pobj"] - p.obj_star) <= 1e-12 * max(1.0, abs(p.obj_star))

@@ -3,17 +3,20 @@ import sys, os, argparse
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2505_00311_b200 as P
-from instances import gen_lasso, gen_fisher, gen_mpo
+from instances import gen_lasso, gen_fisher, gen_mpo, gen_mixed_large
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="lasso")
 ap.add_argument("--m", type=int, default=200000)
 ap.add_argument("--iters", type=int, default=30)
+ap.add_argument("--scale", type=float, default=1.0 / 32)
 a = ap.parse_args()
 if a.config == "lasso":
     prog = gen_lasso(a.m, 10000, 0.01, seed=0)
 elif a.config == "fisher":
     prog = gen_fisher(10000, 1000, 0.2, seed=0)
+elif a.config == "mixed":
+    prog = gen_mixed_large(a.scale, seed=0)
 else:
     prog = gen_mpo(20, 1000, seed=0)
 g = P.PdcsSolver(prog)

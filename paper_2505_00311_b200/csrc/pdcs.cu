@@ -91,6 +91,7 @@ struct TiledHost {
   std::vector<uint16_t> col_s;
   std::vector<int32_t> col_d;
   std::vector<int32_t> perm_s, perm_d;
+  std::vector<int32_t> blkb;       // sliced staged segments: segment-relative first quad of each warp block
   int64_t scratch = 0, staged = 0, nnz = 0;
   int32_t T = 0, elem = 1;
   double build_ms = 0.0;
@@ -99,6 +100,19 @@ struct TiledHost {
 // shared-memory tile size in bytes (PDCS_TILE_KB overrides; default 32 KB)
 int tiled_tile_bytes() {
   static const int b = std::getenv("PDCS_TILE_KB") ? 1024 * std::atoi(std::getenv("PDCS_TILE_KB")) : 32768;
+  return b;
+}
+
+// TMA-pipelined partial kernel (opt-in, PDCS_TMA=1): it streams row-major
+// segments, so the sliced layout is off with it.
+bool tiled_tma_env() {
+  static const bool b = std::getenv("PDCS_TMA") && std::atoi(std::getenv("PDCS_TMA")) != 0;
+  return b;
+}
+// sliced (warp-interleaved) staged segments, tiled.cuh seg_row_dot_sliced;
+// PDCS_TILE_SLICED=0 keeps the row-major quad layout
+bool tiled_sliced() {
+  static const bool b = !tiled_tma_env() && !(std::getenv("PDCS_TILE_SLICED") && std::atoi(std::getenv("PDCS_TILE_SLICED")) == 0);
   return b;
 }
 
@@ -132,6 +146,59 @@ void tiled_block_schedule(const int32_t* rp, int32_t nr, int V, int blk, std::ve
     for (int l = 0; l < V; ++l)
       for (int32_t q = l; q < nq; q += V) lanes[a * V + l].push_back({a, q});
   }
+}
+
+// Physical quad (segment-relative) of logical quad j of segment position pos:
+// row-major, or sliced (warp block base + (pos in block) * V + j % V + 32 (j / V)).
+int64_t quad_slot(const std::vector<int32_t>& blkb, const TSeg& S, const int32_t* rp, int32_t pos, int32_t j) {
+  if (S.bb < 0) return (int64_t)rp[pos] + j;
+  const int rpw = 32 / S.V;
+  return (int64_t)blkb[S.bb + pos / rpw] + (pos % rpw) * S.V + j % S.V + 32 * (int64_t)(j / S.V);
+}
+
+// Re-lay the staged segments among [s0, s1) of the chunk just built (all at
+// the end of H.col_s, in order) in the sliced layout of seg_row_dot_sliced.
+// The bank balancing is preserved: every (warp block, time step, lane) reads
+// the same quad as before.  Segments start on 16-quad boundaries (512 B of
+// values, 128 B of column ids), so a warp's loads cover whole lines.
+void slice_segments(TiledHost& H, int32_t s0, int32_t s1, int32_t nr) {
+  int64_t base = -1;
+  for (int32_t si = s0; si < s1; ++si)
+    if (H.seg[si].tile >= 0) { base = H.seg[si].nz; break; }
+  if (base < 0) return;
+  std::vector<uint16_t> nc;
+  std::vector<int32_t> np;
+  for (int32_t si = s0; si < s1; ++si) {
+    TSeg& S = H.seg[si];
+    if (S.tile < 0) continue;
+    const int32_t* rp = H.rowptr.data() + S.rp;
+    const int64_t off = (int64_t)((base + (int64_t)nc.size() + 63) & ~(int64_t)63) - base;
+    const int rpw = 32 / S.V;
+    const int nblk = tiled_blocks(nr, S.V);
+    S.bb = (int64_t)H.blkb.size();
+    int64_t cur = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+      H.blkb.push_back((int32_t)cur);
+      int32_t tmax = 0;
+      for (int a = 0; a < rpw && blk * rpw + a < nr; ++a) {
+        const int32_t nq = rp[blk * rpw + a + 1] - rp[blk * rpw + a];
+        tmax = std::max(tmax, (nq + S.V - 1) / S.V);
+      }
+      cur += 32 * (int64_t)tmax;
+    }
+    nc.resize(off + 4 * cur, 0);
+    np.resize(off + 4 * cur, -1);
+    for (int32_t pos = 0; pos < nr; ++pos)
+      for (int32_t j = 0; j < rp[pos + 1] - rp[pos]; ++j) {
+        const int64_t from = S.nz + 4 * ((int64_t)rp[pos] + j), to = off + 4 * quad_slot(H.blkb, S, rp, pos, j);
+        for (int k = 0; k < 4; ++k) { nc[to + k] = H.col_s[from + k]; np[to + k] = H.perm_s[from + k]; }
+      }
+    S.nz = base + off;
+  }
+  H.col_s.resize(base);
+  H.perm_s.resize(base);
+  H.col_s.insert(H.col_s.end(), nc.begin(), nc.end());
+  H.perm_s.insert(H.perm_s.end(), np.begin(), np.end());
 }
 
 // Shared-memory bank balancing of one staged segment (in place).  At every
@@ -265,10 +332,10 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
     }
     const int32_t s_begin = (int32_t)H.seg.size();
     std::vector<int64_t> seg_nz;
-    if (direct_nz) { H.seg.push_back(TSeg{-1, 1, 0, 0}); seg_nz.push_back(direct_nz); }
+    if (direct_nz) { H.seg.push_back(TSeg{-1, 1, 0, 0, -1}); seg_nz.push_back(direct_nz); }
     for (int64_t t : staged_tiles) {
       segof[t] = (int32_t)(H.seg.size() - s_begin);
-      H.seg.push_back(TSeg{(int32_t)t, 1, 0, 0});
+      H.seg.push_back(TSeg{(int32_t)t, 1, 0, 0, -1});
       seg_nz.push_back(cnt[t]);
     }
     const int nseg = (int)seg_nz.size();
@@ -340,8 +407,10 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
         if (S.tile < 0 || S.V > 32) continue;
         balance_banks(H.col_s.data() + S.nz, H.perm_s.data() + S.nz, H.rowptr.data() + rpbase[k], nr, S.V, elem);
       }
+    if (tiled_sliced()) slice_segments(H, s_begin, s_begin + nseg, nr);
     // work items: consecutive segments up to group_nz nonzeros; the staged
-    // segments of an item are cut into TMA batches of <= kBQ quads
+    // segments of an item are cut into TMA batches of <= kBQ quads (row-major
+    // layout only, PDCS_TMA=1)
     auto emit_item = [&](int32_t gg, int32_t sa, int32_t sb) {
       const int32_t b0 = (int32_t)H.batch.size();
       int32_t ord = -1;
@@ -415,15 +484,22 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
   H.elem = elem;
   H.nnz = ptr[rows];
   size_t ns = 0, nd = 0, nrp = 0;
-  for (const auto& P : part) { ns += P.col_s.size() + 8; nd += P.col_d.size(); nrp += P.rowptr.size(); }
+  for (const auto& P : part) { ns += P.col_s.size() + 64; nd += P.col_d.size(); nrp += P.rowptr.size(); }
   H.col_s.reserve(ns + 8); H.perm_s.reserve(ns + 8); H.col_d.reserve(nd); H.perm_d.reserve(nd);
   H.rowptr.reserve(nrp + 8);
   for (auto& P : part) {
-    H.col_s.resize((H.col_s.size() + 7) & ~(size_t)7, 0);    // keep segment starts 16-B aligned
+    H.col_s.resize((H.col_s.size() + 63) & ~(size_t)63, 0);  // keep segment starts 512-B aligned (values)
     H.perm_s.resize(H.col_s.size(), -1);
+    const int64_t bbbase = (int64_t)H.blkb.size();
     const int64_t sbase = (int64_t)H.seg.size(), bbase = (int64_t)H.batch.size(), cbase = (int64_t)H.chunk.size();
     const int64_t rpb = (int64_t)H.rowptr.size(), nzs = (int64_t)H.col_s.size(), nzd = (int64_t)H.col_d.size();
-    for (TSeg S : P.seg) { S.rp += rpb; S.nz += S.tile >= 0 ? nzs : nzd; H.seg.push_back(S); }
+    for (TSeg S : P.seg) {
+      S.rp += rpb;
+      S.nz += S.tile >= 0 ? nzs : nzd;
+      if (S.bb >= 0) S.bb += bbbase;
+      H.seg.push_back(S);
+    }
+    H.blkb.insert(H.blkb.end(), P.blkb.begin(), P.blkb.end());
     for (TBatch B : P.batch) { B.seg += (int32_t)sbase; H.batch.push_back(B); }
     for (TWork W : P.work) {
       W.chunk += (int32_t)cbase; W.s0 += (int32_t)sbase; W.s1 += (int32_t)sbase;
@@ -442,6 +518,7 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
     P = TiledHost();
   }
   H.col_s.resize(H.col_s.size() + 8, 0);      // TMA column-id copies may read one quad past the end
+  H.blkb.push_back(0);                        // never empty (device upload)
   H.rowptr.resize(H.rowptr.size() + 8, 0);    // TMA row-pointer slices are rounded up to 16 B
   H.srow.resize(H.rowptr.size(), 0);
   H.perm_s.resize(H.col_s.size(), -1);
@@ -517,7 +594,7 @@ struct pdcs_ctx {
     bool tma = true;
     DBuf<TChunk> chunk;
     DBuf<TSeg> seg;
-    DBuf<int32_t> rowptr, col_d;
+    DBuf<int32_t> rowptr, col_d, blkb;
     DBuf<uint16_t> col_s, srow;
     DBuf<double> val_s, val_d, scratch;
     int g_partial = 0, g_combine = 0;
@@ -881,13 +958,16 @@ struct pdcs_ctx {
     launch(name, [&] {
       if (elem == 2) {
         if (D.tma) k_tiled_tma<2><<<D.g_partial, kTThreads, tma_smem(2), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        else if (tiled_sliced()) k_tiled_sliced<2><<<D.g_partial, kTThreads, sliced_smem(2), st>>>(D.M, xin, D.scratch.p, ctl, guard);
         else k_tiled_partial<2><<<D.g_partial, kTThreads, tiled_smem(2), st>>>(D.M, xin, D.scratch.p, ctl, guard);
       } else {
         if (D.tma) k_tiled_tma<1><<<D.g_partial, kTThreads, tma_smem(1), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        else if (tiled_sliced()) k_tiled_sliced<1><<<D.g_partial, kTThreads, sliced_smem(1), st>>>(D.M, xin, D.scratch.p, ctl, guard);
         else k_tiled_partial<1><<<D.g_partial, kTThreads, tiled_smem(1), st>>>(D.M, xin, D.scratch.p, ctl, guard);
       }
     });
   }
+  static size_t sliced_smem(int elem) { return 2 * (size_t)tiled_tile_bytes() + (size_t)kTRows * elem * sizeof(double); }
   static size_t tiled_smem(int elem) { return (size_t)tiled_tile_bytes() + (size_t)kTRows * elem * sizeof(double); }
 
   // Build the tiled copy of a CSR (structure on the host, scaled values on the device).
@@ -905,6 +985,7 @@ struct pdcs_ctx {
     upload(D.srow, H.srow, st);
     upload(D.col_s, H.col_s, st);
     upload(D.col_d, H.col_d, st);
+    upload(D.blkb, H.blkb, st);
     DBuf<int32_t> perm;
     D.val_s.alloc(std::max<size_t>(H.col_s.size(), 1));
     D.val_d.alloc(std::max<size_t>(H.col_d.size(), 1));
@@ -925,19 +1006,24 @@ struct pdcs_ctx {
     M.work = D.work.p; M.chunk = D.chunk.p; M.seg = D.seg.p; M.rowptr = D.rowptr.p; M.srow = D.srow.p;
     M.val_s = D.val_s.p; M.col_s = D.col_s.p; M.val_d = D.val_d.p; M.col_d = D.col_d.p;
     M.batch = D.batch.p;
+    M.blkb = D.blkb.p;
     // TMA-pipelined variant (k_tiled_tma) is opt-in: on B200 it measured slower than
     // the 4-CTA/SM register-streaming kernel, PDCS_TMA=1 enables it.
-    D.tma = std::getenv("PDCS_TMA") && std::atoi(std::getenv("PDCS_TMA")) != 0;
+    D.tma = tiled_tma_env();
     int occ = 1;
     if (elem == 2) {
       CK(cudaFuncSetAttribute(k_tiled_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(2)));
+      CK(cudaFuncSetAttribute(k_tiled_sliced<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(2)));
       CK(cudaFuncSetAttribute(k_tiled_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(2)));
       if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<2>, kTThreads, tma_smem(2)));
+      else if (tiled_sliced()) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_sliced<2>, kTThreads, sliced_smem(2)));
       else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<2>, kTThreads, tiled_smem(2)));
     } else {
       CK(cudaFuncSetAttribute(k_tiled_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(1)));
+      CK(cudaFuncSetAttribute(k_tiled_sliced<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(1)));
       CK(cudaFuncSetAttribute(k_tiled_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(1)));
       if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<1>, kTThreads, tma_smem(1)));
+      else if (tiled_sliced()) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_sliced<1>, kTThreads, sliced_smem(1)));
       else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<1>, kTThreads, tiled_smem(1)));
     }
     D.g_partial = (int)std::max<int64_t>(1, std::min<int64_t>(M.nwork, (int64_t)sms * std::max(occ, 1)));
@@ -999,6 +1085,7 @@ struct pdcs_ctx {
       if (!(tt < 0.9f * tc)) {
         D.on = false;
         D.work.free_(); D.chunk.free_(); D.seg.free_(); D.rowptr.free_(); D.srow.free_(); D.col_d.free_(); D.col_s.free_();
+        D.blkb.free_();
         D.val_s.free_(); D.val_d.free_(); D.scratch.free_();
       }
     }
@@ -1939,7 +2026,9 @@ int pdcs_tiled_layout_stats(const int64_t* row_ptr, const int32_t* col, int64_t 
     for (const TWork& W : H.work)
       if ((int64_t)si >= W.s0 && (int64_t)si < W.s1) { nr = H.chunk[W.chunk].nrows; break; }
     quads += rp[nr] - rp[0];
-    for (int64_t e = 4 * (int64_t)rp[0]; e < 4 * (int64_t)rp[nr]; ++e) pads += H.perm_s[S.nz + e] < 0;
+    for (int32_t pos = 0; pos < nr; ++pos)
+      for (int32_t j = 0; j < rp[pos + 1] - rp[pos]; ++j)
+        for (int k = 0; k < 4; ++k) pads += H.perm_s[S.nz + 4 * quad_slot(H.blkb, S, rp, pos, j) + k] < 0;
     const int nblk = tiled_blocks(nr, S.V);
     for (int blk = 0; blk < nblk; ++blk) {
       tiled_block_schedule(rp, nr, S.V, blk, brows, lanes);
@@ -1956,7 +2045,7 @@ int pdcs_tiled_layout_stats(const int64_t* row_ptr, const int32_t* col, int64_t 
             for (int lane = ph * P; lane < ph * P + P; ++lane) {
               if (t >= lanes[lane].size()) continue;
               ++active;
-              const int64_t e = S.nz + 4 * (int64_t)(rp[brows[lanes[lane][t].first]] + lanes[lane][t].second) + k;
+              const int64_t e = S.nz + 4 * quad_slot(H.blkb, S, rp, brows[lanes[lane][t].first], lanes[lane][t].second) + k;
               const int c = H.col_s[e];
               const int g = c % P;
               if (H.perm_s[e] >= 0) ++load[g];
@@ -1981,13 +2070,19 @@ int pdcs_tiled_layout_stats(const int64_t* row_ptr, const int32_t* col, int64_t 
     for (const TWork& W : H.work)
       if ((int64_t)si >= W.s0 && (int64_t)si < W.s1) { nr = H.chunk[W.chunk].nrows; break; }
     const int32_t* rp = H.rowptr.data() + S.rp;
-    const int64_t ne = S.tile >= 0 ? 4 * (int64_t)rp[nr] : rp[nr];
-    for (int64_t e = 0; e < ne; ++e) {
+    auto visit = [&](int64_t e) {
       const int32_t pp = S.tile >= 0 ? H.perm_s[S.nz + e] : H.perm_d[S.nz + e];
-      if (pp < 0) continue;
+      if (pp < 0) return;
       const int64_t c = S.tile >= 0 ? (int64_t)S.tile * H.T + H.col_s[S.nz + e] : H.col_d[S.nz + e];
-      if (pp >= nnz || hit[pp] || c != col[pp]) { bad += 1; continue; }
+      if (pp >= nnz || hit[pp] || c != col[pp]) { bad += 1; return; }
       hit[pp] = 1;
+    };
+    if (S.tile >= 0) {
+      for (int32_t pos = 0; pos < nr; ++pos)
+        for (int32_t j = 0; j < rp[pos + 1] - rp[pos]; ++j)
+          for (int k = 0; k < 4; ++k) visit(4 * quad_slot(H.blkb, S, rp, pos, j) + k);
+    } else {
+      for (int64_t e = 0; e < rp[nr]; ++e) visit(e);
     }
   }
   for (int64_t q = 0; q < nnz; ++q) bad += hit[q] == 0;

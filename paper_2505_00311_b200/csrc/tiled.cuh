@@ -38,6 +38,7 @@ struct TSeg {
   int32_t V;         // lanes per row (1, 2, 4, 8, 16, 32)
   int64_t rp;        // offset of the segment's row pointers (nrows + 1 entries)
   int64_t nz;        // offset of the segment's entries in its pool (staged: in entries, = 4 * quads)
+  int64_t bb;        // staged, >= 0: sliced layout, offset of the segment's warp-block bases in blkb
 };
 struct TChunk {
   int64_t row0;
@@ -70,6 +71,7 @@ struct TiledMat {
   const double* val_d = nullptr;
   const int32_t* col_d = nullptr;
   const TBatch* batch = nullptr;
+  const int32_t* blkb = nullptr;      // sliced staged segments: first quad of every warp block
 };
 
 // Shared-memory loads with 32-bit shared addresses (the tile pointer would
@@ -442,6 +444,196 @@ __global__ void __launch_bounds__(kTThreads) k_tiled_tma(TiledMat M, const doubl
     for (int i = threadIdx.x; i < C.nrows * ELEM; i += blockDim.x) out[i] = acc[i];
     __syncthreads();
   }
+}
+
+// ------------------------------------------------------------------ sliced layout
+// Staged segments in the sliced layout (pdcs.cu slice_segments): the quads of
+// a warp block of 32/V consecutive segment rows are stored time step by time
+// step, lane by lane, so the quad lane l of the block reads at step t sits at
+// blkb[block] + l + 32 t.  A warp-wide LDG.256 then reads 1 KB of consecutive
+// values (8 full lines) and the column-id load 256 consecutive bytes.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Asynchronous copy (LDGSTS) of vector tile `tile` into shared buffer dst.
+template <int ELEM>
+__device__ __forceinline__ void tile_fetch_async(const TiledMat& M, const double* __restrict__ x, int32_t tile,
+                                                 double* dst) {
+  const int64_t base = (int64_t)tile * M.T;
+  const int64_t len = (M.nvec - base < M.T ? M.nvec - base : M.T) * ELEM;   // doubles
+  const double* src = x + base * ELEM;
+  const uint32_t d = smem_u32(dst);
+  for (int64_t i = threadIdx.x; i < len / 2; i += blockDim.x) cp_async16(d + 16u * (uint32_t)i, src + 2 * i);
+  if ((len & 1) && threadIdx.x == 0) dst[len - 1] = __ldg(src + len - 1);
+}
+
+#ifndef PDCS_SL_U2
+#define PDCS_SL_U2 4                  // quads in flight per lane, pair gather (B200 sweep: 2 -> 4 is -2% / -21%)
+#endif
+#ifndef PDCS_SL_U1
+#define PDCS_SL_U1 4                  // quads in flight per lane, single gather
+#endif
+// One staged segment, warp per block of 32/V rows.  Blocks go to warps in
+// snake order (rows are sorted longest first, so this balances the warps);
+// the next block's row lengths, base and output rows are loaded before the
+// current block's data loop, so the only exposed latency is the data's.
+template <int V, int ELEM>
+__device__ __forceinline__ void sliced_blocks(const TiledMat& M, const TSeg& S, int32_t nrows, uint32_t xs_s,
+                                              double* acc) {
+  constexpr int RPW = 32 / V;
+  constexpr int U = ELEM == 2 ? PDCS_SL_U2 : PDCS_SL_U1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int a = lane / V, l = lane % V;
+  const int32_t* rp = M.rowptr + S.rp;
+  const uint16_t* srow = M.srow + S.rp;
+  const int32_t* bb = M.blkb + S.bb;
+  const double* val = M.val_s + S.nz;
+  const uint16_t* col = M.col_s + S.nz;
+  const int nblk = (nrows + RPW - 1) / RPW;
+  auto blk_of = [&](int i) { return i * nw + ((i & 1) ? nw - 1 - warp : warp); };
+  auto meta = [&](int blk, int32_t& nq, int32_t& base, int& rr) {
+    nq = 0; base = 0; rr = -1;
+    if (blk < nblk) {
+      const int pos = blk * RPW + a;
+      base = __ldg(bb + blk);
+      if (pos < nrows) { nq = __ldg(rp + pos + 1) - __ldg(rp + pos); rr = __ldg(srow + pos); }
+    }
+  };
+  int i = 0, blk = blk_of(0);
+  int32_t nq, base;
+  int rr;
+  meta(blk, nq, base, rr);
+  while (blk < nblk) {
+    const int blk2 = blk_of(i + 1);
+    int32_t nq2, base2;
+    int rr2;
+    meta(blk2, nq2, base2, rr2);
+    const int32_t nt = nq > l ? (nq - l + V - 1) / V : 0;     // quads of this lane
+    const int32_t tmax = (int32_t)__reduce_max_sync(0xffffffffu, (unsigned)nt);
+    const double* vp = val + 4 * ((int64_t)base + lane);
+    const uint16_t* cp = col + 4 * ((int64_t)base + lane);
+    double s1 = 0.0, s2 = 0.0;
+    for (int32_t t0 = 0; t0 < tmax; t0 += U) {
+      double q[U][4];
+      uint2 c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (t0 + u < nt) {
+          const double4 v = ld_stream4(vp + 128 * (int64_t)(t0 + u));
+          c[u] = ld_stream_u2(cp + 128 * (int64_t)(t0 + u));
+          q[u][0] = v.x; q[u][1] = v.y; q[u][2] = v.z; q[u][3] = v.w;
+        } else {
+          c[u] = make_uint2(0u, 0u);
+          q[u][0] = q[u][1] = q[u][2] = q[u][3] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t0 + u < nt) {
+          const uint32_t cc[4] = {c[u].x & 0xffffu, c[u].x >> 16, c[u].y & 0xffffu, c[u].y >> 16};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (ELEM == 2) {
+              const double2 v = lds_v2(xs_s + cc[k] * 16u);
+              s1 += q[u][k] * v.x;
+              s2 += q[u][k] * v.y;
+            } else {
+              s1 += q[u][k] * lds_f64(xs_s + cc[k] * 8u);
+            }
+          }
+        }
+    }
+    if (V > 1) {
+#pragma unroll
+      for (int o = V / 2; o >= 1; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o, V);
+        if (ELEM == 2) s2 += __shfl_xor_sync(0xffffffffu, s2, o, V);
+      }
+    }
+    if (l == 0 && rr >= 0) {
+      acc[rr * ELEM] += s1;
+      if (ELEM == 2) acc[rr * ELEM + 1] += s2;
+    }
+    blk = blk2; nq = nq2; base = base2; rr = rr2;
+    ++i;
+  }
+}
+
+__device__ __forceinline__ int32_t next_staged(const TiledMat& M, int32_t s, int32_t e) {
+  for (; s < e; ++s)
+    if (M.seg[s].tile >= 0) return s;
+  return -1;
+}
+
+// Partial products, sliced layout.  The vector tile of the next staged segment
+// (in this work item, else in the CTA's next item) is copied asynchronously
+// into the second shared buffer while the current segment runs.
+#ifndef PDCS_TS_MINB1
+#define PDCS_TS_MINB1 2               // k_tiled_sliced<1>: 64 registers (40 spills)
+#endif
+template <int ELEM>
+__global__ void __launch_bounds__(kTThreads, ELEM == 1 ? PDCS_TS_MINB1 : PDCS_TP_MINB)
+    k_tiled_sliced(TiledMat M, const double* __restrict__ x, double* __restrict__ scratch, const Ctl* ctl, int guard) {
+  if (guard >= 1 && ctl->status != 4) return;
+  if (guard == 2 && !ctl->accepted) return;
+  extern __shared__ __align__(128) double smem[];
+  const int64_t TE = (int64_t)M.T * ELEM;
+  double* tiles = smem;                              // 2 buffers of T * ELEM doubles
+  double* acc = smem + 2 * TE;                       // kTRows * ELEM doubles
+  int buf = 0;                                       // buffer of the tile in flight
+  int32_t inflight = -1;                             // segment whose tile is in flight
+  if (blockIdx.x < M.nwork) {
+    const TWork W = M.work[blockIdx.x];
+    inflight = next_staged(M, W.s0, W.s1);
+    if (inflight >= 0) tile_fetch_async<ELEM>(M, x, M.seg[inflight].tile, tiles + buf * TE);
+  }
+  for (int64_t w = blockIdx.x; w < M.nwork; w += gridDim.x) {
+    const TWork W = M.work[w];
+    const TChunk C = M.chunk[W.chunk];
+    for (int i = threadIdx.x; i < C.nrows * ELEM; i += blockDim.x) acc[i] = 0.0;
+    __syncthreads();
+    for (int s = W.s0; s < W.s1; ++s) {
+      const TSeg S = M.seg[s];
+      if (S.tile >= 0) {
+        if (s != inflight) tile_fetch_async<ELEM>(M, x, S.tile, tiles + buf * TE);
+        cp_async_wait_all();
+        __syncthreads();                               // tile visible; the other buffer is free
+        const uint32_t xs_s = smem_u32(tiles + buf * TE);
+        buf ^= 1;
+        inflight = next_staged(M, s + 1, W.s1);
+        if (inflight < 0 && w + gridDim.x < M.nwork) {
+          const TWork W2 = M.work[w + gridDim.x];
+          inflight = next_staged(M, W2.s0, W2.s1);
+        }
+        if (inflight >= 0) tile_fetch_async<ELEM>(M, x, M.seg[inflight].tile, tiles + buf * TE);
+        switch (S.V) {
+          case 1: sliced_blocks<1, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          case 2: sliced_blocks<2, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          case 4: sliced_blocks<4, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          case 8: sliced_blocks<8, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          case 16: sliced_blocks<16, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          default: sliced_blocks<32, ELEM>(M, S, C.nrows, xs_s, acc); break;
+        }
+      } else {
+        switch (S.V) {
+          case 1: seg_rows<1, ELEM>(M, S, C, x, 0u, false, acc); break;
+          case 2: seg_rows<2, ELEM>(M, S, C, x, 0u, false, acc); break;
+          case 4: seg_rows<4, ELEM>(M, S, C, x, 0u, false, acc); break;
+          case 8: seg_rows<8, ELEM>(M, S, C, x, 0u, false, acc); break;
+          case 16: seg_rows<16, ELEM>(M, S, C, x, 0u, false, acc); break;
+          default: seg_rows<32, ELEM>(M, S, C, x, 0u, false, acc); break;
+        }
+      }
+      __syncthreads();                                 // acc rows are shared across segments
+    }
+    double* out = scratch + C.scratch + (int64_t)W.group * C.nrows * ELEM;
+    for (int i = threadIdx.x; i < C.nrows * ELEM; i += blockDim.x) out[i] = acc[i];
+    __syncthreads();
+  }
+  cp_async_wait_all();
 }
 
 // Sum the partials of every row (fixed order) and run the fused epilogue.

@@ -268,6 +268,13 @@ struct EpiStore2 {
   __device__ void row(int64_t i, double dot, double, Acc<NA>&) { out[i] = dot; }
 };
 
+// (a_j, 0) pairs for a single-vector product through the pair-gather tiled K.
+__global__ void __launch_bounds__(kThreads) k_pair_stage(int64_t n, const double* __restrict__ a,
+                                                         double2* __restrict__ xx) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    xx[j] = make_double2(a[j], 0.0);
+}
+
 // y-side ReflectedHalpern + average: y+, ysum.
 __global__ void __launch_bounds__(kThreads) k_halpern_y(int64_t m, const double* __restrict__ yh,
                                                         const double* __restrict__ y0,

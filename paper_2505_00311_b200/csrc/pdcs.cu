@@ -708,6 +708,27 @@ struct pdcs_ctx {
     spmv("spmv_store", A, xin, nullptr, e, nullptr, 0);
   }
 
+  // Product sweeps of the Eq. 9 check: the tiled copies when the autotune kept
+  // them (K x through the pair-gather format with (x_j, 0) staged into xx,
+  // which the next trial's primal kernel rewrites anyway), else CSR.
+  void spmv_check_KT(const double* yin, double* out) {
+    if (!tKT.on) { spmv_store(KT, yin, out); return; }
+    tiled_partial("tiled_check_partial", tKT, 1, yin, 0);
+    EpiStore e{out};
+    launch("check_combine", [&] {
+      k_tiled_combine<EpiStore, 1><<<tKT.g_combine, kThreads, 0, st>>>(tKT.M, tKT.scratch.p, e, ctl, nullptr, 0);
+    });
+  }
+  void spmv_check_K(const double* xin, double* out) {
+    if (!tK.on) { spmv_store(K, xin, out); return; }
+    launch("pair_stage", [&] { k_pair_stage<<<g_pe, kThreads, 0, st>>>(n, xin, xx.p); });
+    tiled_partial("tiled_check_partial", tK, 2, reinterpret_cast<const double*>(xx.p), 0);
+    EpiStore2 e{out};
+    launch("check_combine", [&] {
+      k_tiled_combine<EpiStore2, 2><<<tK.g_combine, kThreads, 0, st>>>(tK.M, tK.scratch.p, e, ctl, nullptr, 0);
+    });
+  }
+
   void read_ctl() {
     CK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -853,7 +874,7 @@ struct pdcs_ctx {
     const bool van = prm.vanilla_pdhg != 0;
     KktCand c0{xh.p, yh.p, kxh.p, ktyh.p, res0.p, lam0.p};
     KktCand c1{xa.p, ya.p, kxa.p, ktya.p, res1.p, lam1.p};
-    spmv_store(KT, yh.p, ktyh.p);   // K^T y^ of the current candidate (K x^ kept by the K pass)
+    spmv_check_KT(yh.p, ktyh.p);    // K^T y^ of the current candidate (K x^ kept by the K pass)
     allreduce(ktyh.p, n, ncclSum);
     if (!van) {
       launch("avg_elem", [&] { k_avg_elem<<<g_pe, kThreads, 0, st>>>(n, ek.p, xsum.p, lt.p, ut.p, xa.p, ctl); });
@@ -864,8 +885,8 @@ struct pdcs_ctx {
       BlockArgs B = bargs(false, BOP_AVG_DUAL);
       B.sum = ysum.p; B.out = ya.p;
       run_blocks(false, B, false, 0);
-      spmv_store(K, xa.p, kxa.p);
-      spmv_store(KT, ya.p, ktya.p);
+      spmv_check_K(xa.p, kxa.p);
+      spmv_check_KT(ya.p, ktya.p);
       allreduce(ktya.p, n, ncclSum);
     }
     kkt_launch(c0, c1, van ? 1 : 2, 1);

@@ -654,8 +654,24 @@ __global__ void __launch_bounds__(kThreads) k_tiled_combine(TiledMat M, const do
     const int r = slab * blockDim.x + threadIdx.x;
     if (r < C.nrows) {
       const double* src = scratch + C.scratch;
+      // groups summed in order; loads batched 8 deep (chunks of long rows have
+      // ~100 groups, a load-add chain would serialise their latencies)
       double s1 = 0.0, s2 = 0.0;
-      for (int g = 0; g < C.ngroups; ++g) {
+      int g = 0;
+      for (; g + 8 <= C.ngroups; g += 8) {
+        double u1[8], u2[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          u1[k] = src[((int64_t)(g + k) * C.nrows + r) * ELEM];
+          if (ELEM == 2) u2[k] = src[((int64_t)(g + k) * C.nrows + r) * ELEM + 1];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          s1 += u1[k];
+          if (ELEM == 2) s2 += u2[k];
+        }
+      }
+      for (; g < C.ngroups; ++g) {
         s1 += src[((int64_t)g * C.nrows + r) * ELEM];
         if (ELEM == 2) s2 += src[((int64_t)g * C.nrows + r) * ELEM + 1];
       }

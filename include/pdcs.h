@@ -234,6 +234,37 @@ void pdcs_destroy(pdcs_ctx *ctx);
 int pdcs_tiled_layout_stats(const int64_t *row_ptr, const int32_t *col, int64_t rows, int64_t nvec, int elem,
                             double *out, int cap);
 
+/* ---- Standalone multi-cone projection (§4 "GPU
+ * implementation", Table "Projection strategies", Figs. 3-4; Thm 1
+ * PAPER.md:651-661 and Thm 4 PAPER.md:1272-1311 for the rescaled cones).
+ *
+ * A plan holds the block descriptors of one cone product K = K_1 x ... x K_nb,
+ * block b of kind kinds[b] (PDCS_CONE_SOC dim >= 2, PDCS_CONE_RSOC dim >= 3,
+ * PDCS_CONE_EXP / PDCS_CONE_DUAL_EXP dim 3) covering dims[b] consecutive
+ * coordinates, in order, of a vector of length sum(dims).  team selects the
+ * parallel strategy for the SOC/RSOC blocks: -1 the solver's size classes
+ * (thread <= 32, warp <= 512, CTA <= 4096, 8-CTA cluster <= 131072, whole
+ * grid beyond); 0..4 forces thread / warp / CTA / cluster / grid for every one
+ * of them (the paper's thread-, block- and grid-wise strategies).  Exp blocks
+ * are always one thread per cone.  kinds/dims are host arrays,
+ * copied; the plan owns device memory on `device` until pdcs_proj_destroy.
+ * Errors: PDCS_ERR_ARG (null lists, bad team/device), PDCS_ERR_CONE (bad
+ * kind/dim), PDCS_ERR_CUDA (no sm_100 device).  The message is returned by
+ * pdcs_last_error(NULL). */
+typedef struct pdcs_proj pdcs_proj;
+pdcs_status pdcs_proj_create(pdcs_proj **out, int device, const int32_t *kinds, const int64_t *dims,
+                             int64_t nblocks, int team);
+/* out = P_{diag(D) K}(v), blockwise (the rescaled cone D K = {D w : w in K}).
+ * v, out: device arrays of sum(dims) doubles (may not alias); D: device array
+ * of positive multipliers of the same length, or NULL for K itself (unit
+ * scaling).  RSOC blocks need D[0] == D[1] (reading A21).  Enqueued on
+ * `stream` (a cudaStream_t, NULL = legacy default); does not synchronise. */
+pdcs_status pdcs_proj_run(pdcs_proj *plan, const double *D, const double *v, double *out, void *stream);
+/* Blocks and grid size per team (thread, warp, CTA, cluster, grid) into
+ * counts[5] / grids[5] (either may be NULL).  Returns 5. */
+int pdcs_proj_info(const pdcs_proj *plan, int64_t *counts, int64_t *grids);
+void pdcs_proj_destroy(pdcs_proj *plan);
+
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 broadcasts it). */
 pdcs_status pdcs_nccl_unique_id(void *out128);
 

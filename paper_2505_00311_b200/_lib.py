@@ -93,6 +93,11 @@ def lib():
         L.pdcs_tiled_layout_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                               C.c_void_p, C.c_int]
         L.pdcs_tiled_layout_stats.restype = C.c_int
+        L.pdcs_proj_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, P_I32, P_I64, C.c_int64, C.c_int]
+        L.pdcs_proj_run.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.pdcs_proj_info.argtypes = [C.c_void_p, P_I64, P_I64]
+        L.pdcs_proj_info.restype = C.c_int
+        L.pdcs_proj_destroy.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -101,7 +106,8 @@ EXPORTED = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterat
             "pdcs_solve", "pdcs_get_iterate", "pdcs_set_iterate", "pdcs_get_scaling",
             "pdcs_kernel_times", "pdcs_enable_timing", "pdcs_launch_count", "pdcs_last_error",
             "pdcs_destroy", "pdcs_nccl_unique_id", "pdcs_get_scalars", "pdcs_get_state",
-            "pdcs_set_state", "pdcs_tiled_layout_stats"]
+            "pdcs_set_state", "pdcs_tiled_layout_stats", "pdcs_proj_create", "pdcs_proj_run",
+            "pdcs_proj_info", "pdcs_proj_destroy"]
 
 STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e_prev", "best_e", "k",
               "total", "trials", "restarts"]
@@ -260,3 +266,35 @@ def pdcs_tiled_layout_stats(row_ptr, col, nvec: int, elem: int) -> dict:
     if k == 0:
         raise PdcsError(-1, "pdcs_tiled_layout_stats: bad arguments")
     return dict(zip(TILED_STAT_KEYS[:k], out[:k]))
+
+
+# ---------------------------------------------------------------- standalone projections
+TEAMS = {"auto": -1, "thread": 0, "warp": 1, "cta": 2, "cluster": 3, "grid": 4}
+
+
+def pdcs_proj_create(kinds, dims, team=-1, device=0):
+    """Plan of a multi-cone projection (include/pdcs.h): kinds/dims host arrays."""
+    k = np.ascontiguousarray(kinds, np.int32)
+    d = np.ascontiguousarray(dims, np.int64)
+    h = C.c_void_p()
+    team = TEAMS[team] if isinstance(team, str) else int(team)
+    _check(lib().pdcs_proj_create(C.byref(h), int(device), k.ctypes.data_as(P_I32), d.ctypes.data_as(P_I64),
+                                  k.shape[0], team))
+    return h
+
+
+def pdcs_proj_run(plan, D, v, out, stream=None):
+    """out = P_{diag(D) K}(v); D, v, out device tensors / pointers (D None: unit)."""
+    st = None if stream is None else C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    _check(lib().pdcs_proj_run(plan, None if D is None else _ptr(D), _ptr(v), _ptr(out), st))
+
+
+def pdcs_proj_info(plan):
+    counts = np.zeros(5, np.int64)
+    grids = np.zeros(5, np.int64)
+    lib().pdcs_proj_info(plan, counts.ctypes.data_as(P_I64), grids.ctypes.data_as(P_I64))
+    return {"counts": counts.tolist(), "grids": grids.tolist()}
+
+
+def pdcs_proj_destroy(plan):
+    lib().pdcs_proj_destroy(plan)

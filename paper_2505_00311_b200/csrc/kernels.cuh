@@ -99,10 +99,13 @@ struct DstKktCols {       // distance of lambda_2 to K_p^*, Eq. 9 err_d
 };
 
 // Project one block with a team.  exp_dual: EXP means K_exp^* (and DEXP K_exp).
-template <class Team, class Src, class Dst>
+// HAS_EXP = false for the multi-thread teams (exp blocks are always in the
+// thread class): the exp root finder is then not compiled into their kernels,
+// whose register allocation would otherwise be set by it.
+template <bool HAS_EXP, class Team, class Src, class Dst>
 __device__ __forceinline__ void project_block(Team& tm, const Block& b, bool exp_dual, bool unit,
                                               const Src& src, Dst& dst) {
-  if (b.kind == C_SOC || b.kind == C_RSOC) {
+  if (!HAS_EXP || b.kind == C_SOC || b.kind == C_RSOC) {
     SrcAdapt<Src> s{src};
     soc_team(tm, (int64_t)b.dim, b.kind == C_RSOC, unit, s, dst);
   } else {  // 3-d exponential blocks: one thread
@@ -126,7 +129,8 @@ enum BlockOp : int32_t {
   BOP_AVG_PRIMAL = 2,     // xa = P(xsum/W)
   BOP_AVG_DUAL = 3,       // ya = P(ysum/W)
   BOP_KKT_ROWS = 4,       // dist(res, C_b), unit scaling
-  BOP_KKT_COLS = 5        // dist(lam_2, K_p^*), unit scaling
+  BOP_KKT_COLS = 5,       // dist(lam_2, K_p^*), unit scaling
+  BOP_PROJECT = 6         // standalone: out = P_{D K}(v) (pdcs_proj_run; D == nullptr: unit)
 };
 
 struct BlockArgs {
@@ -148,53 +152,62 @@ struct BlockArgs {
   int64_t slot0;
 };
 
-template <class Team>
+// OP is the kernel's template constant (BlockOp), so each kernel holds one path.
+template <bool HAS_EXP, int OP, class Team>
 __device__ __forceinline__ void run_block(Team& tm, const BlockArgs& A, const Ctl* ctl, const Block& b,
                                           Acc<kAcc>& acc, double* kv) {
-  switch (A.op) {
+  switch (OP) {
     case BOP_TRIAL_PRIMAL: {
       SrcPrimalTrial s{A.x, A.c, A.kty, A.D, ctl->tau, b.off};
       DstTrialPrimal d{A.xh, A.xx, A.x, b.off, &acc};
-      project_block(tm, b, false, false, s, d);
+      project_block<HAS_EXP>(tm, b, false, false, s, d);
       break;
     }
     case BOP_TRIAL_DUAL: {
       SrcStored s{A.yh, A.D, b.off};
       DstTrialDual d{A.yh, A.y, A.kxd, b.off, &acc};
-      project_block(tm, b, true, false, s, d);
+      project_block<HAS_EXP>(tm, b, true, false, s, d);
       break;
     }
     case BOP_AVG_PRIMAL:
     case BOP_AVG_DUAL: {
       SrcAverage s{A.sum, A.D, ctl->Wsum, b.off};
       DstStore d{A.out, b.off};
-      project_block(tm, b, A.op == BOP_AVG_DUAL, false, s, d);
+      project_block<HAS_EXP>(tm, b, OP == BOP_AVG_DUAL, false, s, d);
       break;
     }
     case BOP_KKT_ROWS: {
       SrcStored s{A.scratch, nullptr, b.off};
       DstKktRows d{A.scratch, b.off, kv + 0, kv + 2};
-      project_block(tm, b, false, true, s, d);
+      project_block<HAS_EXP>(tm, b, false, true, s, d);
       break;
     }
     case BOP_KKT_COLS: {
       SrcStored s{A.scratch, nullptr, b.off};
       DstKktCols d{A.scratch, b.off, kv + 5};
-      project_block(tm, b, true, true, s, d);
+      project_block<HAS_EXP>(tm, b, true, true, s, d);
+      break;
+    }
+    case BOP_PROJECT: {
+      SrcStored s{A.scratch, A.D, b.off};
+      DstStore d{A.out, b.off};
+      project_block<HAS_EXP>(tm, b, false, A.D == nullptr, s, d);
       break;
     }
   }
 }
 
+template <int OP>
 __device__ __forceinline__ bool block_op_active(const BlockArgs& A, const Ctl* ctl) {
-  if (A.op == BOP_TRIAL_PRIMAL || A.op == BOP_TRIAL_DUAL) return ctl->status == 4;  // running
+  if (OP == BOP_TRIAL_PRIMAL || OP == BOP_TRIAL_DUAL) return ctl->status == 4;  // running
   return true;
 }
 
+template <int OP>
 __device__ __forceinline__ void finish_block_partials(const BlockArgs& A, Acc<kAcc>& acc, double* kv) {
-  if (A.op == BOP_TRIAL_PRIMAL || A.op == BOP_TRIAL_DUAL) {
+  if (OP == BOP_TRIAL_PRIMAL || OP == BOP_TRIAL_DUAL) {
     cta_write_partials<kAcc>(acc, A.part, A.slot0 + blockIdx.x);
-  } else if (A.op == BOP_KKT_ROWS || A.op == BOP_KKT_COLS) {
+  } else if (OP == BOP_KKT_ROWS || OP == BOP_KKT_COLS) {
     // max-reduce kv[0..9] over the CTA; write into candidate half of the slot
     __shared__ double red[10][kThreads / 32];
     for (int i = 0; i < 10; ++i) {
@@ -215,22 +228,24 @@ __device__ __forceinline__ void finish_block_partials(const BlockArgs& A, Acc<kA
 }
 
 // One block per thread (exp / dual exp / SOC of dim <= 32).
+template <int OP>
 __global__ void __launch_bounds__(kThreads) k_blocks_thread(BlockArgs A, const Ctl* ctl) {
-  if (!block_op_active(A, ctl)) return;
+  if (!block_op_active<OP>(A, ctl)) return;
   Acc<kAcc> acc; acc.zero();
   double kv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   ThreadTeam tm;
   for (int64_t bi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; bi < A.nblocks;
        bi += (int64_t)gridDim.x * blockDim.x) {
     const Block b = A.blocks[bi];
-    run_block(tm, A, ctl, b, acc, kv);
+    run_block<true, OP>(tm, A, ctl, b, acc, kv);
   }
-  finish_block_partials(A, acc, kv);
+  finish_block_partials<OP>(A, acc, kv);
 }
 
 // One block per warp (SOC/RSOC of dim 33..512).
+template <int OP>
 __global__ void __launch_bounds__(kThreads) k_blocks_warp(BlockArgs A, const Ctl* ctl) {
-  if (!block_op_active(A, ctl)) return;
+  if (!block_op_active<OP>(A, ctl)) return;
   Acc<kAcc> acc; acc.zero();
   double kv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   WarpTeam tm{(int)(threadIdx.x & 31)};
@@ -238,30 +253,32 @@ __global__ void __launch_bounds__(kThreads) k_blocks_warp(BlockArgs A, const Ctl
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t bi = wid; bi < A.nblocks; bi += nw) {
     const Block b = A.blocks[bi];
-    run_block(tm, A, ctl, b, acc, kv);
+    run_block<false, OP>(tm, A, ctl, b, acc, kv);
   }
-  finish_block_partials(A, acc, kv);
+  finish_block_partials<OP>(A, acc, kv);
 }
 
 // One block per CTA (SOC/RSOC of dim 513..4096).
+template <int OP>
 __global__ void __launch_bounds__(kThreads) k_blocks_cta(BlockArgs A, const Ctl* ctl) {
-  if (!block_op_active(A, ctl)) return;
+  if (!block_op_active<OP>(A, ctl)) return;
   __shared__ double sm[2 * (kThreads / 32) + 2];
   Acc<kAcc> acc; acc.zero();
   double kv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   CtaTeam tm{sm};
   for (int64_t bi = blockIdx.x; bi < A.nblocks; bi += gridDim.x) {
     const Block b = A.blocks[bi];
-    run_block(tm, A, ctl, b, acc, kv);
+    run_block<false, OP>(tm, A, ctl, b, acc, kv);
   }
-  finish_block_partials(A, acc, kv);
+  finish_block_partials<OP>(A, acc, kv);
 }
 
 // One block per thread-block cluster of kClusterCtas CTAs (SOC/RSOC of dim
 // 4097..131072): per-pass reductions through distributed shared memory.
+template <int OP>
 __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
     k_blocks_cluster(BlockArgs A, const Ctl* ctl) {
-  if (!block_op_active(A, ctl)) return;
+  if (!block_op_active<OP>(A, ctl)) return;
   __shared__ double sm[2 * (kThreads / 32) + 2];
   Acc<kAcc> acc; acc.zero();
   double kv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -269,23 +286,65 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
   const int64_t cid = blockIdx.x / kClusterCtas, ncl = gridDim.x / kClusterCtas;
   for (int64_t bi = cid; bi < A.nblocks; bi += ncl) {
     const Block b = A.blocks[bi];
-    run_block(tm, A, ctl, b, acc, kv);
+    run_block<false, OP>(tm, A, ctl, b, acc, kv);
   }
-  finish_block_partials(A, acc, kv);
+  finish_block_partials<OP>(A, acc, kv);
 }
 
 // All CTAs on one block at a time (giant SOC/RSOC; cooperative launch).
+template <int OP>
 __global__ void __launch_bounds__(kThreads) k_blocks_grid(BlockArgs A, const Ctl* ctl, double* gbuf) {
-  if (!block_op_active(A, ctl)) return;
+  if (!block_op_active<OP>(A, ctl)) return;
   __shared__ double sm[2 * (kThreads / 32) + 2];
   Acc<kAcc> acc; acc.zero();
   double kv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   GridTeam tm{sm, gbuf, 0};
   for (int64_t bi = 0; bi < A.nblocks; ++bi) {
     const Block b = A.blocks[bi];
-    run_block(tm, A, ctl, b, acc, kv);
+    run_block<false, OP>(tm, A, ctl, b, acc, kv);
   }
-  finish_block_partials(A, acc, kv);
+  finish_block_partials<OP>(A, acc, kv);
+}
+
+// Host side: launch the kernel of size class c (thread, warp, CTA, cluster,
+// grid) for block operation op; each (class, op) pair is its own kernel.
+template <int OP>
+inline cudaError_t launch_blocks_op(int c, int g, BlockArgs B, const Ctl* ctl, double* gbuf, cudaStream_t st) {
+  switch (c) {
+    case 0: k_blocks_thread<OP><<<g, kThreadsSmall, 0, st>>>(B, ctl); return cudaGetLastError();
+    case 1: k_blocks_warp<OP><<<g, kThreads, 0, st>>>(B, ctl); return cudaGetLastError();
+    case 2: k_blocks_cta<OP><<<g, kThreads, 0, st>>>(B, ctl); return cudaGetLastError();
+    case 3: k_blocks_cluster<OP><<<g, kThreads, 0, st>>>(B, ctl); return cudaGetLastError();
+    default: {
+      void* args[] = {(void*)&B, (void*)&ctl, (void*)&gbuf};
+      return cudaLaunchCooperativeKernel((void*)k_blocks_grid<OP>, dim3(g), dim3(kThreads), args, 0, st);
+    }
+  }
+}
+inline cudaError_t launch_blocks(int c, int g, const BlockArgs& B, const Ctl* ctl, double* gbuf, cudaStream_t st) {
+  switch (B.op) {
+    case BOP_TRIAL_PRIMAL: return launch_blocks_op<BOP_TRIAL_PRIMAL>(c, g, B, ctl, gbuf, st);
+    case BOP_TRIAL_DUAL: return launch_blocks_op<BOP_TRIAL_DUAL>(c, g, B, ctl, gbuf, st);
+    case BOP_AVG_PRIMAL: return launch_blocks_op<BOP_AVG_PRIMAL>(c, g, B, ctl, gbuf, st);
+    case BOP_AVG_DUAL: return launch_blocks_op<BOP_AVG_DUAL>(c, g, B, ctl, gbuf, st);
+    case BOP_KKT_ROWS: return launch_blocks_op<BOP_KKT_ROWS>(c, g, B, ctl, gbuf, st);
+    case BOP_KKT_COLS: return launch_blocks_op<BOP_KKT_COLS>(c, g, B, ctl, gbuf, st);
+    default: return launch_blocks_op<BOP_PROJECT>(c, g, B, ctl, gbuf, st);
+  }
+}
+// Co-resident CTAs per SM of the grid-team kernel (cooperative launch bound),
+// the minimum over its instantiations.
+inline cudaError_t grid_team_occupancy(int* nb) {
+  int m = 1 << 20, v = 0;
+  cudaError_t e;
+#define PDCS_OCC(OPV) \
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_blocks_grid<OPV>, kThreads, 0)) != cudaSuccess) return e; \
+  m = v < m ? v : m;
+  PDCS_OCC(BOP_TRIAL_PRIMAL) PDCS_OCC(BOP_TRIAL_DUAL) PDCS_OCC(BOP_AVG_PRIMAL) PDCS_OCC(BOP_AVG_DUAL)
+  PDCS_OCC(BOP_KKT_ROWS) PDCS_OCC(BOP_KKT_COLS) PDCS_OCC(BOP_PROJECT)
+#undef PDCS_OCC
+  *nb = m;
+  return cudaSuccess;
 }
 
 }  // namespace pdcs

@@ -553,6 +553,36 @@ void validate_csr(const int64_t* ptr, const int32_t* col, const double* val, int
   fail(PDCS_ERR_NONFINITE, "non-finite matrix entry in row " + row);
 }
 
+// Size class of each cone block: 0 thread, 1 warp, 2 CTA,
+// 3 cluster, 4 grid.  Exp blocks and SOC/RSOC of dim <= 32 take one thread.
+// The warp class covers dims up to 512, or up to 16384 when it then holds
+// enough blocks to give every SM 32 warps; the CTA class up to 4096, or up to
+// 262144 when it holds >= 2 blocks per SM; the cluster class the rest up to
+// 131072; the grid team beyond.  (Measured: profiles/r1_proj_v2.json, the
+// unit-scaling sweep of PAPER.md:719-742 Fig. 3 with every team forced.)
+struct ClassPolicy {
+  int64_t t_warp = 512, t_cta = 4096;
+  int of(const Block& b) const {
+    if (b.kind == C_EXP || b.kind == C_DEXP || b.dim <= 32) return 0;
+    if (b.dim <= t_warp) return 1;
+    if (b.dim <= t_cta) return 2;
+    return b.dim <= 131072 ? 3 : 4;
+  }
+};
+ClassPolicy class_policy(const std::vector<Block>& v, int sms) {
+  ClassPolicy P;
+  int64_t n_warp = 0;
+  for (const Block& b : v)
+    if ((b.kind == C_SOC || b.kind == C_RSOC) && b.dim > 32 && b.dim <= 16384) ++n_warp;
+  if (n_warp >= 32 * (int64_t)sms) P.t_warp = 16384;
+  int64_t n_cta = 0;
+  for (const Block& b : v)
+    if ((b.kind == C_SOC || b.kind == C_RSOC) && b.dim > P.t_warp && b.dim <= 262144) ++n_cta;
+  if (n_cta >= 2 * (int64_t)sms) P.t_cta = std::max<int64_t>(P.t_warp, 262144);
+  else P.t_cta = std::max<int64_t>(P.t_warp, 4096);
+  return P;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -765,21 +795,9 @@ struct pdcs_ctx {
       B.cand = cand;
       B.part = kkt ? kpart.p : tpart.p;
       B.slot0 = kkt ? cl[c].kslot[cand] : cl[c].slot;
-      const int g = cl[c].grid;
-      if (c == 0) launch("blocks_thread", [&] { k_blocks_thread<<<g, kThreadsSmall, 0, st>>>(B, ctl); });
-      else if (c == 1) launch("blocks_warp", [&] { k_blocks_warp<<<g, kThreads, 0, st>>>(B, ctl); });
-      else if (c == 2) {
-        launch("blocks_cta", [&] { k_blocks_cta<<<g, kThreads, 0, st>>>(B, ctl); });
-      } else if (c == 3) {
-        launch("blocks_cluster", [&] { k_blocks_cluster<<<g, kThreads, 0, st>>>(B, ctl); });
-      } else {
-        double* gb = gbuf.p;
-        const Ctl* cp = ctl;
-        void* args[] = {(void*)&B, (void*)&cp, (void*)&gb};
-        launch("blocks_grid", [&] {
-          CK(cudaLaunchCooperativeKernel((void*)k_blocks_grid, dim3(g), dim3(kThreads), args, 0, st));
-        });
-      }
+      static const char* names[kNClass] = {"blocks_thread", "blocks_warp", "blocks_cta", "blocks_cluster",
+                                           "blocks_grid"};
+      launch(names[c], [&] { CK(launch_blocks(c, cl[c].grid, B, ctl, gbuf.p, st)); });
     }
   }
 
@@ -1519,15 +1537,13 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
       off += rdim[b];
     }
     if (off != mg) fail(PDCS_ERR_CONE, "row cone dims do not sum to m");
-    // Size classes: thread (exp, soc <= 32), warp (<= 512), cta (<= 4096),
-    // cluster of kClusterCtas CTAs (<= 131072), grid.  Within a class blocks are
+    // Size classes (class_policy): thread (exp, soc <= 32), warp, CTA, cluster
+    // of kClusterCtas CTAs (<= 131072), grid.  Within a class blocks are
     // ordered by (kind, dim) so that the lanes / warps of a launch run the same
     // code path with similar trip counts.
     auto classify = [&](std::vector<Block>& v, pdcs_ctx::BClass* cl) {
-      auto cls = [](const Block& b) {
-        return (b.kind == C_EXP || b.kind == C_DEXP || b.dim <= 32) ? 0 : b.dim <= 512 ? 1 : b.dim <= 4096 ? 2
-               : b.dim <= 131072 ? 3 : 4;
-      };
+      const ClassPolicy pol = class_policy(v, ctx->sms);
+      auto cls = [&](const Block& b) { return pol.of(b); };
       std::stable_sort(v.begin(), v.end(), [&](const Block& a, const Block& b) {
         const int ca = cls(a), cb = cls(b);
         if (ca != cb) return ca < cb;
@@ -1549,8 +1565,8 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
         else if (c == 3) cl[c].grid = kClusterCtas * (int)std::min<int64_t>(cnt, (int64_t)ctx->sms * 2 / kClusterCtas);
         else {
           int nb = 0;
-          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_blocks_grid, kThreads, 0));
-          cl[c].grid = std::max(1, std::min(nb, 2)) * ctx->sms;
+          CK(grid_team_occupancy(&nb));
+          cl[c].grid = std::max(1, std::min(nb, 4)) * ctx->sms;
         }
       }
     };
@@ -2113,6 +2129,123 @@ int pdcs_tiled_layout_stats(const int64_t* row_ptr, const int32_t* col, int64_t 
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }
+
+// ---------------------------------------------------------------- standalone projections
+// Multi-cone projection plan (Figs. 3-4):
+// the block descriptors of one cone product, grouped into the solver's size
+// classes (or all SOC/RSOC blocks forced into one team), uploaded once.
+struct pdcs_proj {
+  int device = 0, sms = 0;
+  DBuf<Block> blocks;
+  pdcs_ctx::BClass cls[kNClass];
+  DBuf<double> gbuf;
+  int64_t len = 0;
+  std::string err;
+};
+
+pdcs_status pdcs_proj_create(pdcs_proj** out, int device, const int32_t* kinds, const int64_t* dims,
+                             int64_t nblocks, int team) {
+  if (!out) return PDCS_ERR_ARG;
+  *out = nullptr;
+  pdcs_proj* P = new pdcs_proj();
+  pdcs_status s = guard(nullptr, [&] {
+    if (nblocks < 0 || (nblocks > 0 && (!kinds || !dims))) fail(PDCS_ERR_ARG, "bad block list");
+    if (team < -1 || team >= kNClass) fail(PDCS_ERR_ARG, "team must be -1 (auto) or 0..4");
+    std::vector<Block> v;
+    v.reserve((size_t)nblocks);
+    int64_t off = 0;
+    for (int64_t b = 0; b < nblocks; ++b) {
+      const int32_t k = kinds[b];
+      const int64_t d = dims[b];
+      const bool ok = ((k == C_SOC && d >= 2) || (k == C_RSOC && d >= 3) || ((k == C_EXP || k == C_DEXP) && d == 3)) &&
+                      d <= INT32_MAX;
+      if (!ok) fail(PDCS_ERR_CONE, "block " + std::to_string(b) + ": kind must be SOC (dim>=2), RSOC (>=3), EXP/DEXP (3)");
+      v.push_back(Block{off, k, (int32_t)d});
+      off += d;
+    }
+    P->len = off;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(PDCS_ERR_CUDA, "no CUDA device");
+    if (device < 0 || device >= ndev) fail(PDCS_ERR_ARG, "bad device ordinal");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) fail(PDCS_ERR_CUDA, "libpdcs is built for sm_100a");
+    P->device = device;
+    P->sms = prop.multiProcessorCount;
+    const ClassPolicy pol = class_policy(v, P->sms);
+    auto cls = [&](const Block& b) {
+      if (b.kind == C_EXP || b.kind == C_DEXP) return 0;
+      if (team >= 0) return team;
+      return pol.of(b);
+    };
+    std::stable_sort(v.begin(), v.end(), [&](const Block& a, const Block& b) {
+      const int ca = cls(a), cb = cls(b);
+      if (ca != cb) return ca < cb;
+      if (a.kind != b.kind) return a.kind < b.kind;
+      return a.dim < b.dim;
+    });
+    for (size_t i = 0; i < v.size(); ++i) {
+      const int c = cls(v[i]);
+      if (P->cls[c].count == 0) P->cls[c].begin = (int64_t)i;
+      P->cls[c].count++;
+    }
+    for (int c = 0; c < kNClass; ++c) {
+      const int64_t cnt = P->cls[c].count;
+      if (!cnt) continue;
+      if (c == 0) P->cls[c].grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + kThreadsSmall - 1) / kThreadsSmall, (int64_t)P->sms * 32));
+      else if (c == 1) P->cls[c].grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 7) / 8, (int64_t)P->sms * 8));
+      else if (c == 2) P->cls[c].grid = (int)std::min<int64_t>(cnt, (int64_t)P->sms * 4);
+      else if (c == 3) P->cls[c].grid = kClusterCtas * (int)std::min<int64_t>(cnt, (int64_t)P->sms * 2 / kClusterCtas);
+      else {
+        int nb = 0;
+        CK(grid_team_occupancy(&nb));
+        P->cls[c].grid = std::max(1, std::min(nb, 4)) * P->sms;
+      }
+    }
+    if (!v.empty()) {
+      P->blocks.alloc(v.size());
+      CK(cudaMemcpy(P->blocks.p, v.data(), v.size() * sizeof(Block), cudaMemcpyHostToDevice));
+    }
+    P->gbuf.alloc(4 * (size_t)P->sms * 8);
+  });
+  if (s != PDCS_OK) { delete P; return s; }
+  *out = P;
+  return PDCS_OK;
+}
+
+pdcs_status pdcs_proj_run(pdcs_proj* P, const double* D, const double* v, double* out, void* stream) {
+  if (!P || (P->len > 0 && (!v || !out))) return PDCS_ERR_ARG;
+  return guard(nullptr, [&] {
+    CK(cudaSetDevice(P->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    BlockArgs A{};
+    A.op = BOP_PROJECT;
+    A.D = D;
+    A.scratch = v;
+    A.out = out;
+    for (int c = 0; c < kNClass; ++c) {
+      if (P->cls[c].count == 0) continue;
+      BlockArgs B = A;
+      B.blocks = P->blocks.p + P->cls[c].begin;
+      B.nblocks = P->cls[c].count;
+      const int g = P->cls[c].grid;
+      CK(launch_blocks(c, g, B, nullptr, P->gbuf.p, st));
+      CK(cudaGetLastError());
+    }
+  });
+}
+
+int pdcs_proj_info(const pdcs_proj* P, int64_t* counts, int64_t* grids) {
+  if (!P) return 0;
+  for (int c = 0; c < kNClass; ++c) {
+    if (counts) counts[c] = P->cls[c].count;
+    if (grids) grids[c] = P->cls[c].grid;
+  }
+  return kNClass;
+}
+
+void pdcs_proj_destroy(pdcs_proj* P) { delete P; }
 
 pdcs_status pdcs_nccl_unique_id(void* out128) {
   if (!out128) return PDCS_ERR_ARG;

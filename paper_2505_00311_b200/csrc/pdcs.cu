@@ -216,55 +216,74 @@ void slice_segments(TiledHost& H, int32_t s0, int32_t s1, int32_t nr) {
 // has one, reading an address another lane already reads (a broadcast).
 void balance_banks(uint16_t* cols, int32_t* perm, const int32_t* rp, int32_t nr, int V, int elem) {
   const int G = elem == 2 ? 8 : 16;                           // bank groups = lanes per phase
-  std::vector<std::vector<std::pair<uint16_t, int32_t>>> bucket;
-  std::vector<int32_t> left, slots, rows;
-  std::vector<uint32_t> mask;
-  std::vector<std::vector<std::pair<int32_t, int32_t>>> lanes;
+  const int rpw = 32 / V;
+  // flat per-(row, group) buckets, filled in entry order and consumed from the
+  // back; the schedule of tiled_block_schedule is computed inline (lane a*V+l
+  // reads quad l + t V of block row a at step t); scratch reused across calls
+  thread_local std::vector<uint16_t> ncol, bcol;
+  thread_local std::vector<int32_t> nperm, bperm, bstart, bleft, left, slots;
+  thread_local std::vector<uint32_t> mask;
   const int64_t nslot = 4 * (int64_t)rp[nr];
-  std::vector<uint16_t> ncol(nslot, 0);
-  std::vector<int32_t> nperm(nslot, -1);
+  ncol.assign(nslot, 0);
+  nperm.assign(nslot, -1);
   const int nblk = tiled_blocks(nr, V);
   for (int blk = 0; blk < nblk; ++blk) {
-    tiled_block_schedule(rp, nr, V, blk, rows, lanes);
-    const int R = (int)rows.size();
-    bucket.assign((size_t)R * G, {});
+    const int32_t i0 = blk * rpw;
+    const int R = std::min<int32_t>(rpw, nr - i0);
+    bstart.assign((size_t)R * G + 1, 0);
     left.assign(R, 0);
     slots.assign(R, 0);
     mask.assign(R, 0);
     int rem[16] = {0};
-    size_t tmax = 0;
-    for (const auto& ln : lanes) tmax = std::max(tmax, ln.size());
+    int32_t tmax = 0;
     for (int a = 0; a < R; ++a) {
-      const int32_t q0 = rp[rows[a]], q1 = rp[rows[a] + 1];
+      const int32_t q0 = rp[i0 + a], q1 = rp[i0 + a + 1];
+      tmax = std::max(tmax, (q1 - q0 + V - 1) / V);
       slots[a] = 4 * (q1 - q0);
       for (int64_t e = 4 * (int64_t)q0; e < 4 * (int64_t)q1; ++e)
         if (perm[e] >= 0) {
           const int g = cols[e] % G;
-          bucket[(size_t)a * G + g].push_back({cols[e], perm[e]});
+          ++bstart[(size_t)a * G + g + 1];
           mask[a] |= 1u << g;
           ++rem[g];
           ++left[a];
         }
     }
+    for (size_t z = 1; z < bstart.size(); ++z) bstart[z] += bstart[z - 1];
+    bleft.assign(bstart.begin(), bstart.end() - 1);            // fill cursor, then top (exclusive)
+    bcol.resize(bstart.back());
+    bperm.resize(bstart.back());
+    for (int a = 0; a < R; ++a)
+      for (int64_t e = 4 * (int64_t)rp[i0 + a]; e < 4 * (int64_t)rp[i0 + a + 1]; ++e)
+        if (perm[e] >= 0) {
+          const int32_t z = bleft[(size_t)a * G + cols[e] % G]++;
+          bcol[z] = cols[e];
+          bperm[z] = perm[e];
+        }
     int unit_a[16];
     int64_t unit_slot[16];
-    for (size_t t = 0; t < tmax; ++t)
+    for (int32_t t = 0; t < tmax; ++t)
       for (int k = 0; k < 4; ++k)
         for (int ph = 0; ph < 32 / G; ++ph) {
           int nu = 0;
           for (int lane = ph * G; lane < ph * G + G; ++lane) {
-            if (t >= lanes[lane].size()) continue;
-            const int a = lanes[lane][t].first;
+            const int a = lane / V, l = lane % V;
+            if (a >= R) continue;
+            const int32_t q = l + t * V;
+            if (q >= rp[i0 + a + 1] - rp[i0 + a]) continue;
             unit_a[nu] = a;
-            unit_slot[nu] = 4 * (int64_t)(rp[rows[a]] + lanes[lane][t].second) + k;
+            unit_slot[nu] = 4 * (int64_t)(rp[i0 + a] + q) + k;
             ++nu;
           }
-          // fewest choices first (insertion sort on the popcount of the row's groups)
-          for (int x = 1; x < nu; ++x)
-            for (int y = x; y > 0 && __builtin_popcount(mask[unit_a[y]]) < __builtin_popcount(mask[unit_a[y - 1]]); --y) {
-              std::swap(unit_a[y], unit_a[y - 1]);
-              std::swap(unit_slot[y], unit_slot[y - 1]);
-            }
+          // fewest choices first (stable insertion sort on the popcount of the row's groups)
+          if (nu > 1) {                                             // (as a counting sort)
+            int pc[16], cnt[18] = {0}, sa[16];
+            int64_t ss[16];
+            for (int x = 0; x < nu; ++x) { pc[x] = __builtin_popcount(mask[unit_a[x]]); ++cnt[pc[x] + 1]; }
+            for (int z = 1; z < 18; ++z) cnt[z] += cnt[z - 1];
+            for (int x = 0; x < nu; ++x) { const int z = cnt[pc[x]]++; sa[z] = unit_a[x]; ss[z] = unit_slot[x]; }
+            for (int x = 0; x < nu; ++x) { unit_a[x] = sa[x]; unit_slot[x] = ss[x]; }
+          }
           uint32_t used = 0;
           int any_col = -1;
           for (int x = 0; x < nu; ++x) {
@@ -273,16 +292,18 @@ void balance_banks(uint16_t* cols, int32_t* perm, const int32_t* rp, int32_t nr,
             const uint32_t avail = mask[a] & ~used;
             int g = -1;
             if (avail || (left[a] > 0 && slots[a] == left[a])) {
-              const uint32_t from = avail ? avail : mask[a];        // forced: a conflict
-              for (int h = 0; h < G; ++h)
-                if ((from >> h & 1u) && (g < 0 || rem[h] > rem[g])) g = h;
+              uint32_t from = avail ? avail : mask[a];              // forced: a conflict
+              for (; from; from &= from - 1) {                      // lowest group wins ties
+                const int h = __builtin_ctz(from);
+                if (g < 0 || rem[h] > rem[g]) g = h;
+              }
             }
             if (g >= 0) {
-              auto& b = bucket[(size_t)a * G + g];
-              ncol[slot] = b.back().first;
-              nperm[slot] = b.back().second;
-              b.pop_back();
-              if (b.empty()) mask[a] &= ~(1u << g);
+              const size_t bi = (size_t)a * G + g;
+              const int32_t z = --bleft[bi];
+              ncol[slot] = bcol[z];
+              nperm[slot] = bperm[z];
+              if (bleft[bi] == bstart[bi]) mask[a] &= ~(1u << g);
               --rem[g];
               --left[a];
               used |= 1u << g;
@@ -656,6 +677,11 @@ struct pdcs_ctx {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_st = nullptr, cap_st2 = nullptr;
+  // concurrent size-class kernels of one projection step (run_blocks): side
+  // streams and fork/join events (graph branches when captured)
+  cudaStream_t side[kNClass] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kNClass] = {};
+  bool serial_blocks = false;
   unsigned long long g_retry = 0, g_check = 0;   // nonzero only while capturing / in the graph
   bool graph_failed = false;
   int64_t nodes_trial = 0, nodes_accept = 0, nodes_check = 0;
@@ -676,6 +702,11 @@ struct pdcs_ctx {
     if (graph) cudaGraphDestroy(graph);
     if (cap_st) cudaStreamDestroy(cap_st);
     if (cap_st2) cudaStreamDestroy(cap_st2);
+    for (int c = 0; c < kNClass; ++c) {
+      if (side[c]) cudaStreamDestroy(side[c]);
+      if (ev_join[c]) cudaEventDestroy(ev_join[c]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
     if (ctl) cudaFree(ctl);
     if (hctl) cudaFreeHost(hctl);
     for (auto e : evpool) cudaEventDestroy(e);
@@ -785,18 +816,55 @@ struct pdcs_ctx {
     A.y = y.p; A.yh = yh.p; A.kxd = kxd.p;
     return A;
   }
+  // The size classes of one side are independent (disjoint coordinates and
+  // partial-sum slots): outside per-kernel timing the thread / warp / CTA /
+  // cluster kernels run concurrently on side streams (each alone fills only a
+  // fraction of the GPU: profiles/r1_ncu_blocks_mixed.txt), joined before the
+  // grid-team kernel, which runs last on the main stream.
   void run_blocks(bool primal, BlockArgs A, bool kkt, int cand) {
     BClass* cl = primal ? pcls : rcls;
-    for (int c = 0; c < kNClass; ++c) {
-      if (cl[c].count == 0) continue;
+    static const char* names[kNClass] = {"blocks_thread", "blocks_warp", "blocks_cta", "blocks_cluster",
+                                         "blocks_grid"};
+    int act[kNClass], na = 0;
+    for (int c = 0; c < kNClass - 1; ++c)
+      if (cl[c].count) act[na++] = c;
+    const bool par = !timing && !serial_blocks && na > 1;
+    if (par) {
+      if (!ev_fork) {
+        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        for (int c = 0; c < kNClass; ++c) {
+          CK(cudaStreamCreateWithFlags(&side[c], cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&ev_join[c], cudaEventDisableTiming));
+        }
+      }
+      CK(cudaEventRecord(ev_fork, st));
+    }
+    auto args = [&](int c) {
       BlockArgs B = A;
       B.blocks = A.blocks + cl[c].begin;
       B.nblocks = cl[c].count;
       B.cand = cand;
       B.part = kkt ? kpart.p : tpart.p;
       B.slot0 = kkt ? cl[c].kslot[cand] : cl[c].slot;
-      static const char* names[kNClass] = {"blocks_thread", "blocks_warp", "blocks_cta", "blocks_cluster",
-                                           "blocks_grid"};
+      return B;
+    };
+    for (int i = 0; i < na; ++i) {
+      const int c = act[i];
+      const BlockArgs B = args(c);
+      if (!par || i == 0) {
+        launch(names[c], [&] { CK(launch_blocks(c, cl[c].grid, B, ctl, gbuf.p, st)); });
+        continue;
+      }
+      CK(cudaStreamWaitEvent(side[i], ev_fork, 0));
+      ++launches;
+      CK(launch_blocks(c, cl[c].grid, B, ctl, gbuf.p, side[i]));
+      CK(cudaEventRecord(ev_join[i], side[i]));
+    }
+    if (par)
+      for (int i = 1; i < na; ++i) CK(cudaStreamWaitEvent(st, ev_join[i], 0));
+    if (cl[kNClass - 1].count) {
+      const int c = kNClass - 1;
+      const BlockArgs B = args(c);
       launch(names[c], [&] { CK(launch_blocks(c, cl[c].grid, B, ctl, gbuf.p, st)); });
     }
   }
@@ -1333,6 +1401,7 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
       ctx->dist = true;
     }
     ctx->st = (cudaStream_t)cuda_stream;
+    ctx->serial_blocks = std::getenv("PDCS_SERIAL_BLOCKS") && std::atoi(std::getenv("PDCS_SERIAL_BLOCKS")) != 0;
     ctx->mem_kind = mem_kind;
     ctx->rank = rank;
     ctx->world = world;

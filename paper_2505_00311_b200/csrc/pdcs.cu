@@ -94,26 +94,22 @@ struct TiledHost {
   std::vector<int32_t> blkb;       // sliced staged segments: segment-relative first quad of each warp block
   int64_t scratch = 0, staged = 0, nnz = 0;
   int32_t T = 0, elem = 1;
+  bool sliced = false, tma = false;   // layout / kernel decided once per build (environment read here)
   double build_ms = 0.0;
 };
 
 // shared-memory tile size in bytes (PDCS_TILE_KB overrides; default 32 KB)
 int tiled_tile_bytes() {
-  static const int b = std::getenv("PDCS_TILE_KB") ? 1024 * std::atoi(std::getenv("PDCS_TILE_KB")) : 32768;
-  return b;
+  return std::getenv("PDCS_TILE_KB") ? 1024 * std::atoi(std::getenv("PDCS_TILE_KB")) : 32768;
 }
 
 // TMA-pipelined partial kernel (opt-in, PDCS_TMA=1): it streams row-major
 // segments, so the sliced layout is off with it.
-bool tiled_tma_env() {
-  static const bool b = std::getenv("PDCS_TMA") && std::atoi(std::getenv("PDCS_TMA")) != 0;
-  return b;
-}
+bool tiled_tma_env() { return std::getenv("PDCS_TMA") && std::atoi(std::getenv("PDCS_TMA")) != 0; }
 // sliced (warp-interleaved) staged segments, tiled.cuh seg_row_dot_sliced;
 // PDCS_TILE_SLICED=0 keeps the row-major quad layout
 bool tiled_sliced() {
-  static const bool b = !tiled_tma_env() && !(std::getenv("PDCS_TILE_SLICED") && std::atoi(std::getenv("PDCS_TILE_SLICED")) == 0);
-  return b;
+  return !tiled_tma_env() && !(std::getenv("PDCS_TILE_SLICED") && std::atoi(std::getenv("PDCS_TILE_SLICED")) == 0);
 }
 
 // lanes per row for a segment with `avg` quads (staged) or entries (direct) per
@@ -324,11 +320,10 @@ void balance_banks(uint16_t* cols, int32_t* perm, const int32_t* rp, int32_t nr,
 // Chunks [row_a, row_b) (row_a a multiple of kTRows) into H, offsets local to H.
 void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, int64_t row_b, int64_t nvec,
                        int elem, int64_t group_nz, TiledHost& H) {
-  const int tile_bytes = tiled_tile_bytes();
-  const int32_t T = tile_bytes / (8 * elem);
+  const int tile_bytes = H.T * 8 * elem;
+  const int32_t T = H.T;
   const int64_t stage_min = tile_bytes / 16;           // staging must save >= 2x the gather sectors
   const int64_t ntiles = (nvec + T - 1) / T;
-  H.T = T;
   H.elem = elem;
   H.perm_s.reserve(ptr[row_b] - ptr[row_a]);
   H.col_s.reserve(ptr[row_b] - ptr[row_a]);
@@ -428,7 +423,7 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
         if (S.tile < 0 || S.V > 32) continue;
         balance_banks(H.col_s.data() + S.nz, H.perm_s.data() + S.nz, H.rowptr.data() + rpbase[k], nr, S.V, elem);
       }
-    if (tiled_sliced()) slice_segments(H, s_begin, s_begin + nseg, nr);
+    if (H.sliced) slice_segments(H, s_begin, s_begin + nseg, nr);
     // work items: consecutive segments up to group_nz nonzeros; the staged
     // segments of an item are cut into TMA batches of <= kBQ quads (row-major
     // layout only, PDCS_TMA=1)
@@ -496,13 +491,16 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
     const int64_t r = std::lower_bound(ptr, ptr + rows + 1, target) - ptr;
     cut[w] = std::max(cut[w - 1], std::min(rows, r / kTRows * kTRows));
   }
+  H.T = tiled_tile_bytes() / (8 * elem);
+  H.elem = elem;
+  H.tma = tiled_tma_env();
+  H.sliced = tiled_sliced();
   std::vector<TiledHost> part(nth);
+  for (auto& P : part) { P.T = H.T; P.sliced = H.sliced; P.tma = H.tma; }
   std::vector<std::thread> th;
   for (int w = 0; w < nth; ++w)
     th.emplace_back([&, w] { build_tiled_range(ptr, col, cut[w], cut[w + 1], nvec, elem, group_nz, part[w]); });
   for (auto& t : th) t.join();
-  H.T = tiled_tile_bytes() / (8 * elem);
-  H.elem = elem;
   H.nnz = ptr[rows];
   size_t ns = 0, nd = 0, nrp = 0;
   for (const auto& P : part) { ns += P.col_s.size() + 64; nd += P.col_d.size(); nrp += P.rowptr.size(); }
@@ -642,7 +640,7 @@ struct pdcs_ctx {
     TiledMat M;
     DBuf<TWork> work;
     DBuf<TBatch> batch;
-    bool tma = true;
+    bool tma = true, sliced = false;
     DBuf<TChunk> chunk;
     DBuf<TSeg> seg;
     DBuf<int32_t> rowptr, col_d, blkb;
@@ -904,7 +902,15 @@ struct pdcs_ctx {
     });
     if (dist) {
       // local K~^T y+ partial -> all-reduce -> x-side Halpern
-      spmv_store(KT, y.p, ktyp.p, true);
+      if (tKT.on) {
+        tiled_partial("tiled_KT_partial", tKT, 1, y.p, 2);
+        EpiStoreAcc ea{ktyp.p, 0};
+        launch("spmv_KT_partial", [&] {
+          k_tiled_combine<EpiStoreAcc, 1><<<tKT.g_combine, kThreads, 0, st>>>(tKT.M, tKT.scratch.p, ea, ctl, nullptr, 0);
+        });
+      } else {
+        spmv_store(KT, y.p, ktyp.p, true);
+      }
       allreduce(ktyp.p, n, ncclSum);
       launch("halpern_x", [&] {
         k_halpern_x<<<g_pe, kThreads, 0, st>>>(n, xh.p, x0.p, ktyp.p, x.p, kty.p, xsum.p, ctl);
@@ -1056,26 +1062,28 @@ struct pdcs_ctx {
     }
   }
 
-  static size_t tma_smem(int elem) {
-    return 2 * (size_t)tiled_tile_bytes() + (size_t)kNST * kBQ * 32 + (size_t)kNST * (kBQ + 2) * 8 +
-           (size_t)kNST * kBR * 4 + (size_t)kTRows * elem * sizeof(double);
+  // dynamic shared memory of the partial kernels, from the matrix's own tile size
+  static size_t tile_bytes(const TiledDev& D) { return (size_t)D.M.T * D.M.elem * sizeof(double); }
+  static size_t tma_smem(const TiledDev& D) {
+    return 2 * tile_bytes(D) + (size_t)kNST * kBQ * 32 + (size_t)kNST * (kBQ + 2) * 8 +
+           (size_t)kNST * kBR * 4 + (size_t)kTRows * D.M.elem * sizeof(double);
   }
   // launch the partial products of a tiled matrix (TMA pipeline or the plain kernel)
   void tiled_partial(const char* name, TiledDev& D, int elem, const double* xin, int guard) {
     launch(name, [&] {
       if (elem == 2) {
-        if (D.tma) k_tiled_tma<2><<<D.g_partial, kTThreads, tma_smem(2), st>>>(D.M, xin, D.scratch.p, ctl, guard);
-        else if (tiled_sliced()) k_tiled_sliced<2><<<D.g_partial, kTThreads, sliced_smem(2), st>>>(D.M, xin, D.scratch.p, ctl, guard);
-        else k_tiled_partial<2><<<D.g_partial, kTThreads, tiled_smem(2), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        if (D.tma) k_tiled_tma<2><<<D.g_partial, kTThreads, tma_smem(D), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        else if (D.sliced) k_tiled_sliced<2><<<D.g_partial, kTThreads, sliced_smem(D), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        else k_tiled_partial<2><<<D.g_partial, kTThreads, tiled_smem(D), st>>>(D.M, xin, D.scratch.p, ctl, guard);
       } else {
-        if (D.tma) k_tiled_tma<1><<<D.g_partial, kTThreads, tma_smem(1), st>>>(D.M, xin, D.scratch.p, ctl, guard);
-        else if (tiled_sliced()) k_tiled_sliced<1><<<D.g_partial, kTThreads, sliced_smem(1), st>>>(D.M, xin, D.scratch.p, ctl, guard);
-        else k_tiled_partial<1><<<D.g_partial, kTThreads, tiled_smem(1), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        if (D.tma) k_tiled_tma<1><<<D.g_partial, kTThreads, tma_smem(D), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        else if (D.sliced) k_tiled_sliced<1><<<D.g_partial, kTThreads, sliced_smem(D), st>>>(D.M, xin, D.scratch.p, ctl, guard);
+        else k_tiled_partial<1><<<D.g_partial, kTThreads, tiled_smem(D), st>>>(D.M, xin, D.scratch.p, ctl, guard);
       }
     });
   }
-  static size_t sliced_smem(int elem) { return 2 * (size_t)tiled_tile_bytes() + (size_t)kTRows * elem * sizeof(double); }
-  static size_t tiled_smem(int elem) { return (size_t)tiled_tile_bytes() + (size_t)kTRows * elem * sizeof(double); }
+  static size_t sliced_smem(const TiledDev& D) { return 2 * tile_bytes(D) + (size_t)kTRows * D.M.elem * sizeof(double); }
+  static size_t tiled_smem(const TiledDev& D) { return tile_bytes(D) + (size_t)kTRows * D.M.elem * sizeof(double); }
 
   // Build the tiled copy of a CSR (structure on the host, scaled values on the device).
   void make_tiled(TiledDev& D, TiledHost& H, int64_t rows, int64_t nvec, int elem, const double* dval) {
@@ -1116,22 +1124,23 @@ struct pdcs_ctx {
     M.blkb = D.blkb.p;
     // TMA-pipelined variant (k_tiled_tma) is opt-in: on B200 it measured slower than
     // the 4-CTA/SM register-streaming kernel, PDCS_TMA=1 enables it.
-    D.tma = tiled_tma_env();
+    D.tma = H.tma;
+    D.sliced = H.sliced;
     int occ = 1;
     if (elem == 2) {
-      CK(cudaFuncSetAttribute(k_tiled_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(2)));
-      CK(cudaFuncSetAttribute(k_tiled_sliced<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(2)));
-      CK(cudaFuncSetAttribute(k_tiled_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(2)));
-      if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<2>, kTThreads, tma_smem(2)));
-      else if (tiled_sliced()) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_sliced<2>, kTThreads, sliced_smem(2)));
-      else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<2>, kTThreads, tiled_smem(2)));
+      CK(cudaFuncSetAttribute(k_tiled_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(D)));
+      CK(cudaFuncSetAttribute(k_tiled_sliced<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
+      CK(cudaFuncSetAttribute(k_tiled_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(D)));
+      if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<2>, kTThreads, tma_smem(D)));
+      else if (D.sliced) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_sliced<2>, kTThreads, sliced_smem(D)));
+      else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<2>, kTThreads, tiled_smem(D)));
     } else {
-      CK(cudaFuncSetAttribute(k_tiled_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(1)));
-      CK(cudaFuncSetAttribute(k_tiled_sliced<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(1)));
-      CK(cudaFuncSetAttribute(k_tiled_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(1)));
-      if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<1>, kTThreads, tma_smem(1)));
-      else if (tiled_sliced()) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_sliced<1>, kTThreads, sliced_smem(1)));
-      else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<1>, kTThreads, tiled_smem(1)));
+      CK(cudaFuncSetAttribute(k_tiled_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(D)));
+      CK(cudaFuncSetAttribute(k_tiled_sliced<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
+      CK(cudaFuncSetAttribute(k_tiled_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(D)));
+      if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<1>, kTThreads, tma_smem(D)));
+      else if (D.sliced) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_sliced<1>, kTThreads, sliced_smem(D)));
+      else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<1>, kTThreads, tiled_smem(D)));
     }
     D.g_partial = (int)std::max<int64_t>(1, std::min<int64_t>(M.nwork, (int64_t)sms * std::max(occ, 1)));
     int64_t slabs = 0;

@@ -93,11 +93,16 @@ def test_gloo_world2_sharded_products():
 
 
 @pytest.mark.gpu
-def test_nccl_path_single_rank_matches_local():
+@pytest.mark.parametrize("tiled", ["auto", "1"])
+def test_nccl_path_single_rank_matches_local(tiled, monkeypatch):
     """The row-sharded code path (NCCL all-reduces, unfused K^T + Halpern,
-    pre-reduced decisions) with a 1-rank communicator reproduces the local path."""
+    pre-reduced decisions) with a 1-rank communicator reproduces the local path
+    (tiled = "1": both sweeps forced through the column-tiled formats)."""
     import torch  # noqa: F401  (loads libnccl.so.2 the library reuses)
     import paper_2505_00311_b200 as P
+    if tiled != "auto":
+        monkeypatch.setenv("PDCS_TILED", tiled)
+        monkeypatch.setenv("PDCS_TILE_KB", "1")
     prog = gen_mixed(400, 60, 200, seed=11, soc_dims=(3, 60))
     uid = P.pdcs_nccl_unique_id()
     g1 = P.PdcsSolver(prog, nccl_id=uid, rank=0, world=1)

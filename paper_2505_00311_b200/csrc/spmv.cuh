@@ -66,12 +66,15 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
 // Software-pipelined: the column ids / values of chunk i+1 are in flight while
 // chunk i's gathers are served; tails are predicated.  Results valid in all
 // lanes of the group.
+#ifndef PDCS_CSR_U
+#define PDCS_CSR_U 8                  // entries in flight per lane, V >= 8 (B200: 4 -> 8 with the 64-register cap, MPO +13%, mixed +7%)
+#endif
 template <int V, int NX>
 __device__ __forceinline__ void row_dot(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                                         const double* __restrict__ val, const double* __restrict__ x1,
                                         const double* __restrict__ x2, int64_t row, int lane, double& s1,
                                         double& s2) {
-  constexpr int U = 4;
+  constexpr int U = (V >= 8 && V <= 32) ? PDCS_CSR_U : 4;   // entries in flight per lane
   s1 = 0.0;
   s2 = 0.0;
   if (row >= 0) {
@@ -126,8 +129,11 @@ __device__ __forceinline__ void row_dot(const int32_t* __restrict__ ptr, const i
 //   __device__ void init(const Ctl*);              read scalars once
 //   __device__ bool active() const;                predicate (false: kernel is a no-op)
 //   __device__ void row(int64_t i, double dot1, double dot2, Acc<NA>&);
+#ifndef PDCS_CSR_MINB
+#define PDCS_CSR_MINB 4               // 64 registers: 4 CTAs of 256 threads per SM
+#endif
 template <class Epi>
-__global__ void __launch_bounds__(kThreads) spmv_kernel(const int32_t* __restrict__ ptr,
+__global__ void __launch_bounds__(kThreads, PDCS_CSR_MINB) spmv_kernel(const int32_t* __restrict__ ptr,
                                                         const int32_t* __restrict__ col,
                                                         const double* __restrict__ val,
                                                         const double* __restrict__ x1,

@@ -175,12 +175,54 @@ __global__ void __launch_bounds__(kThreads, PDCS_CSR_MINB) spmv_kernel(const int
       __syncthreads();
     }
   } else if (K.V == 1) {
-    for (int64_t idx = (int64_t)lcta * kThreads + threadIdx.x; idx < K.nrows;
-         idx += (int64_t)K.ncta * kThreads) {
-      const int64_t row = rowid(idx);
-      double s1, s2;
-      row_dot<1, NX>(ptr, col, val, x1, x2, row, 0, s1, s2);
-      epi.row(row, s1, s2, acc);
+    // one thread per row (rows of <= 2 nnz as binned): R rows per thread and
+    // step, their pointers, first two entries and gathers issued together so
+    // that the dependent latencies of the R rows overlap
+    constexpr int R = 4;
+    const int64_t stride = (int64_t)K.ncta * kThreads;
+    auto gather = [&](int32_t c, double a, double& s1, double& s2) {
+      if (c < 0) return;
+      if (NX == 3) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(x1) + c);
+        s1 += a * v.x;
+        s2 += a * v.y;
+      } else {
+        s1 += a * __ldg(x1 + c);
+        if (NX == 2) s2 += a * __ldg(x2 + c);
+      }
+    };
+    for (int64_t i0 = (int64_t)lcta * kThreads + threadIdx.x; i0 < K.nrows; i0 += R * stride) {
+      int64_t rw[R];
+      int32_t b[R], e[R], c0[R], c1[R];
+      double a0[R], a1[R], s1[R], s2[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int64_t idx = i0 + k * stride;
+        rw[k] = idx < K.nrows ? rowid(idx) : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        b[k] = rw[k] >= 0 ? __ldg(ptr + rw[k]) : 0;
+        e[k] = rw[k] >= 0 ? __ldg(ptr + rw[k] + 1) : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        c0[k] = b[k] < e[k] ? ld_stream(col + b[k]) : -1;
+        a0[k] = b[k] < e[k] ? ld_stream(val + b[k]) : 0.0;
+        c1[k] = b[k] + 1 < e[k] ? ld_stream(col + b[k] + 1) : -1;
+        a1[k] = b[k] + 1 < e[k] ? ld_stream(val + b[k] + 1) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        s1[k] = 0.0;
+        s2[k] = 0.0;
+        gather(c0[k], a0[k], s1[k], s2[k]);
+        gather(c1[k], a1[k], s1[k], s2[k]);
+        for (int32_t p = b[k] + 2; p < e[k]; ++p) gather(ld_stream(col + p), ld_stream(val + p), s1[k], s2[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (rw[k] >= 0) epi.row(rw[k], s1[k], s2[k], acc);
     }
   } else if (K.V >= 8) {
     // V lanes per row, epilogue run directly by the group leader (matrix bytes

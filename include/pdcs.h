@@ -127,7 +127,9 @@ typedef struct {
   int64_t iters;          /* accepted inner iterations */
   int64_t trials;         /* PDHG trials incl. line-search rejects */
   int64_t restarts;
-  int64_t spmv_K, spmv_KT;
+  int64_t spmv_K, spmv_KT; /* matrix passes over K~ / K~^T: one K sweep per trial (K x^ and
+                             K x together), one K^T sweep per accepted step, and per Eq. 9
+                             check K^T y^ (+ K xbar and K^T ybar for the average candidate) */
   double eta, omega, beta;
   double solve_seconds;
 } pdcs_result_t;

@@ -91,6 +91,7 @@ struct Ctl {
   // parameters
   double ls_shrink, ls_grow, beta_max, suff, nec, art;
   int32_t ls_max_rejects, refl_window, check_interval, pad;
+  int64_t checks;            // Eq. 9 checks run by the iteration (matrix-pass accounting)
 };
 
 // Partial-sum slots: every reducing kernel writes NACC doubles per CTA.

@@ -432,6 +432,7 @@ __global__ void k_kkt_decide(int ncand, int mode, double hnorm, double cnorm, Ct
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double* red = ctl->kred;
   Ctl& C = *ctl;
+  if (mode == 1) C.checks++;
   double e[2] = {kInf, kInf};
   for (int c = 0; c < ncand; ++c) {
     auto R = [&](int i) { return red[10 * c + i]; };

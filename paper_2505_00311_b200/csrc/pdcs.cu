@@ -1851,6 +1851,10 @@ static void finish_result(pdcs_ctx* ctx, pdcs_result_t* out, double secs) {
   out->kkt.err_p = C.best_kkt[0]; out->kkt.err_d = C.best_kkt[1]; out->kkt.err_gap = C.best_kkt[2];
   out->kkt.pobj = C.best_kkt[3]; out->kkt.dobj = C.best_kkt[4];
   out->iters = C.total; out->trials = C.trials; out->restarts = C.restarts;
+  // matrix passes: one K sweep per trial (K x^ and K x together), one K^T sweep
+  // per accepted step, and per Eq. 9 check K^T y^ plus (PDCS) K xbar, K^T ybar
+  out->spmv_K = C.trials + (C.vanilla ? 0 : C.checks);
+  out->spmv_KT = C.total + C.checks * (C.vanilla ? 1 : 2);
   out->eta = C.eta; out->omega = C.omega; out->beta = C.beta;
   out->solve_seconds = secs;
 }

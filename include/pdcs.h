@@ -178,6 +178,15 @@ pdcs_status pdcs_kkt(pdcs_ctx *ctx, int which, pdcs_kkt_t *out);
  * evaluated point's residuals (reading A15).  Continues from the current state. */
 pdcs_status pdcs_solve(pdcs_ctx *ctx, pdcs_result_t *out);
 
+/* Set the stopping tolerance (>= 0) and solve time limit (seconds, 0 = none)
+ * for later pdcs_solve calls, and clear a finished status (OPTIMAL, ITERATION_
+ * or TIME_LIMIT) so the next pdcs_solve continues from the current state: the
+ * iterate, anchor, average, eta, omega and counters are kept.  Used to time
+ * one trajectory to several tolerances (1e-3 and
+ * 1e-6).  Errors: ARG (negative / NaN), STATE (before set_cones, or after
+ * NUMERICAL_ERROR), CUDA. */
+pdcs_status pdcs_set_tolerance(pdcs_ctx *ctx, double tol, double time_limit_s);
+
 /* Copy an iterate out: x [n], y [local rows]; space SCALED or ORIGINAL
  * (x = x~/q, y = y~/r, reading A2).  Output memory per the create mem_kind. */
 pdcs_status pdcs_get_iterate(pdcs_ctx *ctx, int which, int space, double *x, double *y);

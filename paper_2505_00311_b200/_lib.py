@@ -78,6 +78,7 @@ def lib():
         L.pdcs_iterate.argtypes = [C.c_void_p, C.c_int64, C.POINTER(pdcs_result_t)]
         L.pdcs_kkt.argtypes = [C.c_void_p, C.c_int, C.POINTER(pdcs_kkt_t)]
         L.pdcs_solve.argtypes = [C.c_void_p, C.POINTER(pdcs_result_t)]
+        L.pdcs_set_tolerance.argtypes = [C.c_void_p, C.c_double, C.c_double]
         L.pdcs_get_iterate.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.pdcs_set_iterate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.pdcs_get_scaling.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -107,7 +108,7 @@ EXPORTED = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterat
             "pdcs_kernel_times", "pdcs_enable_timing", "pdcs_launch_count", "pdcs_last_error",
             "pdcs_destroy", "pdcs_nccl_unique_id", "pdcs_get_scalars", "pdcs_get_state",
             "pdcs_set_state", "pdcs_tiled_layout_stats", "pdcs_proj_create", "pdcs_proj_run",
-            "pdcs_proj_info", "pdcs_proj_destroy"]
+            "pdcs_proj_info", "pdcs_proj_destroy", "pdcs_set_tolerance"]
 
 STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e_prev", "best_e", "k",
               "total", "trials", "restarts"]
@@ -179,6 +180,10 @@ def pdcs_solve(ctx) -> pdcs_result_t:
     r = pdcs_result_t()
     _check(lib().pdcs_solve(ctx, C.byref(r)), ctx)
     return r
+
+
+def pdcs_set_tolerance(ctx, tol, time_limit_s=0.0):
+    _check(lib().pdcs_set_tolerance(ctx, float(tol), float(time_limit_s)), ctx)
 
 
 def pdcs_kkt(ctx, which=CURRENT) -> pdcs_kkt_t:

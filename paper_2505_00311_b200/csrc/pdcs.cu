@@ -1959,6 +1959,25 @@ pdcs_status pdcs_solve(pdcs_ctx* ctx, pdcs_result_t* out) {
   });
 }
 
+// Tighten or loosen the stopping tolerance between solves (multi-tolerance
+// runs: time to 1e-3, then continue to 1e-6 from the same state).  Clears a
+// finished status so the next pdcs_solve continues; NUMERICAL_ERROR stays.
+pdcs_status pdcs_set_tolerance(pdcs_ctx* ctx, double tol, double time_limit_s) {
+  if (!ctx) return PDCS_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
+    if (!(tol >= 0.0) || !(time_limit_s >= 0.0)) fail(PDCS_ERR_ARG, "tol and time_limit_s must be >= 0");
+    ctx->read_ctl();
+    if (ctx->hctl->status == ST_NUMERICAL) fail(PDCS_ERR_STATE, "solver is in NUMERICAL_ERROR");
+    ctx->prm.tol = tol;
+    ctx->prm.time_limit_s = time_limit_s;
+    ctx->hctl->tol = tol;
+    ctx->hctl->done = 0;
+    ctx->hctl->status = ST_RUNNING;
+    ctx->write_ctl();
+  });
+}
+
 pdcs_status pdcs_kkt(pdcs_ctx* ctx, int which, pdcs_kkt_t* out) {
   if (!ctx || !out) return PDCS_ERR_ARG;
   return guard(ctx, [&] {

@@ -54,6 +54,9 @@ class PdcsSolver:
     def solve(self) -> dict:
         return _result_dict(L.pdcs_solve(self.ctx))
 
+    def set_tolerance(self, tol: float, time_limit_s: float = 0.0):
+        L.pdcs_set_tolerance(self.ctx, tol, time_limit_s)
+
     def kkt(self, which=L.CURRENT) -> dict:
         k = L.pdcs_kkt(self.ctx, which)
         return dict(err_p=k.err_p, err_d=k.err_d, err_gap=k.err_gap, pobj=k.pobj, dobj=k.dobj)

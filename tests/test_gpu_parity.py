@@ -218,6 +218,27 @@ def test_solve_fisher_and_mpo(P):
         assert max(r["err_p"], r["err_d"], r["err_gap"]) <= tol
 
 
+def test_set_tolerance_continues_trajectory(P):
+    """Solve to 1e-3, pdcs_set_tolerance(1e-6), solve again: the continued run
+    is the same trajectory as one solve straight to 1e-6 (stops land on Eq. 9
+    checks, the state is kept), so the iteration count and iterate bits match."""
+    prog = gen_lasso(100, 50, 1.0, seed=0, dense=True)
+    g = P.PdcsSolver(prog, tol=1e-3)
+    r1 = g.solve()
+    assert r1["status"] == "OPTIMAL" and max(r1["err_p"], r1["err_d"], r1["err_gap"]) <= 1e-3
+    g.set_tolerance(1e-6)
+    r2 = g.solve()
+    assert r2["status"] == "OPTIMAL" and max(r2["err_p"], r2["err_d"], r2["err_gap"]) <= 1e-6
+    h = P.PdcsSolver(prog, tol=1e-6)
+    r3 = h.solve()
+    assert r2["iters"] == r3["iters"] and r2["restarts"] == r3["restarts"]
+    x2, y2 = g.get_iterate(P.BEST)
+    x3, y3 = h.get_iterate(P.BEST)
+    assert np.array_equal(x2, x3) and np.array_equal(y2, y3)
+    with pytest.raises(P.PdcsError):
+        g.set_tolerance(-1.0)
+
+
 # ------------------------------------------------------------------ boundary errors
 def test_create_errors(P):
     prog = gen_lasso(10, 5, 1.0, dense=True)

@@ -111,6 +111,18 @@ def spmv_alg_bytes(prog):
     return {"spmv_K_dual": k_dual, "spmv_KT_halpern": kt_halpern}
 
 
+def elem_alg_bytes(prog):
+    """Algorithmic bytes of the two fused elementwise update kernels per launch.
+    k_primal_elem over the box / zero / R+ coordinates: kind byte, x, c~, K~^T y
+    in; x^ and the (x^, x) pair out (49 B), plus 8 B per finite l~ / u~.
+    k_halpern_y over all rows: y^, y, y0, sum(eta y) in; y+, sum out (48 B)."""
+    from instances import ZERO, NONNEG
+    pk, pdim = np.asarray(prog.pk), np.asarray(prog.pdim)
+    n_elem = prog.n1 + int(pdim[(pk == ZERO) | (pk == NONNEG)].sum())
+    bounds = 8 * int(np.isfinite(prog.l).sum() + np.isfinite(prog.u).sum())
+    return {"primal_elem": 49 * n_elem + bounds, "halpern_y": 48 * prog.m}
+
+
 def iter_alg_bytes(prog):
     """SURVEY §8(d) B_iter = [12 nnz + 4(m+1)] + [12 nnz + 4(n+1)] + 8*14*(m+n)."""
     nnz, m, n = prog.nnz, prog.m, prog.n
@@ -199,7 +211,7 @@ def run_reference(args):
     v = done / el
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / done,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config(prog, args),
             "cpu_baseline": {"value": v, "unit": "iter/s", "kind": "oracle", "cores": 1,
                              "sample": f"{done} of {args.steps} requested accepted iterations of the full "
@@ -326,7 +338,11 @@ def main():
                 "avg_launch_ms": avg_s * 1e3, "launches": cnt, "peak_source": peak_src,
                 "other_sweep": {k: {"GB/s": algb[k] / (v[0] / v[1] / 1e3) / 1e9,
                                     "frac": algb[k] / (v[0] / v[1] / 1e3) / 1e9 / peak}
-                                for k, v in sweeps.items() if k != dom}}
+                                for k, v in sweeps.items() if k != dom},
+                "fused_update": {k: {"GB/s": b / (ktimes[k][0] / ktimes[k][1] / 1e3) / 1e9,
+                                     "frac": b / (ktimes[k][0] / ktimes[k][1] / 1e3) / 1e9 / peak,
+                                     "alg_bytes_per_launch": b}
+                                 for k, b in elem_alg_bytes(prog).items() if k in ktimes and b > 0}}
     total_kernel_ms = sum(v[0] for v in ktimes.values())
     iter_bytes = iter_alg_bytes(prog)
 
@@ -372,7 +388,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded Philox, PAPER.md:1663 recipe at BASELINE configs[1] size)",
                 "config": _config(prog, args), "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,

@@ -66,59 +66,64 @@ __device__ __forceinline__ void set_graph_flags(unsigned long long h_retry, unsi
 
 // Reduce the trial partial slots into ctl->red3 (row-sharded runs all-reduce
 // red3[1..2] between this kernel and k_decide).
-__global__ void __launch_bounds__(kThreads) k_reduce_trial(const double* __restrict__ part, int64_t nslots,
-                                                           Ctl* ctl) {
-  if (ctl->status != ST_RUNNING) return;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (int64_t i = threadIdx.x; i < nslots; i += blockDim.x) {
-    s0 += part[i * kAcc + 0];
-    s1 += part[i * kAcc + 1];
-    s2 += part[i * kAcc + 2];
+// Sum of the trial partial slots in a fixed order by one CTA of kDecideThreads:
+// each thread keeps 4 independent chains (slots t, t+T, t+2T, t+3T, then
+// +4T ...) so 12 loads are in flight per thread instead of 3 (the serial
+// chain had made k_decide ~11 us, latency-bound: profiles/r1_launches_*).
+constexpr int kDecideThreads = 1024;
+__device__ __forceinline__ void block_sum3(const double* __restrict__ part, int64_t nslots, double out[3]) {
+  double s[4][3] = {};
+  const int64_t T = blockDim.x;
+  int64_t i = threadIdx.x;
+  for (; i + 3 * T < nslots; i += 4 * T) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s[u][c] += part[(i + u * T) * kAcc + c];
   }
-  __shared__ double red[3][kThreads];
-  red[0][threadIdx.x] = s0; red[1][threadIdx.x] = s1; red[2][threadIdx.x] = s2;
+  for (; i < nslots; i += T)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) s[0][c] += part[i * kAcc + c];
+  __shared__ double red[3][kDecideThreads];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) red[c][threadIdx.x] = (s[0][c] + s[1][c]) + (s[2][c] + s[3][c]);
   __syncthreads();
   for (int w = blockDim.x / 2; w >= 1; w >>= 1) {
     if ((int)threadIdx.x < w) {
-      red[0][threadIdx.x] += red[0][threadIdx.x + w];
-      red[1][threadIdx.x] += red[1][threadIdx.x + w];
-      red[2][threadIdx.x] += red[2][threadIdx.x + w];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) red[c][threadIdx.x] += red[c][threadIdx.x + w];
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) { ctl->red3[0] = red[0][0]; ctl->red3[1] = red[1][0]; ctl->red3[2] = red[2][0]; }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out[c] = red[c][0];
 }
 
-__global__ void __launch_bounds__(kThreads) k_decide(const double* __restrict__ part, int64_t nslots,
-                                                     Ctl* ctl, unsigned long long h_retry,
-                                                     unsigned long long h_check, int prereduced) {
+// Reduce the trial partial slots into ctl->red3 (row-sharded runs all-reduce
+// red3[1..2] between this kernel and k_decide).
+__global__ void __launch_bounds__(kDecideThreads) k_reduce_trial(const double* __restrict__ part, int64_t nslots,
+                                                                 Ctl* ctl) {
+  if (ctl->status != ST_RUNNING) return;
+  double r[3];
+  block_sum3(part, nslots, r);
+  if (threadIdx.x == 0) { ctl->red3[0] = r[0]; ctl->red3[1] = r[1]; ctl->red3[2] = r[2]; }
+}
+
+__global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restrict__ part, int64_t nslots,
+                                                           Ctl* ctl, unsigned long long h_retry,
+                                                           unsigned long long h_check, int prereduced) {
   if (ctl->status != ST_RUNNING) {
     if (threadIdx.x == 0) set_graph_flags(h_retry, h_check, 0u, 0u);
     return;
   }
   if (prereduced) nslots = 0;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (int64_t i = threadIdx.x; i < nslots; i += blockDim.x) {
-    s0 += part[i * kAcc + 0];
-    s1 += part[i * kAcc + 1];
-    s2 += part[i * kAcc + 2];
-  }
-  __shared__ double red[3][kThreads];
-  red[0][threadIdx.x] = s0; red[1][threadIdx.x] = s1; red[2][threadIdx.x] = s2;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w >= 1; w >>= 1) {
-    if ((int)threadIdx.x < w) {
-      red[0][threadIdx.x] += red[0][threadIdx.x + w];
-      red[1][threadIdx.x] += red[1][threadIdx.x + w];
-      red[2][threadIdx.x] += red[2][threadIdx.x + w];
-    }
-    __syncthreads();
-  }
+  double red[3];
+  block_sum3(part, nslots, red);
   if (threadIdx.x != 0) return;
   Ctl& C = *ctl;
-  const double dxx = prereduced ? C.red3[0] : red[0][0];
-  const double dyy = prereduced ? C.red3[1] : red[1][0];
-  const double cross = prereduced ? C.red3[2] : red[2][0];
+  const double dxx = prereduced ? C.red3[0] : red[0];
+  const double dyy = prereduced ? C.red3[1] : red[1];
+  const double cross = prereduced ? C.red3[2] : red[2];
   C.last_dxx = dxx; C.last_dyy = dyy; C.last_cross = cross;
   const double num = C.omega * dxx + dyy / C.omega;
   C.last_num = num;

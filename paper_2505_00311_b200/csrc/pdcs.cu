@@ -887,11 +887,11 @@ struct pdcs_ctx {
     }
     run_blocks(false, bargs(false, BOP_TRIAL_DUAL), false, 0);
     if (dist) {
-      launch("reduce_trial", [&] { k_reduce_trial<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl); });
+      launch("reduce_trial", [&] { k_reduce_trial<<<1, kDecideThreads, 0, st>>>(tpart.p, nslot_trial, ctl); });
       allreduce(&ctl->red3[1], 2, ncclSum);     // ||dy||^2 and <dy, K dx> over the row shards
-      launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, 0, ctl, g_retry, g_check, 1); });
+      launch("decide", [&] { k_decide<<<1, kDecideThreads, 0, st>>>(tpart.p, 0, ctl, g_retry, g_check, 1); });
     } else {
-      launch("decide", [&] { k_decide<<<1, kThreads, 0, st>>>(tpart.p, nslot_trial, ctl, g_retry, g_check, 0); });
+      launch("decide", [&] { k_decide<<<1, kDecideThreads, 0, st>>>(tpart.p, nslot_trial, ctl, g_retry, g_check, 0); });
     }
   }
   // Accepted step: y+ (Halpern/average on y), then K^T y+ with the fused

@@ -231,6 +231,15 @@ int64_t pdcs_launch_count(const pdcs_ctx *ctx);
 const char *pdcs_last_error(const pdcs_ctx *ctx);
 void pdcs_destroy(pdcs_ctx *ctx);
 
+/* Host-only diagnostic: build the column-tiled format of the CSR (row_ptr
+ * [rows+1], col [nnz], host memory) on host threads exactly as pdcs_create /
+ * pdcs_set_cones do, and report out[0] = total build ms, out[1] = ms of the
+ * threaded per-range phase, out[2] = staged nonzeros.  elem 2 = the K sweep's
+ * (x^, x) pair gather, 1 = the K^T sweep's doubles.  Returns 3, or 0 on bad
+ * arguments.  No device is touched. */
+int pdcs_tiled_build_host(const int64_t *row_ptr, const int32_t *col, int64_t rows, int64_t nvec, int elem,
+                          double *out);
+
 /* Host-only diagnostic, no GPU needed: build the column-tiled layout
  * of a CSR structure (row_ptr[rows+1], col[nnz], valid and
  * sorted; elem = 2 for the (x^, x) pair gather of K, 1 for the y gather of

@@ -94,6 +94,8 @@ def lib():
         L.pdcs_tiled_layout_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                               C.c_void_p, C.c_int]
         L.pdcs_tiled_layout_stats.restype = C.c_int
+        L.pdcs_tiled_build_host.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+        L.pdcs_tiled_build_host.restype = C.c_int
         L.pdcs_proj_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, P_I32, P_I64, C.c_int64, C.c_int]
         L.pdcs_proj_run.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.pdcs_proj_info.argtypes = [C.c_void_p, P_I64, P_I64]
@@ -108,7 +110,7 @@ EXPORTED = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterat
             "pdcs_kernel_times", "pdcs_enable_timing", "pdcs_launch_count", "pdcs_last_error",
             "pdcs_destroy", "pdcs_nccl_unique_id", "pdcs_get_scalars", "pdcs_get_state",
             "pdcs_set_state", "pdcs_tiled_layout_stats", "pdcs_proj_create", "pdcs_proj_run",
-            "pdcs_proj_info", "pdcs_proj_destroy", "pdcs_set_tolerance"]
+            "pdcs_proj_info", "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host"]
 
 STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e_prev", "best_e", "k",
               "total", "trials", "restarts"]
@@ -180,6 +182,16 @@ def pdcs_solve(ctx) -> pdcs_result_t:
     r = pdcs_result_t()
     _check(lib().pdcs_solve(ctx, C.byref(r)), ctx)
     return r
+
+
+def pdcs_tiled_build_host(row_ptr, col, rows, nvec, elem) -> dict:
+    """Host-only timing of the tiled-format build (no device)."""
+    out = np.zeros(3)
+    rp = np.ascontiguousarray(row_ptr, np.int64); cl = np.ascontiguousarray(col, np.int32)
+    n = lib().pdcs_tiled_build_host(rp.ctypes.data, cl.ctypes.data, rows, nvec, elem, out.ctypes.data)
+    if n != 3:
+        raise ValueError("pdcs_tiled_build_host: bad arguments")
+    return dict(build_ms=out[0], ranges_ms=out[1], staged=int(out[2]))
 
 
 def pdcs_set_tolerance(ctx, tol, time_limit_s=0.0):

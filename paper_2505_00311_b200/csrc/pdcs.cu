@@ -95,7 +95,15 @@ struct TiledHost {
   int64_t scratch = 0, staged = 0, nnz = 0;
   int32_t T = 0, elem = 1;
   bool sliced = false, tma = false;   // layout / kernel decided once per build (environment read here)
-  double build_ms = 0.0;
+  double build_ms = 0.0, ranges_ms = 0.0;
+  // Parts mode (the solver's builds): the per-entry arrays stay in the
+  // per-thread parts and are uploaded slice by slice at these offsets
+  // (no host concatenation; tot_* are the concatenated sizes incl. padding).
+  std::vector<TiledHost> parts;
+  std::vector<size_t> o_s, o_d, o_rp, o_bb;
+  size_t tot_s = 0, tot_d = 0, tot_rp = 0, tot_bb = 0;
+  size_t n_s() const { return parts.empty() ? col_s.size() : tot_s; }
+  size_t n_d() const { return parts.empty() ? col_d.size() : tot_d; }
 };
 
 // shared-memory tile size in bytes (PDCS_TILE_KB overrides; default 32 KB)
@@ -473,7 +481,7 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
 // built on host threads (build_tiled_range) and concatenated in order with
 // their offsets rebased, so the result does not depend on the thread count.
 void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
-                 TiledHost& H) {
+                 TiledHost& H, bool keep_parts = false) {
   const auto t_start = std::chrono::steady_clock::now();
   // work-item size: enough items to fill the GPU several times over, no more
   // partial groups per chunk than needed (PDCS_TILE_GROUP overrides)
@@ -501,24 +509,30 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
   for (int w = 0; w < nth; ++w)
     th.emplace_back([&, w] { build_tiled_range(ptr, col, cut[w], cut[w + 1], nvec, elem, group_nz, part[w]); });
   for (auto& t : th) t.join();
+  H.ranges_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   H.nnz = ptr[rows];
-  size_t ns = 0, nd = 0, nrp = 0;
-  for (const auto& P : part) { ns += P.col_s.size() + 64; nd += P.col_d.size(); nrp += P.rowptr.size(); }
-  H.col_s.reserve(ns + 8); H.perm_s.reserve(ns + 8); H.col_d.reserve(nd); H.perm_d.reserve(nd);
-  H.rowptr.reserve(nrp + 8);
-  for (auto& P : part) {
-    H.col_s.resize((H.col_s.size() + 63) & ~(size_t)63, 0);  // keep segment starts 512-B aligned (values)
-    H.perm_s.resize(H.col_s.size(), -1);
-    const int64_t bbbase = (int64_t)H.blkb.size();
+  // Concatenate the parts in order.  The small per-segment / per-item arrays
+  // are rebased serially; the per-entry arrays (column ids, value permutation,
+  // row pointers, block bases) are copied verbatim, one thread per part, into
+  // vectors sized once (the serial inserts had taken ~25% of the build).
+  const int np = (int)part.size();
+  std::vector<size_t> o_s(np), o_d(np), o_rp(np), o_bb(np);
+  size_t ns = 0, nd = 0, nrp = 0, nbb = 0;
+  for (int w = 0; w < np; ++w) {
+    const TiledHost& P = part[w];
+    ns = (ns + 63) & ~(size_t)63;              // keep segment starts 512-B aligned (values)
+    o_s[w] = ns; o_d[w] = nd; o_rp[w] = nrp; o_bb[w] = nbb;
+    ns += P.col_s.size(); nd += P.col_d.size(); nrp += P.rowptr.size(); nbb += P.blkb.size();
+  }
+  for (int w = 0; w < np; ++w) {
+    TiledHost& P = part[w];
     const int64_t sbase = (int64_t)H.seg.size(), bbase = (int64_t)H.batch.size(), cbase = (int64_t)H.chunk.size();
-    const int64_t rpb = (int64_t)H.rowptr.size(), nzs = (int64_t)H.col_s.size(), nzd = (int64_t)H.col_d.size();
     for (TSeg S : P.seg) {
-      S.rp += rpb;
-      S.nz += S.tile >= 0 ? nzs : nzd;
-      if (S.bb >= 0) S.bb += bbbase;
+      S.rp += (int64_t)o_rp[w];
+      S.nz += S.tile >= 0 ? (int64_t)o_s[w] : (int64_t)o_d[w];
+      if (S.bb >= 0) S.bb += (int64_t)o_bb[w];
       H.seg.push_back(S);
     }
-    H.blkb.insert(H.blkb.end(), P.blkb.begin(), P.blkb.end());
     for (TBatch B : P.batch) { B.seg += (int32_t)sbase; H.batch.push_back(B); }
     for (TWork W : P.work) {
       W.chunk += (int32_t)cbase; W.s0 += (int32_t)sbase; W.s1 += (int32_t)sbase;
@@ -528,13 +542,36 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
     for (TChunk C : P.chunk) { C.scratch += H.scratch; H.chunk.push_back(C); }
     H.scratch += P.scratch;
     H.staged += P.staged;
-    H.rowptr.insert(H.rowptr.end(), P.rowptr.begin(), P.rowptr.end());
-    H.srow.insert(H.srow.end(), P.srow.begin(), P.srow.end());
-    H.col_s.insert(H.col_s.end(), P.col_s.begin(), P.col_s.end());
-    H.perm_s.insert(H.perm_s.end(), P.perm_s.begin(), P.perm_s.end());
-    H.col_d.insert(H.col_d.end(), P.col_d.begin(), P.col_d.end());
-    H.perm_d.insert(H.perm_d.end(), P.perm_d.begin(), P.perm_d.end());
-    P = TiledHost();
+  }
+  if (keep_parts) {
+    H.o_s = std::move(o_s); H.o_d = std::move(o_d); H.o_rp = std::move(o_rp); H.o_bb = std::move(o_bb);
+    H.tot_s = ns + 8;          // TMA column-id copies may read one quad past the end
+    H.tot_d = nd;
+    H.tot_rp = nrp + 8;        // TMA row-pointer slices are rounded up to 16 B
+    H.tot_bb = nbb + 1;        // never empty (device upload)
+    for (auto& P : part) { P.seg.clear(); P.batch.clear(); P.work.clear(); P.chunk.clear(); }
+    H.parts = std::move(part);
+    H.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    return;
+  }
+  H.col_s.assign(ns, 0); H.perm_s.assign(ns, -1);
+  H.col_d.resize(nd); H.perm_d.resize(nd);
+  H.rowptr.resize(nrp); H.srow.resize(nrp); H.blkb.resize(nbb);
+  {
+    std::vector<std::thread> cp;
+    for (int w = 0; w < np; ++w)
+      cp.emplace_back([&, w] {
+        TiledHost& P = part[w];
+        std::copy(P.col_s.begin(), P.col_s.end(), H.col_s.begin() + o_s[w]);
+        std::copy(P.perm_s.begin(), P.perm_s.end(), H.perm_s.begin() + o_s[w]);
+        std::copy(P.col_d.begin(), P.col_d.end(), H.col_d.begin() + o_d[w]);
+        std::copy(P.perm_d.begin(), P.perm_d.end(), H.perm_d.begin() + o_d[w]);
+        std::copy(P.rowptr.begin(), P.rowptr.end(), H.rowptr.begin() + o_rp[w]);
+        std::copy(P.srow.begin(), P.srow.end(), H.srow.begin() + o_rp[w]);
+        std::copy(P.blkb.begin(), P.blkb.end(), H.blkb.begin() + o_bb[w]);
+        P = TiledHost();
+      });
+    for (auto& t : cp) t.join();
   }
   H.col_s.resize(H.col_s.size() + 8, 0);      // TMA column-id copies may read one quad past the end
   H.blkb.push_back(0);                        // never empty (device upload)
@@ -1096,22 +1133,54 @@ struct pdcs_ctx {
     upload(D.batch, H.batch, st);
     upload(D.chunk, H.chunk, st);
     upload(D.seg, H.seg, st);
-    upload(D.rowptr, H.rowptr, st);
-    upload(D.srow, H.srow, st);
-    upload(D.col_s, H.col_s, st);
-    upload(D.col_d, H.col_d, st);
-    upload(D.blkb, H.blkb, st);
     DBuf<int32_t> perm;
-    D.val_s.alloc(std::max<size_t>(H.col_s.size(), 1));
-    D.val_d.alloc(std::max<size_t>(H.col_d.size(), 1));
-    if (!H.perm_s.empty()) {
-      upload(perm, H.perm_s, st);
-      k_gather_vals<<<grid_for((int64_t)H.perm_s.size(), sms, 32), kThreads, 0, st>>>((int64_t)H.perm_s.size(), perm.p, dval, D.val_s.p);
+    if (H.parts.empty()) {
+      upload(D.rowptr, H.rowptr, st);
+      upload(D.srow, H.srow, st);
+      upload(D.col_s, H.col_s, st);
+      upload(D.col_d, H.col_d, st);
+      upload(D.blkb, H.blkb, st);
+    } else {
+      // slices of the parts at their offsets; the gaps and tails hold the
+      // padding values of the concatenated layout (ids 0, permutation -1)
+      D.rowptr.alloc(H.tot_rp); D.srow.alloc(H.tot_rp); D.col_s.alloc(H.tot_s);
+      D.col_d.alloc(std::max<size_t>(H.tot_d, 1)); D.blkb.alloc(H.tot_bb);
+      perm.alloc(std::max<size_t>(H.tot_s, 1));
+      CK(cudaMemsetAsync(D.rowptr.p, 0, H.tot_rp * sizeof(int32_t), st));
+      CK(cudaMemsetAsync(D.srow.p, 0, H.tot_rp * sizeof(uint16_t), st));
+      CK(cudaMemsetAsync(D.col_s.p, 0, H.tot_s * sizeof(uint16_t), st));
+      CK(cudaMemsetAsync(D.blkb.p, 0, H.tot_bb * sizeof(int32_t), st));
+      CK(cudaMemsetAsync(perm.p, 0xff, H.tot_s * sizeof(int32_t), st));
+      auto put = [&](auto* dst, const auto& v, size_t off) {
+        if (!v.empty()) CK(cudaMemcpyAsync(dst + off, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, st));
+      };
+      for (size_t w = 0; w < H.parts.size(); ++w) {
+        const TiledHost& P = H.parts[w];
+        put(D.rowptr.p, P.rowptr, H.o_rp[w]);
+        put(D.srow.p, P.srow, H.o_rp[w]);
+        put(D.col_s.p, P.col_s, H.o_s[w]);
+        put(perm.p, P.perm_s, H.o_s[w]);
+        put(D.col_d.p, P.col_d, H.o_d[w]);
+        put(D.blkb.p, P.blkb, H.o_bb[w]);
+      }
+    }
+    D.val_s.alloc(std::max<size_t>(H.n_s(), 1));
+    D.val_d.alloc(std::max<size_t>(H.n_d(), 1));
+    if (H.n_s()) {
+      if (H.parts.empty()) upload(perm, H.perm_s, st);
+      k_gather_vals<<<grid_for((int64_t)H.n_s(), sms, 32), kThreads, 0, st>>>((int64_t)H.n_s(), perm.p, dval, D.val_s.p);
       CK(cudaStreamSynchronize(st));
     }
-    if (!H.perm_d.empty()) {
-      upload(perm, H.perm_d, st);
-      k_gather_vals<<<grid_for((int64_t)H.perm_d.size(), sms, 32), kThreads, 0, st>>>((int64_t)H.perm_d.size(), perm.p, dval, D.val_d.p);
+    if (H.n_d()) {
+      if (H.parts.empty()) upload(perm, H.perm_d, st);
+      else {
+        perm.alloc(H.tot_d);
+        for (size_t w = 0; w < H.parts.size(); ++w)
+          if (!H.parts[w].perm_d.empty())
+            CK(cudaMemcpyAsync(perm.p + H.o_d[w], H.parts[w].perm_d.data(), H.parts[w].perm_d.size() * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, st));
+      }
+      k_gather_vals<<<grid_for((int64_t)H.n_d(), sms, 32), kThreads, 0, st>>>((int64_t)H.n_d(), perm.p, dval, D.val_d.p);
       CK(cudaStreamSynchronize(st));
     }
     D.scratch.alloc(std::max<int64_t>(H.scratch, 1));
@@ -1446,7 +1515,7 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
     // tiled format of K~ (structure only) on host threads, overlapping the uploads
     // and the device transpose below; joined before this call returns
     ctx->thK = std::thread([ctx, hcolp, m, n] {
-      build_tiled(ctx->hptr.data(), hcolp, m, n, 2, ctx->hK);
+      build_tiled(ctx->hptr.data(), hcolp, m, n, 2, ctx->hK, true);
     });
     struct Joiner {
       std::thread& t;
@@ -1534,7 +1603,7 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
     ctx->hKTcol.resize(nnz);
     if (nnz) CK(cudaMemcpy(ctx->hKTcol.data(), ctx->KTcol.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
     ctx->thKT = std::thread([ctx, m, n] {
-      build_tiled(ctx->hKTptr.data(), ctx->hKTcol.data(), n, m, 1, ctx->hKT);
+      build_tiled(ctx->hKTptr.data(), ctx->hKTcol.data(), n, m, 1, ctx->hKT, true);
     });
     upload(ctx->planrows, rowstore, st);
     ctx->patch_plan(ctx->K);
@@ -2140,6 +2209,18 @@ int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
 int64_t pdcs_launch_count(const pdcs_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 void pdcs_destroy(pdcs_ctx* ctx) { delete ctx; }
+
+// Host-only timing of the tiled-format build (setup diagnostics; no device).
+// out[0] = total ms, out[1] = ms in the threaded per-range builds, out[2] = staged nnz.
+int pdcs_tiled_build_host(const int64_t* row_ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
+                          double* out) {
+  if (!row_ptr || (!col && row_ptr[rows] > 0) || rows < 0 || nvec <= 0 || (elem != 1 && elem != 2) || !out)
+    return 0;
+  TiledHost H;
+  build_tiled(row_ptr, col, rows, nvec, elem, H, true);
+  out[0] = H.build_ms; out[1] = H.ranges_ms; out[2] = (double)H.staged;
+  return 3;
+}
 
 int pdcs_tiled_layout_stats(const int64_t* row_ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
                             double* out, int cap) {

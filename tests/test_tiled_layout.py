@@ -100,3 +100,20 @@ def test_bank_balancing_lowers_wavefronts(monkeypatch):
         assert raw["structure_errors"] == 0 and bal["structure_errors"] == 0
         assert bal["lds_wavefronts"] < 0.85 * raw["lds_wavefronts"], (raw, bal)
         assert bal["lds_wavefronts"] <= 1.3 * bal["lds_wavefront_bound"], bal
+
+
+def test_parts_mode_build_matches_concatenated(monkeypatch):
+    """The solver's builds keep the per-thread parts and upload them at their
+    offsets (pdcs_tiled_build_host times that mode); the staged-entry count
+    must equal the concatenated layout's for any thread count."""
+    prog = gen_lasso(9000, 600, 0.03, seed=5)
+    K, KT = _csr(prog)
+    for A, nvec, elem in [(K, prog.n, 2), (KT, prog.m, 1)]:
+        ref = _stats(A, nvec, elem)
+        for th in ("1", "3", "8"):
+            monkeypatch.setenv("PDCS_BUILD_THREADS", th)
+            b = _lib.pdcs_tiled_build_host(A.indptr.astype(np.int64), A.indices.astype(np.int32),
+                                           A.shape[0], nvec, elem)
+            assert b["staged"] == ref["staged"] and b["build_ms"] >= b["ranges_ms"] >= 0.0
+    with pytest.raises(ValueError):
+        _lib.pdcs_tiled_build_host(K.indptr.astype(np.int64), K.indices.astype(np.int32), K.shape[0], 0, 2)

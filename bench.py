@@ -92,6 +92,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+DATA = {
+    "lasso": "synthetic (seeded Philox, PAPER.md:1663 recipe at BASELINE configs[1] size)",
+    "tiny_lasso": "synthetic (seeded Philox, PAPER.md:1663 recipe at BASELINE configs[0] size)",
+    "fisher": "synthetic (seeded Philox, PAPER.md:1618-1623 recipe at BASELINE configs[2] size)",
+    "mpo": "synthetic (seeded Philox, PAPER.md:1694-1705 with synthetic covariances, reading A24, BASELINE configs[3])",
+    "mixed": "synthetic (seeded Philox, SURVEY 8(d) cfg 5 planted mixed-cone recipe, one GPU's 1/8 share of BASELINE configs[4])",
+}
+
+
 def build_instance(config, seed):
     from instances import CONFIGS
     t = time.perf_counter()
@@ -389,7 +398,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded Philox, PAPER.md:1663 recipe at BASELINE configs[1] size)",
+                "data": DATA.get(args.config, "synthetic (seeded Philox)"),
                 "config": _config(prog, args), "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
                 "time_to_1e-4": tol_run,

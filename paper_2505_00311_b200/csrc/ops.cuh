@@ -109,18 +109,9 @@ __global__ void __launch_bounds__(kDecideThreads) k_reduce_trial(const double* _
   if (threadIdx.x == 0) { ctl->red3[0] = r[0]; ctl->red3[1] = r[1]; ctl->red3[2] = r[2]; }
 }
 
-__global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restrict__ part, int64_t nslots,
-                                                           Ctl* ctl, unsigned long long h_retry,
-                                                           unsigned long long h_check, int prereduced) {
-  if (ctl->status != ST_RUNNING) {
-    if (threadIdx.x == 0) set_graph_flags(h_retry, h_check, 0u, 0u);
-    return;
-  }
-  if (prereduced) nslots = 0;
-  double red[3];
-  block_sum3(part, nslots, red);
-  if (threadIdx.x != 0) return;
-  Ctl& C = *ctl;
+// Thread 0 of k_decide: accept test, beta window, Halpern coefficients, flags.
+__device__ __forceinline__ void decide_serial(Ctl& C, const double red[3], int prereduced,
+                                           unsigned long long h_retry, unsigned long long h_check) {
   const double dxx = prereduced ? C.red3[0] : red[0];
   const double dyy = prereduced ? C.red3[1] : red[1];
   const double cross = prereduced ? C.red3[2] : red[2];
@@ -170,6 +161,31 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restr
   C.tau = C.eta / C.omega;
   C.sigma = C.eta * C.omega;
   set_graph_flags(h_retry, h_check, (!acc && C.status == ST_RUNNING) ? 1u : 0u, C.need_check ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restrict__ part, int64_t nslots,
+                                                           Ctl* ctl, unsigned long long h_retry,
+                                                           unsigned long long h_check, int prereduced) {
+  if (ctl->status != ST_RUNNING) {
+    if (threadIdx.x == 0) set_graph_flags(h_retry, h_check, 0u, 0u);
+    return;
+  }
+  if (prereduced) nslots = 0;
+  // The decision is a serial chain of reads and writes of the control block;
+  // done on a shared-memory copy (loaded while the partials are summed, stored
+  // back by all threads) instead of ~10 dependent global round trips by one
+  // thread (k_decide was ~10 us in the launch list, the reduction ~1.5 of it).
+  static_assert(sizeof(Ctl) % sizeof(double) == 0, "Ctl is copied as doubles");
+  constexpr int kCtlWords = sizeof(Ctl) / sizeof(double);
+  __shared__ Ctl sC;
+  for (int i = threadIdx.x; i < kCtlWords; i += blockDim.x)
+    reinterpret_cast<double*>(&sC)[i] = reinterpret_cast<const double*>(ctl)[i];
+  double red[3];
+  block_sum3(part, nslots, red);               // ends with __syncthreads: sC is visible
+  if (threadIdx.x == 0) decide_serial(sC, red, prereduced, h_retry, h_check);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCtlWords; i += blockDim.x)
+    reinterpret_cast<double*>(ctl)[i] = reinterpret_cast<const double*>(&sC)[i];
 }
 
 // ---------------------------------------------------------------- SpMV epilogues

@@ -1706,7 +1706,14 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
       for (int c = 0; c < kNClass; ++c) {
         const int64_t cnt = cl[c].count;
         if (!cnt) continue;
-        if (c == 0) cl[c].grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + kThreadsSmall - 1) / kThreadsSmall, (int64_t)ctx->sms * 32));
+        if (c == 0) {
+          // PDCS_THREAD_CPT: cones per thread of the thread class (default 1);
+          // more per thread averages the exp root finder's iteration counts
+          // within a lane (the warp waits for its slowest lane) at lower occupancy
+          const int64_t cpt = std::getenv("PDCS_THREAD_CPT") ? std::max(1, std::atoi(std::getenv("PDCS_THREAD_CPT"))) : 1;
+          cl[c].grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + cpt * kThreadsSmall - 1) / (cpt * kThreadsSmall),
+                                                                  (int64_t)ctx->sms * 32));
+        }
         else if (c == 1) cl[c].grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 7) / 8, (int64_t)ctx->sms * 8));
         else if (c == 2) cl[c].grid = (int)std::min<int64_t>(cnt, (int64_t)ctx->sms * 4);
         else if (c == 3) cl[c].grid = kClusterCtas * (int)std::min<int64_t>(cnt, (int64_t)ctx->sms * 2 / kClusterCtas);

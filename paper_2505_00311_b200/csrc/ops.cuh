@@ -82,35 +82,19 @@ __device__ __forceinline__ void block_sum3(const double* __restrict__ part, int6
   for (; i < nslots; i += T)
 #pragma unroll
     for (int c = 0; c < 3; ++c) s[0][c] += part[i * kAcc + c];
-  // warp shuffles, then one warp over the per-warp sums: two barriers
-  // instead of a 10-level shared-memory tree (fixed order, deterministic)
-  double v[3];
+  __shared__ double red[3][kDecideThreads];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    v[c] = (s[0][c] + s[1][c]) + (s[2][c] + s[3][c]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v[c] += __shfl_down_sync(0xffffffffu, v[c], off);
-  }
-  __shared__ double wsum[3][kDecideThreads / 32];
-  __shared__ double tot[3];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  if (lane == 0) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) wsum[c][warp] = v[c];
-  }
+  for (int c = 0; c < 3; ++c) red[c][threadIdx.x] = (s[0][c] + s[1][c]) + (s[2][c] + s[3][c]);
   __syncthreads();
-  if (warp == 0) {
+  for (int w = blockDim.x / 2; w >= 1; w >>= 1) {
+    if ((int)threadIdx.x < w) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double w = lane < nwarp ? wsum[c][lane] : 0.0;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) w += __shfl_down_sync(0xffffffffu, w, off);
-      if (lane == 0) tot[c] = w;
+      for (int c = 0; c < 3; ++c) red[c][threadIdx.x] += red[c][threadIdx.x + w];
     }
+    __syncthreads();
   }
-  __syncthreads();
 #pragma unroll
-  for (int c = 0; c < 3; ++c) out[c] = tot[c];
+  for (int c = 0; c < 3; ++c) out[c] = red[c][0];
 }
 
 // Reduce the trial partial slots into ctl->red3 (row-sharded runs all-reduce

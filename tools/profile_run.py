@@ -10,6 +10,7 @@ ap.add_argument("--config", default="lasso")
 ap.add_argument("--m", type=int, default=200000)
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--scale", type=float, default=1.0 / 32)
+ap.add_argument("--T", type=int, default=20, help="MPO periods (bench config: 100)")
 a = ap.parse_args()
 if a.config == "lasso":
     prog = gen_lasso(a.m, 10000, 0.01, seed=0)
@@ -18,7 +19,7 @@ elif a.config == "fisher":
 elif a.config == "mixed":
     prog = gen_mixed_large(a.scale, seed=0)
 else:
-    prog = gen_mpo(20, 1000, seed=0)
+    prog = gen_mpo(a.T, 1000, seed=0)
 g = P.PdcsSolver(prog)
 g.iterate(a.iters)
 print("done", prog.m, prog.n, prog.nnz)

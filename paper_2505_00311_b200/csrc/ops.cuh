@@ -161,9 +161,17 @@ __device__ __forceinline__ void decide_serial(Ctl& C, const double red[3], int p
   set_graph_flags(h_retry, h_check, (!acc && C.status == ST_RUNNING) ? 1u : 0u, C.need_check ? 1u : 0u);
 }
 
+// Small duals (m <= kFuseYMax, single GPU): the accepted step's y-side
+// Halpern/average update (k_halpern_y) runs in this kernel after the
+// decision, saving a graph node per iteration where node latency dominates
+// (PAPER.md:918).  Same formula, same bits.
+constexpr int64_t kFuseYMax = 2048;
+struct FusedY { int64_t m; const double* yh; const double* y0; double* y; double* ysum; };
+
 __global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restrict__ part, int64_t nslots,
                                                            Ctl* ctl, unsigned long long h_retry,
-                                                           unsigned long long h_check, int prereduced) {
+                                                           unsigned long long h_check, int prereduced,
+                                                           FusedY fy) {
   if (ctl->status != ST_RUNNING) {
     if (threadIdx.x == 0) set_graph_flags(h_retry, h_check, 0u, 0u);
     return;
@@ -182,6 +190,14 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restr
   block_sum3(part, nslots, red);               // ends with __syncthreads: sC is visible
   if (threadIdx.x == 0) decide_serial(sC, red, prereduced, h_retry, h_check);
   __syncthreads();
+  if (fy.m > 0 && sC.status == ST_RUNNING && sC.accepted) {
+    const double a = sC.ha, b = sC.hbeta, c = sC.hb, eta = sC.eta_used;
+    for (int64_t i = threadIdx.x; i < fy.m; i += blockDim.x) {
+      const double yn = a * ((1.0 + b) * fy.yh[i] - b * fy.y[i]) + c * fy.y0[i];
+      fy.y[i] = yn;
+      fy.ysum[i] += eta * yn;
+    }
+  }
   for (int i = threadIdx.x; i < kCtlWords; i += blockDim.x)
     reinterpret_cast<double*>(ctl)[i] = reinterpret_cast<const double*>(&sC)[i];
 }

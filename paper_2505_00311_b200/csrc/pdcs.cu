@@ -856,14 +856,18 @@ struct pdcs_ctx {
   // cluster kernels run concurrently on side streams (each alone fills only a
   // fraction of the GPU: profiles/r1_ncu_blocks_mixed.txt), joined before the
   // grid-team kernel, which runs last on the main stream.
-  void run_blocks(bool primal, BlockArgs A, bool kkt, int cand) {
+  // extra (optional): one more independent kernel of the same phase (the
+  // trial's elementwise primal update), run as its own graph branch next to
+  // the size classes; joined before the grid-team kernel like them.
+  void run_blocks(bool primal, BlockArgs A, bool kkt, int cand,
+                  const std::function<void(cudaStream_t)>* extra = nullptr) {
     BClass* cl = primal ? pcls : rcls;
     static const char* names[kNClass] = {"blocks_thread", "blocks_warp", "blocks_cta", "blocks_cluster",
                                          "blocks_grid"};
     int act[kNClass], na = 0;
     for (int c = 0; c < kNClass - 1; ++c)
       if (cl[c].count) act[na++] = c;
-    const bool par = !timing && !serial_blocks && na > 1;
+    const bool par = !timing && !serial_blocks && na + (extra ? 1 : 0) > 1;
     if (par) {
       if (!ev_fork) {
         CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
@@ -873,6 +877,15 @@ struct pdcs_ctx {
         }
       }
       CK(cudaEventRecord(ev_fork, st));
+    }
+    if (extra) {
+      if (par) {
+        CK(cudaStreamWaitEvent(side[kNClass - 1], ev_fork, 0));
+        (*extra)(side[kNClass - 1]);
+        CK(cudaEventRecord(ev_join[kNClass - 1], side[kNClass - 1]));
+      } else {
+        (*extra)(st);
+      }
     }
     auto args = [&](int c) {
       BlockArgs B = A;
@@ -895,8 +908,10 @@ struct pdcs_ctx {
       CK(launch_blocks(c, cl[c].grid, B, ctl, gbuf.p, side[i]));
       CK(cudaEventRecord(ev_join[i], side[i]));
     }
-    if (par)
+    if (par) {
       for (int i = 1; i < na; ++i) CK(cudaStreamWaitEvent(st, ev_join[i], 0));
+      if (extra) CK(cudaStreamWaitEvent(st, ev_join[kNClass - 1], 0));
+    }
     if (cl[kNClass - 1].count) {
       const int c = kNClass - 1;
       const BlockArgs B = args(c);
@@ -907,11 +922,13 @@ struct pdcs_ctx {
   // ---------------------------------------------------------------- Alg. 1 pieces
   // One trial of AdaptiveStepPDHG (PDHG step Eq. 5 + accept test).
   void trial() {
-    launch("primal_elem", [&] {
-      k_primal_elem<<<g_pe, kThreads, 0, st>>>(n, ek.p, x.p, ct.p, kty.p, lt.p, ut.p, xh.p, xx.p, ctl,
-                                               tpart.p, slot_pe);
-    });
-    run_blocks(true, bargs(true, BOP_TRIAL_PRIMAL), false, 0);
+    const std::function<void(cudaStream_t)> pe = [&](cudaStream_t s_) {
+      launch("primal_elem", [&] {
+        k_primal_elem<<<g_pe, kThreads, 0, s_>>>(n, ek.p, x.p, ct.p, kty.p, lt.p, ut.p, xh.p, xx.p, ctl,
+                                                 tpart.p, slot_pe);
+      });
+    };
+    run_blocks(true, bargs(true, BOP_TRIAL_PRIMAL), false, 0, &pe);
     EpiDualTrial e{y.p, ht.p, rk.p, kxh.p, kxd.p, yh.p, 0.0, 0};
     if (tK.on) {
       tiled_partial("tiled_K_partial", tK, 2, reinterpret_cast<const double*>(xx.p), 1);
@@ -926,17 +943,22 @@ struct pdcs_ctx {
     if (dist) {
       launch("reduce_trial", [&] { k_reduce_trial<<<1, kDecideThreads, 0, st>>>(tpart.p, nslot_trial, ctl); });
       allreduce(&ctl->red3[1], 2, ncclSum);     // ||dy||^2 and <dy, K dx> over the row shards
-      launch("decide", [&] { k_decide<<<1, kDecideThreads, 0, st>>>(tpart.p, 0, ctl, g_retry, g_check, 1); });
+      launch("decide", [&] { k_decide<<<1, kDecideThreads, 0, st>>>(tpart.p, 0, ctl, g_retry, g_check, 1, FusedY{}); });
     } else {
-      launch("decide", [&] { k_decide<<<1, kDecideThreads, 0, st>>>(tpart.p, nslot_trial, ctl, g_retry, g_check, 0); });
+      const FusedY fy = fuse_y() ? FusedY{m, yh.p, y0.p, y.p, ysum.p} : FusedY{};
+      launch("decide", [&] { k_decide<<<1, kDecideThreads, 0, st>>>(tpart.p, nslot_trial, ctl, g_retry, g_check, 0, fy); });
     }
   }
   // Accepted step: y+ (Halpern/average on y), then K^T y+ with the fused
   // Halpern/average on x.
+  // y-side Halpern update folded into k_decide (small m, single GPU; PDCS_FUSE_Y=0 disables)
+  bool fuse_y_off = std::getenv("PDCS_FUSE_Y") && !std::atoi(std::getenv("PDCS_FUSE_Y"));   // read at create
+  bool fuse_y() const { return !dist && m > 0 && m <= kFuseYMax && !fuse_y_off; }
   void accept() {
-    launch("halpern_y", [&] {
-      k_halpern_y<<<g_m, kThreads, 0, st>>>(m, yh.p, y0.p, y.p, ysum.p, ctl);
-    });
+    if (!fuse_y())
+      launch("halpern_y", [&] {
+        k_halpern_y<<<g_m, kThreads, 0, st>>>(m, yh.p, y0.p, y.p, ysum.p, ctl);
+      });
     if (dist) {
       // local K~^T y+ partial -> all-reduce -> x-side Halpern
       if (tKT.on) {

@@ -424,3 +424,27 @@ def test_cta_and_grid_teams_one_step(P):
             o.iterate(1)
             assert parity(*g.get_iterate(P.PDHG_OUT), *o.get_iterate(1)) <= 1e-12
         g.close()
+
+
+@pytest.mark.parametrize("fuse", ["0", "1"])
+def test_fused_y_update_bit_identical(P, monkeypatch, fuse):
+    """The y-side Halpern update folded into k_decide (m <= 2048) computes the
+    same formula in the same order as k_halpern_y: 300 iterations with and
+    without it give the same bits, and both match the oracle."""
+    prog = mixed(11, m=500, n1=60, n2=200)
+    monkeypatch.setenv("PDCS_FUSE_Y", "1")
+    a = P.PdcsSolver(prog)
+    a.iterate(300)
+    monkeypatch.setenv("PDCS_FUSE_Y", fuse)
+    b = P.PdcsSolver(prog)
+    b.iterate(300)
+    xa, ya = a.get_iterate(P.CURRENT)
+    xb, yb = b.get_iterate(P.CURRENT)
+    assert np.array_equal(xa, xb) and np.array_equal(ya, yb)
+    o = O.OracleSolver(prog)
+    o.iterate(120)
+    c = P.PdcsSolver(prog)
+    c.iterate(120)
+    xc, yc = c.get_iterate(P.CURRENT)
+    xo, yo = o.get_iterate(0)
+    assert parity(xc, yc, xo, yo) <= TOL

@@ -316,12 +316,16 @@ static void proj_exp_scaled(const double* v0, const double* D, double* out) {
     }
   }
   // candidates (reading A18): root point, face point, t-raised point, 0.
-  double best[3] = {0.0, 0.0, 0.0};
-  double bestd = r0 * r0 + s0 * s0 + t0 * t0;   // candidate 0
+  // "Nearest" is decided by the sign of ||p - v0||^2 - ||q - v0||^2 =
+  // <p - q, p + q - 2 v0> (reading P7): the two squared distances can differ
+  // by less than one ulp of their common part (a far-away t0) while the
+  // points differ in r, s at 1e-6 relative.
+  double best[3] = {0.0, 0.0, 0.0};              // candidate 0
   auto consider = [&](double a, double b, double c) {
     if (!std::isfinite(a) || !std::isfinite(b) || !std::isfinite(c)) return;
-    double dd = (a - r0) * (a - r0) + (b - s0) * (b - s0) + (c - t0) * (c - t0);
-    if (dd < bestd) { bestd = dd; best[0] = a; best[1] = b; best[2] = c; }
+    double diff = (a - best[0]) * (a + best[0] - 2.0 * r0) + (b - best[1]) * (b + best[1] - 2.0 * s0) +
+                  (c - best[2]) * (c + best[2] - 2.0 * t0);
+    if (diff < 0.0) { best[0] = a; best[1] = b; best[2] = c; }
   };
   if (have_root && std::isfinite(rho)) {
     // v_p = (<v0,u>/||u||^2) u (orthogonal coefficient), u scaled by e^-max(rho,0)

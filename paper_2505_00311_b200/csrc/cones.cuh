@@ -363,12 +363,14 @@ __device__ __noinline__ void proj_exp_d(double r0, double s0, double t0, double 
     }
   }
   // candidates: root point, face (min(r0,0), 0, t0^+), t-raised point, 0
+  // nearest by the sign of <p - q, p + q - 2 v0> (reading P7; the squared
+  // distances themselves can tie to the ulp while the points differ)
   double b0 = 0.0, b1 = 0.0, b2 = 0.0;
-  double bd = r0 * r0 + s0 * s0 + t0 * t0;
   auto consider = [&](double a, double b, double c) {
     if (!isfinite(a) || !isfinite(b) || !isfinite(c)) return;
-    const double dd = (a - r0) * (a - r0) + (b - s0) * (b - s0) + (c - t0) * (c - t0);
-    if (dd < bd) { bd = dd; b0 = a; b1 = b; b2 = c; }
+    const double diff = (a - b0) * (a + b0 - 2.0 * r0) + (b - b1) * (b + b1 - 2.0 * s0) +
+                        (c - b2) * (c + b2 - 2.0 * t0);
+    if (diff < 0.0) { b0 = a; b1 = b; b2 = c; }
   };
   if (have && isfinite(rho)) {
     const double sc = exp(-fmax(rho, 0.0));

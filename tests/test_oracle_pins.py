@@ -582,3 +582,24 @@ def test_determinism():
     xa, ya = a.get_iterate(0)
     xb, yb = b.get_iterate(0)
     assert np.array_equal(xa, xb) and np.array_equal(ya, yb)
+
+
+def test_exp_nearest_candidate_when_distances_tie_to_the_ulp():
+    """Reading P7.  A point far below the cone (t0 << 0) next to the s = 0 face:
+    the root point and the t-raised point are at squared distances that agree
+    to one ulp of t0^2, yet differ in r, s at 1e-6 relative.  "Nearest" is
+    decided by <p - q, p + q - 2 v0>.  The first case is a primal exp block of
+    the mixed cfg 5 bench instance (seed 0, block 33696, first trial from the
+    seeded random point of tests/test_full_size.py); the rest are random
+    points of the same shape.  All are checked against the 60-digit
+    reference."""
+    cases = [(np.array([-53.848289446000855, 5.317878561776792, -533.0367249585]),
+              np.array([25.540130991958577, 59.559580156562696, 414.0600653716415]))]
+    rng = np.random.default_rng(11)
+    for _ in range(12):
+        D = 10 ** rng.uniform(-1, 2.5, 3)
+        cases.append((np.array([-rng.uniform(5, 80), rng.uniform(0.5, 8), -rng.uniform(100, 5000)]), D))
+    for v, D in cases:
+        ref = mp_exp_reference(v, D)
+        got = O.proj_exp_scaled(v, D)
+        assert np.max(np.abs(got - ref)) <= 1e-13 * (1 + np.max(np.abs(v))), (v, D, got, ref)

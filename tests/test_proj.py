@@ -112,3 +112,32 @@ def test_proj_teams_match_oracle(team, scaled):
     assert np.all(np.isfinite(g))
     err = _blockwise_err(kinds, dims, g, ref, v)
     assert err <= TOL, err
+
+
+@pytest.mark.gpu
+def test_proj_exp_far_below_face_nearest_candidate():
+    """Reading P7 on the GPU: exp / dual-exp blocks far below the cone next to
+    the s = 0 face, where the candidates' squared distances tie to the ulp
+    (the first block is the mixed cfg 5 case of
+    test_oracle_pins.test_exp_nearest_candidate_when_distances_tie_to_the_ulp).
+    The GPU must pick the oracle's (and the 60-digit reference's) point."""
+    import torch
+    import paper_2505_00311_b200 as P
+    rng = np.random.default_rng(11)
+    vs = [np.array([-53.848289446000855, 5.317878561776792, -533.0367249585])]
+    Ds = [np.array([25.540130991958577, 59.559580156562696, 414.0600653716415])]
+    for _ in range(200):
+        Ds.append(10 ** rng.uniform(-1, 2.5, 3))
+        vs.append(np.array([-rng.uniform(5, 80), rng.uniform(0.5, 8), -rng.uniform(100, 5000)]))
+    kinds = np.array([EXP] * len(vs) + [DUAL_EXP] * len(vs), np.int32)
+    dims = np.full(kinds.shape[0], 3, np.int64)
+    v = np.concatenate(vs + [-a for a in vs])
+    D = np.concatenate(Ds + [1.0 / d for d in Ds])
+    plan = P.pdcs_proj_create(kinds, dims)
+    out = torch.full((v.shape[0],), float("nan"), dtype=torch.float64, device="cuda")
+    P.pdcs_proj_run(plan, torch.from_numpy(D).cuda(), torch.from_numpy(v).cuda(), out)
+    torch.cuda.synchronize()
+    P.pdcs_proj_destroy(plan)
+    g = out.cpu().numpy()
+    o = _oracle(kinds, dims, v, D)
+    assert _blockwise_err(kinds, dims, g, o, v) <= TOL

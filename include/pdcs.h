@@ -191,7 +191,11 @@ pdcs_status pdcs_set_tolerance(pdcs_ctx *ctx, double tol, double time_limit_s);
  * (x = x~/q, y = y~/r, reading A2).  Output memory per the create mem_kind. */
 pdcs_status pdcs_get_iterate(pdcs_ctx *ctx, int which, int space, double *x, double *y);
 
-/* Set the current iterate (and anchor) from ORIGINAL-space x [n], y [local rows]. */
+/* Set the current iterate from ORIGINAL-space x [n], y [local rows] and start
+ * a new epoch there (as a restart does): anchor z0 = PDHG
+ * output = the point, its anchor KKT error evaluated, the inner counter k,
+ * the average sums and weight W, beta (= beta_max) and the previous-check
+ * error reset.  eta, omega and the total / trial / restart counters are kept. */
 pdcs_status pdcs_set_iterate(pdcs_ctx *ctx, const double *x, const double *y);
 
 /* Checkpoint / resume of the full Alg. 1 state in SCALED space:

@@ -946,6 +946,10 @@ void orc_set_iterate(void* h, const double* x, const double* y) {
   std::copy(y, y + S->P.m, S->y.begin());
   S->x0 = S->x; S->y0 = S->y; S->xh = S->x; S->yh = S->y;
   S->e_anchor = S->kmax(S->kkt(S->x.data(), S->y.data()));
+  // a new epoch at the given point, as pdcs_set_iterate (include/pdcs.h)
+  std::fill(S->xsum.begin(), S->xsum.end(), 0.0);
+  std::fill(S->ysum.begin(), S->ysum.end(), 0.0);
+  S->Wsum = 0.0; S->k = 0; S->beta = S->prm.beta_max; S->e_prev = -1.0;
 }
 // Full Alg. 1 state (scaled space) for checkpoint shadowing.
 void orc_get_state(void* h, double* x, double* y, double* x0, double* y0, double* xs, double* ys,

@@ -448,3 +448,28 @@ def test_fused_y_update_bit_identical(P, monkeypatch, fuse):
     xc, yc = c.get_iterate(P.CURRENT)
     xo, yo = o.get_iterate(0)
     assert parity(xc, yc, xo, yo) <= TOL
+
+
+def test_set_iterate_mid_run_starts_new_epoch(P):
+    """pdcs_set_iterate after some iterations starts a new epoch at the point
+    (include/pdcs.h): the oracle's set_iterate does the same, so the two agree
+    on the steps that follow (k, W, sums, beta reset; eta, omega, counters kept)."""
+    prog = mixed(13, m=400, n1=60, n2=200)
+    g = P.PdcsSolver(prog)
+    o = O.OracleSolver(prog)
+    ro, qo = o.get_scaling()
+    g.iterate(60)
+    o.iterate(60)
+    rng = np.random.default_rng(13)
+    x, y = rng.standard_normal(prog.n), rng.standard_normal(prog.m)
+    # eta / omega carry over and differ by rounding after 60 steps: hand the
+    # GPU the oracle's exact state first, then restart both at the point
+    g.set_state(o.get_state())
+    g.set_iterate(x, y)
+    o.set_iterate(x * qo, y * ro)
+    sg, so = g.get_state(), o.get_state()
+    assert np.array_equal(sg["sc"][9:], so["sc"][9:]) and sg["sc"][3] == so["sc"][3], (sg["sc"], so["sc"])
+    assert sg["sc"][4] == 0.0 and so["sc"][4] == 0.0
+    g.iterate(40)
+    o.iterate(40)
+    assert parity(*g.get_iterate(P.CURRENT), *o.get_iterate(0)) <= TOL

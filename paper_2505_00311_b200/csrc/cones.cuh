@@ -88,10 +88,12 @@ struct ClusterTeam {
 };
 
 // Whole-grid team (cooperative launch).  gbuf holds 2 buffers x 2 x gridDim doubles.
+constexpr int kGridCache = 8;   // elements per thread the grid team keeps in shared memory
 struct GridTeam {
   double* sm;      // >= 2*(blockDim/32) + 2 doubles of shared memory
   double* gbuf;
   int parity;
+  double* cache;   // 2 * kGridCache * blockDim doubles of dynamic shared memory (or nullptr)
   __device__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
   __device__ int size() const { return gridDim.x * blockDim.x; }
   __device__ void sum2(double& a, double& b) {
@@ -123,6 +125,12 @@ struct GridTeam {
 // Preconditions: d >= 2 (SOC) / >= 3 (RSOC); all team members call uniformly.
 enum SocMode { SM_ZERO = 0, SM_IDENT = 1, SM_HALF = 2, SM_LAM = 3, SM_MU = 4 };
 
+// Per-thread element cache of a team (only the grid team has one): the
+// member's first kGridCache elements are staged once in shared memory and
+// every later pass reads them from there instead of from L2 / HBM.
+template <class Team> __device__ __forceinline__ double* team_cache(Team&) { return nullptr; }
+__device__ __forceinline__ double* team_cache(GridTeam& t) { return t.cache; }
+
 template <class Team, class Src, class Dst>
 __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool unit, const Src& src,
                                          Dst& dst, int* newton_iters = nullptr) {
@@ -133,14 +141,29 @@ __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool un
   const int r = tm.rank(), S = tm.size();
   auto X = [&](int64_t i) { return i == 1 ? x1 : src.v(i); };
   auto H = [&](int64_t i) { return unit ? 1.0 : src.D(i) / D0; };   // dhat_i
+  // elements of this member in order i = 1 + r, 1 + r + S, ...: the first KC
+  // from the team's shared-memory cache (same values, same order: same bits)
+  double* const cache = team_cache(tm);
+  const int KC = cache ? kGridCache : 0, CT = blockDim.x, ct = threadIdx.x;
+  if (cache) {
+    int64_t i = 1 + r;
+    for (int k = 0; k < KC && i < d; ++k, i += S) {
+      cache[k * CT + ct] = X(i);
+      cache[(KC + k) * CT + ct] = H(i);
+    }
+  }
+  auto each = [&](auto&& f) {
+    int64_t i = 1 + r;
+    for (int k = 0; k < KC && i < d; ++k, i += S) f(i, cache[k * CT + ct], cache[(KC + k) * CT + ct]);
+    for (; i < d; i += S) f(i, X(i), H(i));
+  };
   // pass 1: ||dh x||^2 and ||x/dh||^2 (Thm 1 case tests)
   double a = 0.0, b = 0.0;
-  for (int64_t i = 1 + r; i < d; i += S) {
-    const double x = X(i), h = H(i);
+  each([&](int64_t, double x, double h) {
     const double p = h * x, q = x / h;
     a += p * p;
     b += q * q;
-  }
+  });
   tm.sum2(a, b);
   const double n_times = sqrt(a), n_over = sqrt(b);
   int mode;
@@ -163,15 +186,15 @@ __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool un
   if (unit) {
     // textbook SOC: ((t + ||x||)/2) (1, x/||x||); here n_times == n_over
     s_out = 0.5 * (t + n_times);
-    for (int64_t i = 1 + r; i < d; i += S) {
-      const double y = s_out * X(i) / n_times;
+    each([&](int64_t i, double x, double) {
+      const double y = s_out * x / n_times;
       if (i == 1) {
         if (rsoc) { dst.put(0, (s_out + y) * kRsqrt2); dst.put(1, (s_out - y) * kRsqrt2); }
         else { dst.put(0, s_out); dst.put(1, y); }
       } else {
         dst.put(i, y);
       }
-    }
+    });
     return;
   }
   int its = 0;
@@ -179,14 +202,14 @@ __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool un
     const double at = fabs(t);
     for (; its < 64; ++its) {
       double S0 = 0.0, S1 = 0.0;
-      for (int64_t i = 1 + r; i < d; i += S) {
-        const double x = X(i), h = H(i), h2 = h * h;
+      each([&](int64_t, double x, double h) {
+        const double h2 = h * h;
         double p, w;
         if (mode == SM_LAM) { const double rd = 1.0 / (h2 + 2.0 * par); p = h * x * rd; w = p * p * rd; }
         else { const double rd = 1.0 / (1.0 + par * h2); p = h * x * rd; w = p * p * h2 * rd; }
         S0 += p * p;
         S1 += w;
-      }
+      });
       tm.sum2(S0, S1);
       const double nrm = sqrt(S0);
       double psi, dpsi;
@@ -210,28 +233,28 @@ __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool un
   }
   if (newton_iters) *newton_iters = its;
   // recovery: y_i, s = ||y/dh|| (reading A16)
-  auto Y = [&](int64_t i) {
-    const double x = X(i), h = H(i), h2 = h * h;
+  auto Y = [&](double x, double h) {
+    const double h2 = h * h;
     if (mode == SM_HALF) return x / (1.0 + 1.0 / h2);
     if (mode == SM_LAM) return h2 * x / (h2 + 2.0 * par);
     return par * h2 * x / (1.0 + par * h2);
   };
   double ss = 0.0, dummy = 0.0;
-  for (int64_t i = 1 + r; i < d; i += S) {
-    const double q = Y(i) / H(i);
+  each([&](int64_t, double x, double h) {
+    const double q = Y(x, h) / h;
     ss += q * q;
-  }
+  });
   tm.sum2(ss, dummy);
   s_out = sqrt(ss);
-  for (int64_t i = 1 + r; i < d; i += S) {
-    const double y = Y(i);
+  each([&](int64_t i, double x, double h) {
+    const double y = Y(x, h);
     if (i == 1) {
       if (rsoc) { dst.put(0, (s_out + y) * kRsqrt2); dst.put(1, (s_out - y) * kRsqrt2); }
       else { dst.put(0, s_out); dst.put(1, y); }
     } else {
       dst.put(i, y);
     }
-  }
+  });
 }
 
 // ------------------------------------------------------------------ exponential cone

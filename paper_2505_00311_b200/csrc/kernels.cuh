@@ -292,13 +292,15 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
 }
 
 // All CTAs on one block at a time (giant SOC/RSOC; cooperative launch).
+constexpr size_t kGridSmem = 2 * kGridCache * kThreads * sizeof(double);   // 32 KB
 template <int OP>
 __global__ void __launch_bounds__(kThreads) k_blocks_grid(BlockArgs A, const Ctl* ctl, double* gbuf) {
   if (!block_op_active<OP>(A, ctl)) return;
   __shared__ double sm[2 * (kThreads / 32) + 2];
   Acc<kAcc> acc; acc.zero();
   double kv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  GridTeam tm{sm, gbuf, 0};
+  extern __shared__ double gcache[];        // kGridSmem bytes (launch_blocks_op)
+  GridTeam tm{sm, gbuf, 0, gcache};
   for (int64_t bi = 0; bi < A.nblocks; ++bi) {
     const Block b = A.blocks[bi];
     run_block<false, OP>(tm, A, ctl, b, acc, kv);
@@ -317,7 +319,7 @@ inline cudaError_t launch_blocks_op(int c, int g, BlockArgs B, const Ctl* ctl, d
     case 3: k_blocks_cluster<OP><<<g, kThreads, 0, st>>>(B, ctl); return cudaGetLastError();
     default: {
       void* args[] = {(void*)&B, (void*)&ctl, (void*)&gbuf};
-      return cudaLaunchCooperativeKernel((void*)k_blocks_grid<OP>, dim3(g), dim3(kThreads), args, 0, st);
+      return cudaLaunchCooperativeKernel((void*)k_blocks_grid<OP>, dim3(g), dim3(kThreads), args, kGridSmem, st);
     }
   }
 }
@@ -338,7 +340,7 @@ inline cudaError_t grid_team_occupancy(int* nb) {
   int m = 1 << 20, v = 0;
   cudaError_t e;
 #define PDCS_OCC(OPV) \
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_blocks_grid<OPV>, kThreads, 0)) != cudaSuccess) return e; \
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_blocks_grid<OPV>, kThreads, kGridSmem)) != cudaSuccess) return e; \
   m = v < m ? v : m;
   PDCS_OCC(BOP_TRIAL_PRIMAL) PDCS_OCC(BOP_TRIAL_DUAL) PDCS_OCC(BOP_AVG_PRIMAL) PDCS_OCC(BOP_AVG_DUAL)
   PDCS_OCC(BOP_KKT_ROWS) PDCS_OCC(BOP_KKT_COLS) PDCS_OCC(BOP_PROJECT)

@@ -168,6 +168,18 @@ __device__ __forceinline__ void decide_serial(Ctl& C, const double red[3], int p
 constexpr int64_t kFuseYMax = 2048;
 struct FusedY { int64_t m; const double* yh; const double* y0; double* y; double* ysum; };
 
+// y-side reflected Halpern step and average sum of one row (Alg. 1 line 5-6,
+// PAPER.md:606): y+ = a((1+beta) y^ - beta y) + c y0, ysum += eta y+.  Explicit
+// roundings so k_decide's fused update and k_halpern_y (scalar or vectorised)
+// produce the same bits whatever contraction the compiler would pick.
+__device__ __forceinline__ double halpern_y_row(double a, double b, double c, double eta, double yh,
+                                                double y, double y0, double& ysum) {
+  const double t = __fma_rn(1.0 + b, yh, __dmul_rn(-b, y));
+  const double yn = __fma_rn(a, t, __dmul_rn(c, y0));
+  ysum = __fma_rn(eta, yn, ysum);
+  return yn;
+}
+
 __global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restrict__ part, int64_t nslots,
                                                            Ctl* ctl, unsigned long long h_retry,
                                                            unsigned long long h_check, int prereduced,
@@ -193,9 +205,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restr
   if (fy.m > 0 && sC.status == ST_RUNNING && sC.accepted) {
     const double a = sC.ha, b = sC.hbeta, c = sC.hb, eta = sC.eta_used;
     for (int64_t i = threadIdx.x; i < fy.m; i += blockDim.x) {
-      const double yn = a * ((1.0 + b) * fy.yh[i] - b * fy.y[i]) + c * fy.y0[i];
-      fy.y[i] = yn;
-      fy.ysum[i] += eta * yn;
+      fy.y[i] = halpern_y_row(a, b, c, eta, fy.yh[i], fy.y[i], fy.y0[i], fy.ysum[i]);
     }
   }
   for (int i = threadIdx.x; i < kCtlWords; i += blockDim.x)
@@ -317,10 +327,39 @@ __global__ void __launch_bounds__(kThreads) k_halpern_y(int64_t m, const double*
                                                         double* __restrict__ ysum, const Ctl* ctl) {
   if (ctl->status != ST_RUNNING || !ctl->accepted) return;
   const double a = ctl->ha, b = ctl->hbeta, c = ctl->hb, eta = ctl->eta_used;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-    const double yn = a * ((1.0 + b) * yh[i] - b * y[i]) + c * y0[i];
-    y[i] = yn;
-    ysum[i] += eta * yn;
+  auto upd = [&](double yhi, double yi, double y0i, double& ysi) {
+    return halpern_y_row(a, b, c, eta, yhi, yi, y0i, ysi);
+  };
+  // 16-byte loads, two pairs (4 rows) per thread and step: 8 loads in flight
+  // per thread instead of 4 scalar ones.  The same arithmetic per row, so the
+  // result is bit-identical to the scalar loop and to k_decide's fused update (the buffers are cudaMalloc'd,
+  // 256-B aligned; the odd tail row is done by the first thread).
+  const int64_t np = m >> 1, T = (int64_t)gridDim.x * blockDim.x;
+  const double2* yh2 = reinterpret_cast<const double2*>(yh);
+  const double2* y02 = reinterpret_cast<const double2*>(y0);
+  double2* y2 = reinterpret_cast<double2*>(y);
+  double2* ys2 = reinterpret_cast<double2*>(ysum);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += 2 * T) {
+    const int64_t j = i + T;
+    const bool two = j < np;
+    const double2 h0 = yh2[i], v0 = y2[i], o0 = y02[i];
+    double2 s0 = ys2[i];
+    double2 h1{}, v1{}, o1{}, s1{};
+    if (two) { h1 = yh2[j]; v1 = y2[j]; o1 = y02[j]; s1 = ys2[j]; }
+    double2 n0;
+    n0.x = upd(h0.x, v0.x, o0.x, s0.x);
+    n0.y = upd(h0.y, v0.y, o0.y, s0.y);
+    y2[i] = n0; ys2[i] = s0;
+    if (two) {
+      double2 n1;
+      n1.x = upd(h1.x, v1.x, o1.x, s1.x);
+      n1.y = upd(h1.y, v1.y, o1.y, s1.y);
+      y2[j] = n1; ys2[j] = s1;
+    }
+  }
+  if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t i = m - 1;
+    y[i] = upd(yh[i], y[i], y0[i], ysum[i]);
   }
 }
 

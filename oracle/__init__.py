@@ -100,6 +100,9 @@ def _declare(L):
                                    C.c_double, C.c_double, C.c_double]
     L.orc_primal_weight.argtypes = [C.c_double, C.c_double, C.c_double]
     L.orc_primal_weight.restype = C.c_double
+    L.orc_reflection_beta.argtypes = [C.c_int64, C.c_int64, C.c_double, P_D, C.c_double]
+    L.orc_reflection_beta.restype = C.c_double
+    L.orc_candidate_is_average.argtypes = [C.c_double, C.c_double]
     L.orc_ruiz.argtypes = [C.c_int64, C.c_int64, C.c_int64, P_I64, P_I32, P_D, P_I32, P_I64,
                            C.c_int64, P_I32, P_I64, C.c_int64, C.c_int, C.c_int, P_D, P_D]
     L.orc_set_iterate.argtypes = [C.c_void_p, P_D, P_D]
@@ -227,6 +230,17 @@ def restart_rule(e, e_anchor, e_prev, k, total, suff=0.2, nec=0.8, art=0.36):
 
 def primal_weight(dxn, dyn, omega):
     return lib().orc_primal_weight(dxn, dyn, omega)
+
+
+def reflection_beta(k, W, res, r_start, beta):
+    """One application of the window rule; returns (beta', r_start')."""
+    rs = C.c_double(r_start)
+    b = lib().orc_reflection_beta(k, W, res, C.byref(rs), beta)
+    return b, rs.value
+
+
+def candidate_is_average(e_current, e_average):
+    return bool(lib().orc_candidate_is_average(e_current, e_average))
 
 
 def ruiz(prog, ruiz_iters=10, pc=1):

@@ -377,6 +377,21 @@ static bool restart_rule(double e, double e_anchor, double e_prev, int64_t k, in
   return e <= suff * e_anchor || (e_prev >= 0.0 && e <= nec * e_anchor && e > e_prev) ||
          (double)k >= art * (double)total;
 }
+// AdaptiveReflectionParameter (Alg. 1 line 5, reading A9):
+// non-overlapping windows of W inner iterations within the epoch; res is the
+// fixed-point residual ||z^ - z||_omega of inner iteration k.  The residual of the
+// window's first iteration is remembered; at the window's last iteration beta is
+// halved when the residual there exceeds the remembered one.
+static double reflection_beta(int64_t k, int64_t W, double res, double* r_start, double beta) {
+  if (k % W == 0) *r_start = res;
+  if (k % W == W - 1 && res > *r_start) beta *= 0.5;
+  return beta;
+}
+// GetRestartCandidate (Alg. 1 line 8, reading A14):
+// the candidate with the smaller aggregate Eq. 9 error; a tie goes to the average.
+static bool candidate_is_average(double e_current, double e_average) {
+  return e_average <= e_current;
+}
 // PrimalWeightUpdate (theta = 1/2; reading A12).
 static double primal_weight(double dxn, double dyn, double omega) {
   if (dxn > 1e-10 && dyn > 1e-10) return std::exp(0.5 * std::log(dyn / dxn) + 0.5 * std::log(omega));
@@ -710,10 +725,7 @@ struct Solver {
       if (eta < 1e-12 * eta_init || rejects > prm.ls_max_rejects) { status = ST_NUMERICAL; return false; }
     }
     // AdaptiveReflectionParameter (line 5): window rule (reading A9)
-    double res = std::sqrt(num);
-    int64_t Wn = prm.refl_window;
-    if (k % Wn == 0) r_start = res;
-    if (k % Wn == Wn - 1 && res > r_start) beta *= 0.5;
+    beta = reflection_beta(k, prm.refl_window, std::sqrt(num), &r_start, beta);
     // ReflectedHalpern (line 6, PAPER.md:606 verbatim)
     double a, b;
     halpern_coef(k, &a, &b);
@@ -750,7 +762,7 @@ struct Solver {
     Kkt ka = kkt(xa.data(), ya.data());
     last_cur = kc; last_avg = ka;
     double ec = kmax(kc), ea = kmax(ka);
-    bool use_avg = ea <= ec;           // tie -> average
+    bool use_avg = candidate_is_average(ec, ea);
     trace.push_back(use_avg ? 11 : 10);
     const vector<double>& xc = use_avg ? xa : xh;
     const vector<double>& yc = use_avg ? ya : yh;
@@ -862,6 +874,12 @@ void orc_halpern_coef(int64_t k, double* a, double* b) { halpern_coef(k, a, b); 
 int orc_restart_rule(double e, double ea, double ep, int64_t k, int64_t total, double s, double n,
                      double a) { return restart_rule(e, ea, ep, k, total, s, n, a); }
 double orc_primal_weight(double dxn, double dyn, double omega) { return primal_weight(dxn, dyn, omega); }
+double orc_reflection_beta(int64_t k, int64_t W, double res, double* r_start, double beta) {
+  return reflection_beta(k, W, res, r_start, beta);
+}
+int orc_candidate_is_average(double e_current, double e_average) {
+  return candidate_is_average(e_current, e_average);
+}
 void orc_ruiz(int64_t m, int64_t n, int64_t n1, const int64_t* ptr, const int32_t* col,
               const double* val, const int32_t* pk, const int64_t* pdim, int64_t npc,
               const int32_t* rk, const int64_t* rdim, int64_t nrc, int ruiz_iters, int pc,

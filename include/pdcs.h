@@ -149,6 +149,12 @@ void pdcs_default_params(pdcs_params *p);
  *   p               parameters (NULL: defaults)
  *   device          CUDA device ordinal; cuda_stream a cudaStream_t or NULL
  *   nccl_unique_id  128-byte ncclUniqueId when world > 1, else NULL
+ * Row-sharded contexts (world > 1, or world == 1 with an id) exchange only
+ * all-reduces; every decision of Alg. 1 is taken from
+ * all-reduced values, so all ranks take the same decisions and stop at the
+ * same Eq. 9 check (the time limit is decided collectively).  Their iteration
+ * is recorded into the CUDA graph with the NCCL calls inside
+ * (PDCS_DIST_GRAPH=0: host-driven loop).
  * Errors: ARG, DIM, BOUNDS, NONFINITE, CUDA, NCCL.  *out is NULL on error;
  * the message is then available from pdcs_last_error(NULL). */
 pdcs_status pdcs_create(pdcs_ctx **out, int64_t m_global, int64_t n, int64_t n1,
@@ -168,14 +174,20 @@ pdcs_status pdcs_set_cones(pdcs_ctx *ctx, const int32_t *pk, const int64_t *pdim
 /* Run exactly n_inner ACCEPTED inner iterations of Alg. 1
  * including the Eq. 9 checks, restarts and primal-weight updates at the
  * check cadence; does not stop at tol.  out (may be NULL) receives counters.
- * Errors: STATE, NUMERICAL, CUDA. */
+ * Errors: STATE (also after a pdcs_solve that finished: OPTIMAL, ITERATION_ or
+ * TIME_LIMIT until pdcs_set_tolerance; NUMERICAL_ERROR for good), NUMERICAL,
+ * CUDA, NCCL. */
 pdcs_status pdcs_iterate(pdcs_ctx *ctx, int64_t n_inner, pdcs_result_t *out);
 
 /* Eq. 9 residuals of the selected iterate, ORIGINAL space. */
 pdcs_status pdcs_kkt(pdcs_ctx *ctx, int which, pdcs_kkt_t *out);
 
 /* Alg. 1 until max(err_p, err_d, err_gap) <= tol or a limit; returns the best
- * evaluated point's residuals (reading A15).  Continues from the current state. */
+ * evaluated point's residuals (reading A15).  Continues from the current state.
+ * On a context whose last solve finished (OPTIMAL, ITERATION_ or TIME_LIMIT)
+ * it runs nothing and reports that result again (pdcs_set_tolerance continues
+ * the trajectory).  Errors: STATE (after NUMERICAL_ERROR), CUDA, NCCL; a line-
+ * search failure is reported as status NUMERICAL_ERROR with PDCS_OK. */
 pdcs_status pdcs_solve(pdcs_ctx *ctx, pdcs_result_t *out);
 
 /* Set the stopping tolerance (>= 0) and solve time limit (seconds, 0 = none)
@@ -198,7 +210,11 @@ pdcs_status pdcs_get_iterate(pdcs_ctx *ctx, int which, int space, double *x, dou
  * error reset.  eta, omega and the total / trial / restart counters are kept. */
 pdcs_status pdcs_set_iterate(pdcs_ctx *ctx, const double *x, const double *y);
 
-/* Checkpoint / resume of the full Alg. 1 state in SCALED space:
+/* Checkpoint / resume of the full Alg. 1 state in SCALED space.  These two
+ * calls REPLACE SURVEY §8(b)'s pdcs_set_decision_trace: instead of forcing the
+ * oracle's discrete decisions onto the GPU, the parity tests load the oracle's
+ * exact state every few iterations and compare the decisions both sides then
+ * take (checkpoint shadowing).  The state is:
  *   x, y (current z^{t,k}), x0, y0 (anchor z^{t,0}), xsum, ysum (sum eta z of
  *   the epoch) — n / local-rows doubles each, memory per the create mem_kind;
  *   sc[13] = eta, eta_init, omega, beta, W, r_start, e_anchor, e_prev, best_e,
@@ -291,6 +307,30 @@ void pdcs_proj_destroy(pdcs_proj *plan);
 
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 broadcasts it). */
 pdcs_status pdcs_nccl_unique_id(void *out128);
+
+/* ---- In-process loopback ranks (SURVEY §8(e) tests on one GPU).
+ * A loopback group stands in for NCCL when `world` row-sharded contexts live
+ * in ONE process on one device, each driven from its own host thread (NCCL
+ * refuses two ranks on one device).  Every collective is a host rendezvous of
+ * the group followed by a device reduction over the ranks' buffers in rank
+ * order, so every rank receives identical bits (as with NCCL).  A rank whose
+ * call fails aborts the group: its peers' pending calls fail with
+ * PDCS_ERR_NCCL instead of waiting (PDCS_LOOPBACK_TIMEOUT_S, default 600 s,
+ * bounds a rendezvous).  The group is owned by the caller and must outlive its
+ * contexts.  Loopback contexts run the host-driven loop (no CUDA graph).
+ * Errors: ARG (world outside 1..16). */
+typedef struct pdcs_loopback pdcs_loopback;
+pdcs_status pdcs_loopback_create(pdcs_loopback **out, int world);
+void pdcs_loopback_destroy(pdcs_loopback *group);
+
+/* pdcs_create for rank `rank` of a loopback group (world = the group's size);
+ * every other argument as pdcs_create. */
+pdcs_status pdcs_create_loopback(pdcs_ctx **out, int64_t m_global, int64_t n, int64_t n1,
+                                 int64_t row_begin, int64_t row_end, const int64_t *row_ptr,
+                                 const int32_t *col_idx, const double *vals, const double *c,
+                                 const double *h, const double *l, const double *u,
+                                 const pdcs_params *p, int device, void *cuda_stream, int mem_kind,
+                                 pdcs_loopback *group, int rank);
 
 #ifdef __cplusplus
 }

@@ -8,7 +8,8 @@ from ._lib import (pdcs_default_params, pdcs_create, pdcs_set_cones, pdcs_iterat
                    pdcs_solve, pdcs_get_iterate, pdcs_set_iterate, pdcs_get_scaling,
                    pdcs_kernel_times, pdcs_enable_timing, pdcs_launch_count, pdcs_last_error,
                    pdcs_destroy, pdcs_nccl_unique_id, pdcs_get_scalars, pdcs_get_state, pdcs_set_state, pdcs_tiled_layout_stats, pdcs_proj_create, pdcs_proj_run, pdcs_proj_info,
-                   pdcs_proj_destroy, pdcs_set_tolerance, pdcs_tiled_build_host, PdcsError, LIB_PATH, CURRENT, PDHG_OUT,
+                   pdcs_proj_destroy, pdcs_set_tolerance, pdcs_tiled_build_host, pdcs_loopback_create,
+                   pdcs_loopback_destroy, pdcs_create_loopback, PdcsError, LIB_PATH, CURRENT, PDHG_OUT,
                    ANCHOR, BEST, CANDIDATE, SCALED, ORIGINAL)
 from .solver import PdcsSolver
 
@@ -16,5 +17,6 @@ __all__ = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterate
            "pdcs_solve", "pdcs_get_iterate", "pdcs_set_iterate", "pdcs_get_scaling",
            "pdcs_kernel_times", "pdcs_enable_timing", "pdcs_launch_count", "pdcs_last_error",
            "pdcs_destroy", "pdcs_nccl_unique_id", "pdcs_get_scalars", "pdcs_get_state", "pdcs_set_state", "pdcs_tiled_layout_stats", "pdcs_proj_create", "pdcs_proj_run", "pdcs_proj_info",
-           "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host", "PdcsError", "PdcsSolver", "LIB_PATH",
+           "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host", "pdcs_loopback_create",
+           "pdcs_loopback_destroy", "pdcs_create_loopback", "PdcsError", "PdcsSolver", "LIB_PATH",
            "CURRENT", "PDHG_OUT", "ANCHOR", "BEST", "CANDIDATE", "SCALED", "ORIGINAL"]

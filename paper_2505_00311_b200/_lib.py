@@ -74,6 +74,12 @@ def lib():
                                   C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(pdcs_params), C.c_int,
                                   C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int]
+        L.pdcs_create_loopback.argtypes = [C.POINTER(C.c_void_p), C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                           C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(pdcs_params),
+                                           C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        L.pdcs_loopback_create.argtypes = [C.POINTER(C.c_void_p), C.c_int]
+        L.pdcs_loopback_destroy.argtypes = [C.c_void_p]
         L.pdcs_set_cones.argtypes = [C.c_void_p, P_I32, P_I64, C.c_int64, P_I32, P_I64, C.c_int64]
         L.pdcs_iterate.argtypes = [C.c_void_p, C.c_int64, C.POINTER(pdcs_result_t)]
         L.pdcs_kkt.argtypes = [C.c_void_p, C.c_int, C.POINTER(pdcs_kkt_t)]
@@ -110,7 +116,8 @@ EXPORTED = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterat
             "pdcs_kernel_times", "pdcs_enable_timing", "pdcs_launch_count", "pdcs_last_error",
             "pdcs_destroy", "pdcs_nccl_unique_id", "pdcs_get_scalars", "pdcs_get_state",
             "pdcs_set_state", "pdcs_tiled_layout_stats", "pdcs_proj_create", "pdcs_proj_run",
-            "pdcs_proj_info", "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host"]
+            "pdcs_proj_info", "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host",
+            "pdcs_loopback_create", "pdcs_loopback_destroy", "pdcs_create_loopback"]
 
 STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e_prev", "best_e", "k",
               "total", "trials", "restarts"]
@@ -161,6 +168,29 @@ def pdcs_create(m_global, n, n1, row_begin, row_end, row_ptr, col_idx, vals, c, 
     del keep
     _check(code)
     return ctx
+
+
+def pdcs_create_loopback(m_global, n, n1, row_begin, row_end, row_ptr, col_idx, vals, c, h, l, u,
+                         params=None, device=0, stream=None, mem_kind=MEM_HOST, group=None, rank=0):
+    ctx = C.c_void_p()
+    keep = [row_ptr, col_idx, vals, c, h, l, u]
+    code = lib().pdcs_create_loopback(C.byref(ctx), m_global, n, n1, row_begin, row_end, _ptr(row_ptr),
+                                      _ptr(col_idx), _ptr(vals), _ptr(c), _ptr(h), _ptr(l), _ptr(u),
+                                      C.byref(params) if params is not None else None, device,
+                                      C.c_void_p(stream) if stream else None, mem_kind, group, rank)
+    del keep
+    _check(code)
+    return ctx
+
+
+def pdcs_loopback_create(world: int):
+    g = C.c_void_p()
+    _check(lib().pdcs_loopback_create(C.byref(g), world))
+    return g
+
+
+def pdcs_loopback_destroy(group):
+    lib().pdcs_loopback_destroy(group)
 
 
 def pdcs_set_cones(ctx, pk, pdim, rk, rdim):

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -667,9 +668,9 @@ struct pdcs_ctx {
   DBuf<double> y, yh, y0, ysum, kxh, kxd, ya, kxa, by, candy, res0, res1, onesm;
   DBuf<double> tmpn, tmpm, scal;
   DBuf<double2> xx;                            // interleaved (x^_j, x_j)
-  // row sharding (comm.h): NCCL communicator over the ranks
+  // row sharding (comm.h): NCCL or in-process loopback communicator over the ranks
   bool dist = false;
-  ncclComm_t comm = nullptr;
+  std::unique_ptr<Comm> comm;
   DBuf<double> ktyp;                           // local K~^T y partial before the all-reduce
   // column-tiled copies of K~ (pair gather) and K~^T (y gather), tiled.cuh
   struct TiledDev {
@@ -732,7 +733,6 @@ struct pdcs_ctx {
   ~pdcs_ctx() {
     if (thK.joinable()) thK.join();
     if (thKT.joinable()) thKT.join();
-    if (comm) nccl().CommDestroy(comm);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
     if (cap_st) cudaStreamDestroy(cap_st);
@@ -834,11 +834,28 @@ struct pdcs_ctx {
     CK(cudaStreamSynchronize(st));
   }
   // In-place all-reduce over the row shards (no-op on a single rank).
-  void allreduce(double* buf, size_t count, ncclRedOp_t op) {
+  void allreduce(double* buf, size_t count, RedOp op) {
     if (!dist || count == 0) return;
     ++launches;
-    const ncclResult_t r = nccl().AllReduce(buf, buf, count, ncclFloat64, op, comm, st);
-    if (r != ncclSuccess) fail(PDCS_ERR_NCCL, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
+    const std::string e = comm->allreduce(buf, count, op, st);
+    if (!e.empty()) fail(PDCS_ERR_NCCL, e);
+  }
+  // Time-limit stop, decided collectively so that every rank leaves at the
+  // same Eq. 9 check (a rank-local clock would strand its peers in the next
+  // collective).
+  bool time_up(std::chrono::steady_clock::time_point t0, double limit) {
+    if (!(limit > 0)) return false;
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return allreduce_host(el > limit ? 1.0 : 0.0, RedOp::Max) > 0.0;
+  }
+  // Host scalar all-reduce (setup values, collective stop decisions).
+  double allreduce_host(double v, RedOp op) {
+    if (!dist) return v;
+    CK(cudaMemcpyAsync(scal.p + 7, &v, sizeof(double), cudaMemcpyHostToDevice, st));
+    allreduce(scal.p + 7, 1, op);
+    CK(cudaMemcpyAsync(&v, scal.p + 7, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return v;
   }
 
   // ---------------------------------------------------------------- block kernels
@@ -942,7 +959,7 @@ struct pdcs_ctx {
     run_blocks(false, bargs(false, BOP_TRIAL_DUAL), false, 0);
     if (dist) {
       launch("reduce_trial", [&] { k_reduce_trial<<<1, kDecideThreads, 0, st>>>(tpart.p, nslot_trial, ctl); });
-      allreduce(&ctl->red3[1], 2, ncclSum);     // ||dy||^2 and <dy, K dx> over the row shards
+      allreduce(&ctl->red3[1], 2, RedOp::Sum);     // ||dy||^2 and <dy, K dx> over the row shards
       launch("decide", [&] { k_decide<<<1, kDecideThreads, 0, st>>>(tpart.p, 0, ctl, g_retry, g_check, 1, FusedY{}); });
     } else {
       const FusedY fy = fuse_y() ? FusedY{m, yh.p, y0.p, y.p, ysum.p} : FusedY{};
@@ -970,7 +987,7 @@ struct pdcs_ctx {
       } else {
         spmv_store(KT, y.p, ktyp.p, true);
       }
-      allreduce(ktyp.p, n, ncclSum);
+      allreduce(ktyp.p, n, RedOp::Sum);
       launch("halpern_x", [&] {
         k_halpern_x<<<g_pe, kThreads, 0, st>>>(n, xh.p, x0.p, ktyp.p, x.p, kty.p, xsum.p, ctl);
       });
@@ -1007,8 +1024,8 @@ struct pdcs_ctx {
     if (ncand == 1) zero_cand1_kslots();
     launch("kkt_reduce", [&] { k_kkt_reduce<<<1, kThreads, 0, st>>>(kpart.p, nslot_kkt, ctl); });
     for (int c = 0; c < ncand; ++c) {             // row-side Eq. 9 terms over the shards
-      allreduce(&ctl->kred[10 * c], 3, ncclMax);
-      allreduce(&ctl->kred[10 * c + 3], 2, ncclSum);
+      allreduce(&ctl->kred[10 * c], 3, RedOp::Max);
+      allreduce(&ctl->kred[10 * c + 3], 2, RedOp::Sum);
     }
     launch("kkt_decide", [&] { k_kkt_decide<<<1, 32, 0, st>>>(ncand, mode, hnorm, cnorm, ctl); });
   }
@@ -1026,7 +1043,7 @@ struct pdcs_ctx {
     KktCand c0{xh.p, yh.p, kxh.p, ktyh.p, res0.p, lam0.p};
     KktCand c1{xa.p, ya.p, kxa.p, ktya.p, res1.p, lam1.p};
     spmv_check_KT(yh.p, ktyh.p);    // K^T y^ of the current candidate (K x^ kept by the K pass)
-    allreduce(ktyh.p, n, ncclSum);
+    allreduce(ktyh.p, n, RedOp::Sum);
     if (!van) {
       launch("avg_elem", [&] { k_avg_elem<<<g_pe, kThreads, 0, st>>>(n, ek.p, xsum.p, lt.p, ut.p, xa.p, ctl); });
       BlockArgs A = bargs(true, BOP_AVG_PRIMAL);
@@ -1038,7 +1055,7 @@ struct pdcs_ctx {
       run_blocks(false, B, false, 0);
       spmv_check_K(xa.p, kxa.p);
       spmv_check_KT(ya.p, ktya.p);
-      allreduce(ktya.p, n, ncclSum);
+      allreduce(ktya.p, n, RedOp::Sum);
     }
     kkt_launch(c0, c1, van ? 1 : 2, 1);
     RestartArgs R{};
@@ -1086,6 +1103,8 @@ struct pdcs_ctx {
   // the host-driven loop.
   void build_graph() {
     if (gexec || graph_failed) return;
+    const cudaStream_t saved_st = st;
+    const bool tsave_ = timing;
     try {
       if (!cap_st) CK(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
       if (!cap_st2) CK(cudaStreamCreateWithFlags(&cap_st2, cudaStreamNonBlocking));
@@ -1112,13 +1131,25 @@ struct pdcs_ctx {
       g_retry = g_check = 0;
       CK(cudaGraphInstantiate(&gexec, graph, 0));
     } catch (const CudaErr& e) {
-      graph_failed = true;
-      g_retry = g_check = 0;
-      cudaGetLastError();
-      if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
-      if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
-      err = std::string("graph build failed (host loop used): ") + cudaGetErrorString(e.e) + " at " + e.what;
+      graph_abandon(saved_st, tsave_, std::string(cudaGetErrorString(e.e)) + " at " + e.what);
+    } catch (const StatusErr& e) {                 // e.g. a collective refused under capture
+      graph_abandon(saved_st, tsave_, e.msg);
     }
+  }
+  void graph_abandon(cudaStream_t saved, bool tsave, const std::string& why) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cap_st && cudaStreamIsCapturing(cap_st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+      cudaGraph_t g2 = nullptr;
+      cudaStreamEndCapture(cap_st, &g2);
+    }
+    st = saved;
+    timing = tsave;
+    graph_failed = true;
+    g_retry = g_check = 0;
+    cudaGetLastError();
+    if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+    if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
+    err = "graph build failed (host loop used): " + why;
   }
 
   // dynamic shared memory of the partial kernels, from the matrix's own tile size
@@ -1302,7 +1333,7 @@ struct pdcs_ctx {
   void products(const double* xs, const double* ys, double* kxo, double* ktyo) {
     spmv_store(K, xs, kxo);
     spmv_store(KT, ys, ktyo);
-    allreduce(ktyo, n, ncclSum);
+    allreduce(ktyo, n, RedOp::Sum);
   }
 
   // ---------------------------------------------------------------- setup helpers
@@ -1380,7 +1411,7 @@ struct pdcs_ctx {
 // ============================================================================
 namespace {
 
-pdcs_status guard(pdcs_ctx* ctx, const std::function<void()>& f) {
+pdcs_status guard_impl(pdcs_ctx* ctx, const std::function<void()>& f) {
   try {
     f();
     return PDCS_OK;
@@ -1396,6 +1427,13 @@ pdcs_status guard(pdcs_ctx* ctx, const std::function<void()>& f) {
     if (ctx) ctx->err = e.what(); else g_create_error = e.what();
     return PDCS_ERR_ARG;
   }
+}
+// A failing rank tells its peers (loopback: they leave their rendezvous with an
+// error instead of waiting for a collective this rank will never join).
+pdcs_status guard(pdcs_ctx* ctx, const std::function<void()>& f) {
+  const pdcs_status s = guard_impl(ctx, f);
+  if (s != PDCS_OK && ctx && ctx->comm) ctx->comm->on_error(ctx->err);
+  return s;
 }
 
 template <class T>
@@ -1466,11 +1504,16 @@ const char* pdcs_last_error(const pdcs_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_create_error.c_str();
 }
 
-pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1, int64_t row_begin,
-                        int64_t row_end, const int64_t* row_ptr, const int32_t* col_idx,
-                        const double* vals, const double* c, const double* h, const double* l,
-                        const double* u, const pdcs_params* p, int device, void* cuda_stream,
-                        int mem_kind, const void* nccl_unique_id, int rank, int world) {
+}  // extern "C"
+
+// pdcs_create / pdcs_create_loopback: the communicator is NCCL (nccl_unique_id),
+// an in-process loopback group (loop), or none.
+static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1, int64_t row_begin,
+                               int64_t row_end, const int64_t* row_ptr, const int32_t* col_idx,
+                               const double* vals, const double* c, const double* h, const double* l,
+                               const double* u, const pdcs_params* p, int device, void* cuda_stream,
+                               int mem_kind, const void* nccl_unique_id, LoopbackGroup* loop, int rank,
+                               int world) {
   if (!out) return PDCS_ERR_ARG;
   *out = nullptr;
   pdcs_ctx* ctx = new pdcs_ctx();
@@ -1480,7 +1523,8 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
     if (row_begin < 0 || row_end < row_begin || row_end > m_global) fail(PDCS_ERR_DIM, "bad row range");
     if (mem_kind != PDCS_MEM_HOST && mem_kind != PDCS_MEM_DEVICE) fail(PDCS_ERR_ARG, "bad mem_kind");
     if (world < 1 || rank < 0 || rank >= world) fail(PDCS_ERR_ARG, "bad rank / world");
-    if (world > 1 && !nccl_unique_id) fail(PDCS_ERR_ARG, "world > 1 needs an nccl_unique_id");
+    if (world > 1 && !nccl_unique_id && !loop) fail(PDCS_ERR_ARG, "world > 1 needs an nccl_unique_id");
+    if (loop && (world != loop->world || world > kLoopMaxRanks)) fail(PDCS_ERR_ARG, "world does not match the loopback group");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(PDCS_ERR_CUDA, "no CUDA device");
     if (device < 0 || device >= ndev) fail(PDCS_ERR_ARG, "bad device ordinal");
@@ -1491,13 +1535,18 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
                                               std::to_string(prop.major * 10 + prop.minor));
     ctx->device = device;
     ctx->sms = prop.multiProcessorCount;
-    if (nccl_unique_id) {                          // row-sharded context (also world == 1, for testing)
-      std::string e;
-      if (!nccl().load(e)) fail(PDCS_ERR_NCCL, e);
-      ncclUniqueId id;
-      std::memcpy(&id, nccl_unique_id, sizeof(id));
-      const ncclResult_t r = nccl().CommInitRank(&ctx->comm, world, id, rank);
-      if (r != ncclSuccess) fail(PDCS_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+    if (loop) {                                    // in-process loopback ranks (tests)
+      auto lc = std::make_unique<LoopbackComm>();
+      lc->g = loop;
+      lc->rank = rank;
+      lc->world = world;
+      ctx->comm = std::move(lc);
+      ctx->dist = true;
+    } else if (nccl_unique_id) {                   // row-sharded context (also world == 1, for testing)
+      auto nc = std::make_unique<NcclComm>();
+      const std::string e = nc->init(nccl_unique_id, rank, world);
+      if (!e.empty()) fail(PDCS_ERR_NCCL, e);
+      ctx->comm = std::move(nc);
       ctx->dist = true;
     }
     ctx->st = (cudaStream_t)cuda_stream;
@@ -1654,6 +1703,39 @@ pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1,
   return PDCS_OK;
 }
 
+extern "C" {
+
+pdcs_status pdcs_create(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1, int64_t row_begin,
+                        int64_t row_end, const int64_t* row_ptr, const int32_t* col_idx,
+                        const double* vals, const double* c, const double* h, const double* l,
+                        const double* u, const pdcs_params* p, int device, void* cuda_stream,
+                        int mem_kind, const void* nccl_unique_id, int rank, int world) {
+  return create_impl(out, m_global, n, n1, row_begin, row_end, row_ptr, col_idx, vals, c, h, l, u, p, device,
+                     cuda_stream, mem_kind, nccl_unique_id, nullptr, rank, world);
+}
+
+pdcs_status pdcs_create_loopback(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1, int64_t row_begin,
+                                 int64_t row_end, const int64_t* row_ptr, const int32_t* col_idx,
+                                 const double* vals, const double* c, const double* h, const double* l,
+                                 const double* u, const pdcs_params* p, int device, void* cuda_stream,
+                                 int mem_kind, pdcs_loopback* group, int rank) {
+  if (!group) { g_create_error = "null loopback group"; return PDCS_ERR_ARG; }
+  LoopbackGroup* g = reinterpret_cast<LoopbackGroup*>(group);
+  return create_impl(out, m_global, n, n1, row_begin, row_end, row_ptr, col_idx, vals, c, h, l, u, p, device,
+                     cuda_stream, mem_kind, nullptr, g, rank, g->world);
+}
+
+pdcs_status pdcs_loopback_create(pdcs_loopback** out, int world) {
+  if (!out || world < 1 || world > kLoopMaxRanks) {
+    g_create_error = "loopback world must be 1..16";
+    return PDCS_ERR_ARG;
+  }
+  *out = reinterpret_cast<pdcs_loopback*>(new LoopbackGroup(world));
+  return PDCS_OK;
+}
+
+void pdcs_loopback_destroy(pdcs_loopback* group) { delete reinterpret_cast<LoopbackGroup*>(group); }
+
 pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim, int64_t npc,
                            const int32_t* rkind, const int64_t* rdim, int64_t nrc) {
   if (!ctx) return PDCS_ERR_ARG;
@@ -1799,6 +1881,9 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     ctx->lt.alloc(std::max<int64_t>(n1, 1));
     ctx->ut.alloc(std::max<int64_t>(n1, 1));
     ctx->scal.alloc(8);
+    // ||h||_inf of Eq. 9's err_p denominator over ALL rows (every rank must score
+    // candidates, restarts and termination identically)
+    ctx->hnorm = ctx->allreduce_host(ctx->hnorm, RedOp::Max);
     const int Gm = grid_for(m, ctx->sms), Gn = grid_for(n, ctx->sms);
     k_fill<<<Gm, kThreads, 0, st>>>(m, 1.0, ctx->r.p);
     k_fill<<<Gm, kThreads, 0, st>>>(m, 1.0, ctx->onesm.p);
@@ -1820,7 +1905,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
                                              ctx->tmpm.p);
         k_row_norms<<<Grn, kThreads, 0, st>>>(n, ctx->KT.ptr, ctx->KT.col, ctx->KT.val, ctx->q.p, ctx->r.p,
                                              mode, ctx->tmpn.p);
-        ctx->allreduce(ctx->tmpn.p, n, mode ? ncclSum : ncclMax);   // column norms over all rows
+        ctx->allreduce(ctx->tmpn.p, n, mode ? RedOp::Sum : RedOp::Max);   // column norms over all rows
         k_apply_root<<<Gm, kThreads, 0, st>>>(m, ctx->tmpm.p, ctx->r.p);
         k_apply_root<<<Gn, kThreads, 0, st>>>(n, ctx->tmpn.p, ctx->q.p);
       }
@@ -1867,7 +1952,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
         for (int it = 0; it < 20; ++it) {
           ctx->spmv_store(ctx->K, ctx->tmpn.p, ctx->tmpm.p);
           ctx->spmv_store(ctx->KT, ctx->tmpm.p, ctx->lam0.p);
-          ctx->allreduce(ctx->lam0.p, n, ncclSum);
+          ctx->allreduce(ctx->lam0.p, n, RedOp::Sum);
           k_reduce<<<1, kThreads, 0, st>>>(n, ctx->lam0.p, 1, ctx->scal.p);
           double s2 = 0.0;
           CK(cudaMemcpyAsync(&s2, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1893,8 +1978,8 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
       k_reduce<<<1, kThreads, 0, st>>>(m, ctx->tmpm.p, 2, ctx->scal.p);
       k_reduce<<<1, kThreads, 0, st>>>(n, ctx->ct.p, 0, ctx->scal.p + 1);
       k_reduce<<<1, kThreads, 0, st>>>(m, ctx->ht.p, 0, ctx->scal.p + 2);
-      ctx->allreduce(ctx->scal.p, 1, ncclMax);        // ||K~||_inf over the row shards
-      ctx->allreduce(ctx->scal.p + 2, 1, ncclMax);    // ||h~||_inf
+      ctx->allreduce(ctx->scal.p, 1, RedOp::Max);        // ||K~||_inf over the row shards
+      ctx->allreduce(ctx->scal.p + 2, 1, RedOp::Max);    // ||h~||_inf
       double hs[3];
       CK(cudaMemcpyAsync(hs, ctx->scal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -1961,7 +2046,12 @@ static void finish_result(pdcs_ctx* ctx, pdcs_result_t* out, double secs) {
 // host synchronises only every check_interval launches (to test termination)
 // or at the end.
 static bool run_steps_graph(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, double time_limit) {
-  if (ctx->timing || ctx->dist || std::getenv("PDCS_NO_GRAPH")) return false;
+  if (ctx->timing || std::getenv("PDCS_NO_GRAPH")) return false;
+  // sharded: the collectives are recorded into the graph when the communicator
+  // allows it (NCCL; PDCS_DIST_GRAPH=0 keeps the host loop), else the host loop
+  if (ctx->dist && (!ctx->comm->capturable() ||
+                    (std::getenv("PDCS_DIST_GRAPH") && !std::atoi(std::getenv("PDCS_DIST_GRAPH")))))
+    return false;
   ctx->build_graph();
   if (!ctx->gexec) return false;
   auto t0 = std::chrono::steady_clock::now();
@@ -1978,10 +2068,7 @@ static bool run_steps_graph(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, do
     ctx->read_ctl();
     if (ctx->hctl->status == ST_NUMERICAL) fail(PDCS_ERR_NUMERICAL, "line search failed (eta underflow / too many rejects)");
     if (ctx->hctl->status != ST_RUNNING) break;
-    if (stop_at_tol && time_limit > 0 &&
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > time_limit) {
-      ctx->hctl->status = ST_TIME; ctx->write_ctl(); break;
-    }
+    if (stop_at_tol && ctx->time_up(t0, time_limit)) { ctx->hctl->status = ST_TIME; ctx->write_ctl(); break; }
   }
   const Ctl& C = *ctx->hctl;
   const int64_t trials = C.trials - before.trials, iters = C.total - before.total;
@@ -1993,7 +2080,8 @@ static bool run_steps_graph(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, do
 }
 
 // Host loop of Alg. 1 (the accept flag is read back after each trial); used
-// with per-kernel timing and as the fallback when graphs are unavailable.
+// with per-kernel timing, with a non-capturable communicator (loopback) and as
+// the fallback when graphs are unavailable.
 static void run_steps(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, double time_limit) {
   if (run_steps_graph(ctx, n_inner, stop_at_tol, time_limit)) return;
   auto t0 = std::chrono::steady_clock::now();
@@ -2002,7 +2090,7 @@ static void run_steps(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, double t
       ctx->trial();
       CK(cudaMemcpyAsync(ctx->hctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->st));
       CK(cudaStreamSynchronize(ctx->st));
-      if (ctx->hctl->status != ST_RUNNING) fail(PDCS_ERR_NUMERICAL, "line search failed (eta underflow / too many rejects)");
+      if (ctx->hctl->status == ST_NUMERICAL) fail(PDCS_ERR_NUMERICAL, "line search failed (eta underflow / too many rejects)");
       if (ctx->hctl->accepted) break;
     }
     const bool chk = ctx->hctl->need_check;
@@ -2012,13 +2100,17 @@ static void run_steps(pdcs_ctx* ctx, int64_t n_inner, bool stop_at_tol, double t
       if (stop_at_tol) {
         ctx->read_ctl();
         if (ctx->hctl->done) { ctx->hctl->status = ST_OPTIMAL; ctx->write_ctl(); return; }
-        if (time_limit > 0 &&
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > time_limit) {
-          ctx->hctl->status = ST_TIME; ctx->write_ctl(); return;
-        }
+        if (ctx->time_up(t0, time_limit)) { ctx->hctl->status = ST_TIME; ctx->write_ctl(); return; }
       }
     }
   }
+}
+
+// pdcs_iterate / pdcs_solve on a context whose last solve ended: NUMERICAL_ERROR
+// is final; OPTIMAL / ITERATION_ / TIME_LIMIT need pdcs_set_tolerance first.
+static int finished_status(pdcs_ctx* ctx) {
+  ctx->read_ctl();
+  return ctx->hctl->status;
 }
 
 pdcs_status pdcs_iterate(pdcs_ctx* ctx, int64_t n_inner, pdcs_result_t* out) {
@@ -2026,6 +2118,9 @@ pdcs_status pdcs_iterate(pdcs_ctx* ctx, int64_t n_inner, pdcs_result_t* out) {
   return guard(ctx, [&] {
     if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
     if (n_inner < 0) fail(PDCS_ERR_ARG, "n_inner < 0");
+    const int fs = finished_status(ctx);
+    if (fs == ST_NUMERICAL) fail(PDCS_ERR_STATE, "solver is in NUMERICAL_ERROR");
+    if (fs != ST_RUNNING) fail(PDCS_ERR_STATE, "the last pdcs_solve finished; pdcs_set_tolerance continues it");
     ctx->launches = 0;
     auto t0 = std::chrono::steady_clock::now();
     run_steps(ctx, n_inner, false, 0.0);
@@ -2041,6 +2136,12 @@ pdcs_status pdcs_solve(pdcs_ctx* ctx, pdcs_result_t* out) {
     if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
     auto t0 = std::chrono::steady_clock::now();
     ctx->launches = 0;
+    const int fs = finished_status(ctx);
+    if (fs == ST_NUMERICAL) fail(PDCS_ERR_STATE, "solver is in NUMERICAL_ERROR");
+    if (fs != ST_RUNNING) {                        // already finished: report it again
+      finish_result(ctx, out, 0.0);
+      return;
+    }
     const int64_t remaining = std::max<int64_t>(0, ctx->prm.max_iters - ctx->hctl->total);
     try {
       run_steps(ctx, remaining, true, ctx->prm.time_limit_s);

@@ -17,10 +17,11 @@ class PdcsSolver:
     """create -> set_cones on construction; iterate / solve / kkt / get_iterate after."""
 
     def __init__(self, prog, device: int = 0, stream=None, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None, rows=None, **params):
+                 nccl_id: bytes | None = None, rows=None, loopback=None, **params):
         """rows=(row_begin, row_end) selects this rank's shard (dist.partition_rows);
         nccl_id (128 bytes from pdcs_nccl_unique_id on rank 0) enables the
-        NCCL path (also usable with world == 1)."""
+        NCCL path (also usable with world == 1); loopback (a group from
+        pdcs_loopback_create) makes this rank one of N in-process ranks."""
         from . import dist
         self.prog = prog
         self.params = L.pdcs_default_params(**params)
@@ -36,9 +37,14 @@ class PdcsSolver:
         idbuf = None
         if nccl_id is not None:
             idbuf = np.frombuffer(bytes(nccl_id), dtype=np.uint8).copy()
-        self.ctx = L.pdcs_create(prog.m, prog.n, prog.n1, r0, r1, a["row_ptr"], a["col"], a["val"],
-                                 a["c"], a["h"], a["l"], a["u"], self.params, device, stream,
-                                 nccl_unique_id=idbuf, rank=rank, world=world)
+        if loopback is not None:           # in-process loopback group (pdcs_loopback_create)
+            self.ctx = L.pdcs_create_loopback(prog.m, prog.n, prog.n1, r0, r1, a["row_ptr"], a["col"],
+                                              a["val"], a["c"], a["h"], a["l"], a["u"], self.params, device,
+                                              stream, group=loopback, rank=rank)
+        else:
+            self.ctx = L.pdcs_create(prog.m, prog.n, prog.n1, r0, r1, a["row_ptr"], a["col"], a["val"],
+                                     a["c"], a["h"], a["l"], a["u"], self.params, device, stream,
+                                     nccl_unique_id=idbuf, rank=rank, world=world)
         L.pdcs_set_cones(self.ctx, prog.pk, prog.pdim, prog.rk, prog.rdim)
 
     def close(self):

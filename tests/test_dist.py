@@ -114,3 +114,25 @@ def test_nccl_path_single_rank_matches_local(tiled, monkeypatch):
     d = max(np.abs(x1 - x0).max() / (1 + np.abs(x0).max()), np.abs(y1 - y0).max() / (1 + np.abs(y0).max()))
     assert d <= 1e-12, d
     assert g1.scalars()["restarts"] == g0.scalars()["restarts"]
+
+
+@pytest.mark.gpu
+def test_nccl_graph_path_bit_identical_to_host_loop(monkeypatch):
+    """The row-sharded iteration recorded into the CUDA graph with the NCCL
+    all-reduces inside (the default) gives the same bits as the host-driven
+    loop (PDCS_DIST_GRAPH=0), and the graph really is used."""
+    import torch  # noqa: F401
+    import paper_2505_00311_b200 as P
+    prog = gen_mixed(400, 60, 200, seed=12, soc_dims=(3, 60))
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("PDCS_DIST_GRAPH", mode)
+        g = P.PdcsSolver(prog, nccl_id=P.pdcs_nccl_unique_id(), rank=0, world=1)
+        g.iterate(200)
+        out[mode] = (g.get_iterate(P.CURRENT), g.scalars(), P.pdcs_last_error(g.ctx))
+        g.close()
+    (xa, ya), sa, ea = out["1"]
+    (xb, yb), sb, _ = out["0"]
+    assert "graph build failed" not in ea, ea
+    assert np.array_equal(xa, xb) and np.array_equal(ya, yb)
+    assert sa["trials"] == sb["trials"] and sa["restarts"] == sb["restarts"]

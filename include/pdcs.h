@@ -46,7 +46,7 @@ typedef enum {
   PDCS_ERR_BOUNDS = 3,    /* l_i > u_i, or NaN bound */
   PDCS_ERR_NONFINITE = 4, /* non-finite matrix entry, c or h */
   PDCS_ERR_CONE = 5,      /* bad cone kind/dim, dims do not sum to n2 / m */
-  PDCS_ERR_SHARD = 6,     /* a row cone straddles this rank's row range */
+  PDCS_ERR_SHARD = 6,     /* a SOC/RSOC/exp row cone straddles this rank's row range (Zero / NonNeg runs may be cut) */
   PDCS_ERR_CUDA = 7,      /* CUDA runtime error (incl. no sm_100 device) */
   PDCS_ERR_NCCL = 8,      /* NCCL error */
   PDCS_ERR_NUMERICAL = 9, /* eta underflow, > ls_max_rejects line-search rejects */

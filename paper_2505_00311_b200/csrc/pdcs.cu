@@ -1779,9 +1779,11 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
       if (!dim_ok(rkind[b], rdim[b])) fail(PDCS_ERR_CONE, "bad row cone " + std::to_string(b));
       const int64_t lo = off - ctx->row_begin, hi = lo + rdim[b];
       if (hi > 0 && lo < m) {
-        if (lo < 0 || hi > m) fail(PDCS_ERR_SHARD, "row cone " + std::to_string(b) + " straddles the rank's rows");
         const uint8_t e = rkind[b] == C_ZERO ? EK_FREE : rkind[b] == C_NONNEG ? EK_NONNEG : EK_BLOCK;
-        for (int64_t i = lo; i < hi; ++i) rk[i] = e;
+        // Zero / NonNeg rows are elementwise and may be cut by a shard; a cone block may not
+        if (e == EK_BLOCK && (lo < 0 || hi > m))
+          fail(PDCS_ERR_SHARD, "row cone " + std::to_string(b) + " straddles the rank's rows");
+        for (int64_t i = std::max<int64_t>(lo, 0); i < std::min<int64_t>(hi, m); ++i) rk[i] = e;
         if (e == EK_BLOCK) rb.push_back(Block{lo, rkind[b], (int32_t)rdim[b]});
         if (rkind[b] == C_RSOC) rrs.push_back(lo);
       }

@@ -98,6 +98,8 @@ DATA = {
     "fisher": "synthetic (seeded Philox, PAPER.md:1618-1623 recipe at BASELINE configs[2] size)",
     "mpo": "synthetic (seeded Philox, PAPER.md:1694-1705 with synthetic covariances, reading A24, BASELINE configs[3])",
     "mixed": "synthetic (seeded Philox, SURVEY 8(d) cfg 5 planted mixed-cone recipe, one GPU's 1/8 share of BASELINE configs[4])",
+    "mixed_full": "synthetic (seeded Philox streams per row chunk, SURVEY 8(d) cfg 5 planted mixed-cone recipe at "
+                  "BASELINE configs[4]'s size, generated rank-locally)",
 }
 
 
@@ -108,11 +110,29 @@ def build_instance(config, seed):
     return prog, time.perf_counter() - t
 
 
+def build_shard(args, rank, world, allreduce):
+    """configs[4] at its stated size (--config mixed_full, --scale 1.0: m 2e7,
+    n 1e7, nnz 2e9), generated rank-locally: every rank draws only its rows
+    (instances.gen_mixed_shard); c's G^T y* partials are all-reduced."""
+    from instances import mixed_full_layout, gen_mixed_shard
+    from paper_2505_00311_b200 import dist as D
+    t = time.perf_counter()
+    L = mixed_full_layout(args.scale, args.seed)
+    rows = D.partition_rows(L.row_ptr, L.rk, L.rdim, world)[rank]
+    prog = gen_mixed_shard(L, rows, allreduce=allreduce)
+    prog.nnz_total = int(L.row_ptr[-1])
+    return prog, rows, time.perf_counter() - t
+
+
+def local_rows(prog):
+    return prog.rows[1] - prog.rows[0] if hasattr(prog, "rows") else prog.m
+
+
 def spmv_alg_bytes(prog):
     """Algorithmic bytes of the two fused SpMV kernels per launch:
     matrix (8 B value + 4 B column id per nnz) + row pointers (4 B per row) + the
     gathered vector once + the row-indexed epilogue vectors."""
-    nnz, m, n = prog.nnz, prog.m, prog.n
+    nnz, m, n = prog.nnz, local_rows(prog), prog.n
     # K sweep: (x^_j, x_j) pairs gathered once (16 n); y, h~ in, K x^, y^ out (32 m); kind byte (m)
     k_dual = 12 * nnz + 4 * (m + 1) + 16 * n + 32 * m + m
     # K^T sweep: y+ gathered once (8 m); x^, x, x0, xsum in, x, K^T y, xsum out (56 n)
@@ -133,7 +153,7 @@ def elem_alg_bytes(prog):
     l, u = np.asarray(prog.l), np.asarray(prog.u)
     lo0 = (l == 0.0) & ~np.isfinite(u)
     bounds = 8 * int((np.isfinite(l) & ~lo0).sum() + np.isfinite(u).sum())
-    return {"primal_elem": 49 * n_elem + bounds, "halpern_y": 48 * prog.m}
+    return {"primal_elem": 49 * n_elem + bounds, "halpern_y": 48 * local_rows(prog)}
 
 
 # kernels that run only inside the Eq. 9 check (every check_interval iterations);
@@ -148,7 +168,7 @@ def round_up(k, q):
 
 def iter_alg_bytes(prog):
     """SURVEY §8(d) B_iter = [12 nnz + 4(m+1)] + [12 nnz + 4(n+1)] + 8*14*(m+n)."""
-    nnz, m, n = prog.nnz, prog.m, prog.n
+    nnz, m, n = prog.nnz, local_rows(prog), prog.n
     return 12 * nnz + 4 * (m + 1) + 12 * nnz + 4 * (n + 1) + 8 * 14 * (m + n)
 
 
@@ -175,8 +195,19 @@ def make_ctx(P, prog, host, params, stream, device, rows, uid=None, rank=0, worl
 
 def cpu_baseline(prog, budget_s=20.0):
     """Oracle (single-threaded C++, as it stands) on the same instance: timed
-    accepted iterations after one warm-up iteration; setup excluded."""
+    accepted iterations after one warm-up iteration; setup excluded.  For
+    configs[4] at full size (2e9 nnz) the oracle runs the same recipe at 1/64
+    scale and its it/s is extrapolated per nonzero (SURVEY §8(d) cfg 5)."""
     import oracle as O
+    if getattr(prog, "nnz_total", None):
+        from instances import mixed_full_layout, gen_mixed_shard
+        L = mixed_full_layout(1.0 / 64, 0)
+        small = gen_mixed_shard(L, (0, L.m))
+        r = cpu_baseline(small, budget_s)
+        f = small.nnz / prog.nnz_total
+        r["value"] *= f
+        r["sample"] += f"; it/s extrapolated to the full instance per nonzero (x {f:.5f})"
+        return r
     t = time.perf_counter()
     S = O.OracleSolver(prog)
     setup = time.perf_counter() - t
@@ -216,7 +247,14 @@ def run_reference(args):
         if rank != 0:
             dist.barrier()
             return
-    prog, gen_s = build_instance(args.config, args.seed)
+    extrap = 1.0
+    if args.config == "mixed_full":         # the oracle on the 1/64-scale recipe, per-nnz extrapolation
+        from instances import mixed_full_layout, gen_mixed_shard
+        L = mixed_full_layout(args.scale / 64, args.seed)
+        prog, gen_s = gen_mixed_shard(L, (0, L.m)), 0.0
+        extrap = prog.nnz / float(mixed_full_layout(args.scale, args.seed).row_ptr[-1])
+    else:
+        prog, gen_s = build_instance(args.config, args.seed)
     import oracle as O
     t = time.perf_counter()
     S = O.OracleSolver(prog)
@@ -231,7 +269,7 @@ def run_reference(args):
         if time.perf_counter() - t0 > budget:
             break
     el = time.perf_counter() - t0
-    v = done / el
+    v = done / el * extrap
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / done,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -239,7 +277,9 @@ def run_reference(args):
             "cpu_baseline": {"value": v, "unit": "iter/s", "kind": "oracle", "cores": 1,
                              "sample": f"{done} of {args.steps} requested accepted iterations of the full "
                                        f"{prog.name} instance (time-capped at {budget:.0f}s) after "
-                                       f"{min(max(args.warmup, 0), 2)} warm-up; setup {setup:.1f}s excluded"},
+                                       f"{min(max(args.warmup, 0), 2)} warm-up; setup {setup:.1f}s excluded"
+                                       + (f"; 1/64-scale recipe, it/s x {extrap:.5f} per nonzero"
+                                          if extrap != 1.0 else "")},
             "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -248,7 +288,8 @@ def run_reference(args):
 
 
 def _config(prog, args):
-    return {"workload": args.config, "instance": prog.name, "m": prog.m, "n": prog.n, "nnz": prog.nnz,
+    return {"workload": args.config, "instance": prog.name, "m": prog.m, "n": prog.n,
+            "nnz": getattr(prog, "nnz_total", None) or prog.nnz, "nnz_this_rank": prog.nnz,
             "cones": {"primal": [int(k) for k in np.unique(prog.pk)], "rows": [int(k) for k in np.unique(prog.rk)]},
             "l2": "inputs larger than L2 (matrix %.2f GB > 126 MB)" % (24 * prog.nnz / 1e9),
             "parallelism": f"rows-sharded-x{args.gpus} (NCCL all-reduce, replicated primal)" if args.gpus > 1
@@ -263,6 +304,7 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--config", default="lasso")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--scale", type=float, default=1.0, help="mixed_full: fraction of configs[4]'s size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tol-run", action="store_true")
     ap.add_argument("--tol-time-limit", type=float, default=120.0)
@@ -280,9 +322,18 @@ def main():
     build.build()
     import paper_2505_00311_b200 as P
 
-    prog, gen_s = build_instance(args.config, args.seed)
     from paper_2505_00311_b200 import dist as D
-    rows = D.partition_rows(prog.row_ptr, prog.rk, prog.rdim, world)[rank]
+    if args.config == "mixed_full":
+        def allreduce(a):
+            if world == 1:
+                return a
+            t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+            torch.distributed.all_reduce(t)
+            return t.cpu().numpy()
+        prog, rows, gen_s = build_shard(args, rank, world, allreduce)
+    else:
+        prog, gen_s = build_instance(args.config, args.seed)
+        rows = D.partition_rows(prog.row_ptr, prog.rk, prog.rdim, world)[rank]
     uid = None
     if world > 1:
         # rank 0 creates the ncclUniqueId, torch.distributed broadcasts it

@@ -4,7 +4,8 @@ Shared by the CPU oracle (tests, cpu baseline) and the CUDA path (tests, bench).
 """
 from .program import (ConicProgram, ZERO, NONNEG, SOC, RSOC, EXP, DUAL_EXP,
                       KIND_NAMES, csr_from_coo)
-from .generators import gen_lasso, gen_fisher, gen_mpo, gen_mixed, gen_mixed_large, bernoulli_positions
+from .generators import (gen_lasso, gen_fisher, gen_mpo, gen_mixed, gen_mixed_large, bernoulli_positions,
+                         mixed_full_layout, gen_mixed_shard, MixedLayout, ShardedProgram)
 
 # BASELINE.json configs (index -> builder).  configs[0] is the oracle-sized case.
 CONFIGS = {
@@ -18,4 +19,5 @@ CONFIGS = {
 
 __all__ = ["ConicProgram", "ZERO", "NONNEG", "SOC", "RSOC", "EXP", "DUAL_EXP",
            "KIND_NAMES", "csr_from_coo", "gen_lasso", "gen_fisher", "gen_mpo",
-           "gen_mixed", "gen_mixed_large", "bernoulli_positions", "CONFIGS"]
+           "gen_mixed", "gen_mixed_large", "bernoulli_positions", "CONFIGS",
+           "mixed_full_layout", "gen_mixed_shard", "MixedLayout", "ShardedProgram"]

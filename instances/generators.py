@@ -13,6 +13,7 @@ from ``numpy.random.Generator(Philox(seed))``.  Recipes:
 """
 from __future__ import annotations
 
+import dataclasses
 import math
 
 import numpy as np
@@ -642,3 +643,193 @@ def gen_mixed_large(scale: float = 0.125, seed: int = 0) -> ConicProgram:
     prog.x_star, prog.y_star = x_star, y_star
     prog.obj_star = float(prog.c @ x_star)
     return prog
+
+
+# --------------------------------------------------------------------------
+# configs[4] at its stated size, generated rank-locally (SURVEY §8(d) cfg 5, §8(e))
+# --------------------------------------------------------------------------
+_CHUNK_ROWS = 1 << 16        # rows per matrix chunk (one RNG stream each)
+_BLOCK_GROUP = 4096          # row-cone blocks per planted-pair group (one RNG stream each)
+
+
+def _stream(seed: int, tag: int, idx: int) -> np.random.Generator:
+    """Independent Philox stream per (seed, tag, idx): a chunk's data does not
+    depend on which rank draws it or on the number of ranks."""
+    return np.random.Generator(np.random.Philox(np.random.SeedSequence([seed, tag, idx])))
+
+
+@dataclasses.dataclass
+class MixedLayout:
+    """The cheap global part of cfg 5 (O(m + n) numbers): row lengths, column
+    factors, cone lists, the planted primal pair.  Identical on every rank."""
+    scale: float
+    seed: int
+    m: int
+    n: int
+    n1: int
+    row_ptr: np.ndarray
+    cf: np.ndarray
+    rk: np.ndarray
+    rdim: np.ndarray
+    pk: np.ndarray
+    pdim: np.ndarray
+    l: np.ndarray
+    u: np.ndarray
+    x_star: np.ndarray
+    lam: np.ndarray
+
+
+@dataclasses.dataclass
+class ShardedProgram:
+    """Rows [rows[0], rows[1]) of a conic program whose other data is global:
+    m is the GLOBAL row count; row_ptr (rebased to 0), col_idx, vals, h and
+    y_star are this rank's rows only."""
+    m: int
+    n: int
+    n1: int
+    rows: tuple
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    vals: np.ndarray
+    c: np.ndarray
+    h: np.ndarray
+    l: np.ndarray
+    u: np.ndarray
+    pk: np.ndarray
+    pdim: np.ndarray
+    rk: np.ndarray
+    rdim: np.ndarray
+    name: str = "shard"
+    x_star: np.ndarray | None = None
+    y_star: np.ndarray | None = None
+    obj_star: float | None = None
+
+    @property
+    def nnz(self) -> int:             # this rank's nonzeros
+        return int(self.row_ptr[-1])
+
+    @property
+    def n2(self) -> int:
+        return self.n - self.n1
+
+
+def mixed_full_layout(scale: float = 1.0, seed: int = 0) -> MixedLayout:
+    """Global part of SURVEY §8(d) cfg 5 at `scale` (1.0: m = 2e7, n = 1e7,
+    nnz ~ 2e9), same recipe as gen_mixed_large (row lengths U{20..180}, column
+    factors 10^U[-2,2], row cones 30/30/25/5/7.5/2.5 % with 4 giant SOC blocks,
+    columns 40 % box, 60 % cones), drawn from stream (seed, 0, 0)."""
+    rng = _stream(seed, 0, 0)
+    m = int(round(2e7 * scale)); n = int(round(1e7 * scale))
+    n1 = int(round(0.4 * n)); n2 = n - n1
+    lens = np.minimum(rng.integers(20, 181, size=m).astype(np.int64), n)
+    row_ptr = np.zeros(m + 1, np.int64)
+    np.cumsum(lens, out=row_ptr[1:])
+    cf = 10.0 ** rng.uniform(-2.0, 2.0, n)
+    giant = tuple([max(3, int(2.5e5 * scale))] * 4)
+    rk, rdim = _mixed_cones(rng, m, {ZERO: .30, NONNEG: .30, SOC: .25, RSOC: .05, EXP: .075, DUAL_EXP: .025},
+                            giant=giant)
+    pk, pdim = _mixed_cones(rng, n2, {ZERO: .01, NONNEG: .20, SOC: .40, RSOC: .15, EXP: .20, DUAL_EXP: .04})
+    btype = rng.integers(0, 4, size=n1)
+    lo = rng.uniform(-1.0, 0.0, n1)
+    hi = rng.uniform(0.0, 1.0, n1) + lo + 0.5
+    l = np.where((btype == 1) | (btype == 3), lo, -INF)
+    u = np.where((btype == 2) | (btype == 3), hi, INF)
+    status = rng.integers(0, 3, size=n1)
+    fl, fu = np.isfinite(l), np.isfinite(u)
+    atl = (status == 1) & fl
+    atu = (status == 2) & fu & ~atl
+    inter = ~(atl | atu)
+    lz, uz = np.where(fl, l, 0.0), np.where(fu, u, 0.0)
+    x1 = np.where(fl & fu, rng.uniform(0.0, 1.0, n1) * (uz - lz) + lz,
+                  np.where(fl, lz + rng.uniform(0.0, 1.0, n1),
+                           np.where(fu, uz - rng.uniform(0.0, 1.0, n1), rng.standard_normal(n1))))
+    x1 = np.where(atl, l, np.where(atu, u, x1))
+    lam1 = np.where(atl, rng.uniform(0.0, 1.0, n1), np.where(atu, -rng.uniform(0.0, 1.0, n1), 0.0))
+    lam1[inter] = 0.0
+    x2, lam2 = _planted_pairs(rng, pk, pdim)
+    return MixedLayout(scale, seed, m, n, n1, row_ptr, cf, rk, rdim, pk, pdim, l, u,
+                       np.concatenate([x1, x2]), np.concatenate([lam1, lam2]))
+
+
+def _mixed_chunk(L: MixedLayout, c: int):
+    """Rows [c R, (c+1) R) of G: distinct uniform columns per row, values
+    N(0,1) * rowfactor * colfactor; stream (seed, 1, c)."""
+    rng = _stream(L.seed, 1, c)
+    a, b = c * _CHUNK_ROWS, min((c + 1) * _CHUNK_ROWS, L.m)
+    lens = np.diff(L.row_ptr[a:b + 1])
+    nnz = int(lens.sum())
+    rows = np.repeat(np.arange(b - a, dtype=np.int64), lens)
+    key = rows * L.n + rng.integers(0, L.n, nnz)
+    while True:
+        key.sort()
+        dup = np.nonzero(key[1:] == key[:-1])[0] + 1
+        if dup.size == 0:
+            break
+        key[dup] = (key[dup] // L.n) * L.n + rng.integers(0, L.n, dup.size)
+    col = (key % L.n).astype(np.int32)
+    rf = 10.0 ** rng.uniform(-2.0, 2.0, b - a)
+    val = rng.standard_normal(nnz) * rf[rows] * L.cf[col]
+    return col, val
+
+
+def _mixed_row_pairs(L: MixedLayout, a: int, b: int):
+    """Planted (s*, y*) of rows [a, b): whole groups of _BLOCK_GROUP row-cone
+    blocks, stream (seed, 2, group), cut to the rows."""
+    starts = np.concatenate([[0], np.cumsum(L.rdim)]).astype(np.int64)
+    b0 = int(np.searchsorted(starts, a, side="right")) - 1
+    b1 = int(np.searchsorted(starts, b, side="left"))
+    s = np.empty(b - a); y = np.empty(b - a)
+    for g in range(b0 // _BLOCK_GROUP, (max(b1, b0 + 1) - 1) // _BLOCK_GROUP + 1):
+        g0, g1 = g * _BLOCK_GROUP, min((g + 1) * _BLOCK_GROUP, len(L.rdim))
+        sg, yg = _planted_pairs(_stream(L.seed, 2, g), L.rk[g0:g1], L.rdim[g0:g1])
+        lo, hi = max(a, int(starts[g0])), min(b, int(starts[g1]))
+        if hi > lo:
+            s[lo - a:hi - a] = sg[lo - starts[g0]:hi - starts[g0]]
+            y[lo - a:hi - a] = yg[lo - starts[g0]:hi - starts[g0]]
+    return s, y
+
+
+def gen_mixed_shard(L: MixedLayout, rows, allreduce=None, threads=None) -> ShardedProgram:
+    """This rank's rows of cfg 5: its chunks of G, its rows of the planted
+    (s*, y*), h = G x* - s* on its rows, and c = G^T y* + lam* where the
+    G^T y* partials of all ranks are summed by `allreduce` (None: one rank).
+    No process ever holds more than its own rows of G.  Chunks are drawn on
+    `threads` host threads (their streams are independent); the G^T y*
+    partial is summed chunk by chunk in chunk order (deterministic)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    a, b = int(rows[0]), int(rows[1])
+    rp = L.row_ptr
+    nnz = int(rp[b] - rp[a])
+    col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float64)
+    h = np.empty(b - a)
+    s_star, y_star = _mixed_row_pairs(L, a, b)
+
+    def work(c):
+        ca, cb = c * _CHUNK_ROWS, min((c + 1) * _CHUNK_ROWS, L.m)
+        lo, hi = max(a, ca), min(b, cb)
+        if hi <= lo:
+            return None
+        cc, cv = _mixed_chunk(L, c)
+        src = slice(int(rp[lo] - rp[ca]), int(rp[hi] - rp[ca]))
+        dst = slice(int(rp[lo] - rp[a]), int(rp[hi] - rp[a]))
+        col[dst] = cc[src]; val[dst] = cv[src]
+        lr = np.repeat(np.arange(hi - lo, dtype=np.int64), np.diff(rp[lo:hi + 1]))
+        h[lo - a:hi - a] = np.bincount(lr, weights=val[dst] * L.x_star[col[dst]], minlength=hi - lo) \
+            - s_star[lo - a:hi - a]
+        return np.bincount(col[dst], weights=val[dst] * y_star[lo - a + lr], minlength=L.n)
+
+    cpart = np.zeros(L.n)
+    chunks = range(a // _CHUNK_ROWS, (max(b, a + 1) - 1) // _CHUNK_ROWS + 1)
+    with ThreadPoolExecutor(threads or min(16, os.cpu_count() or 1)) as ex:
+        for cp in ex.map(work, chunks):
+            if cp is not None:
+                cpart += cp
+    if allreduce is not None:
+        cpart = allreduce(cpart)
+    c = cpart + L.lam
+    name = f"mixed_full_scale{L.scale:g}_s{L.seed}"
+    return ShardedProgram(m=L.m, n=L.n, n1=L.n1, rows=(a, b), row_ptr=rp[a:b + 1] - rp[a], col_idx=col,
+                          vals=val, c=c, h=h, l=L.l, u=L.u, pk=L.pk, pdim=L.pdim, rk=L.rk, rdim=L.rdim,
+                          name=name, x_star=L.x_star, y_star=y_star, obj_star=float(c @ L.x_star))

@@ -50,7 +50,14 @@ def partition_rows(row_ptr, rk, rdim, world: int):
 
 
 def shard(prog, row_begin: int, row_end: int):
-    """Local CSR (row pointers rebased to 0) and h of rows [row_begin, row_end)."""
+    """Local CSR (row pointers rebased to 0) and h of rows [row_begin, row_end).
+    A program generated rank-locally (instances.ShardedProgram, .rows) already
+    holds exactly its rows."""
+    if hasattr(prog, "rows"):
+        if tuple(prog.rows) != (row_begin, row_end):
+            raise ValueError(f"shard {prog.rows} holds other rows than [{row_begin}, {row_end})")
+        return dict(row_ptr=np.ascontiguousarray(prog.row_ptr, np.int64), col=prog.col_idx, val=prog.vals,
+                    h=np.ascontiguousarray(prog.h))
     rp = np.asarray(prog.row_ptr, np.int64)
     a, b = int(rp[row_begin]), int(rp[row_end])
     return dict(row_ptr=np.ascontiguousarray(rp[row_begin:row_end + 1] - a),

@@ -25,7 +25,7 @@ class PdcsSolver:
         from . import dist
         self.prog = prog
         self.params = L.pdcs_default_params(**params)
-        r0, r1 = rows if rows is not None else (0, prog.m)
+        r0, r1 = rows if rows is not None else getattr(prog, "rows", (0, prog.m))
         self.rows = (r0, r1)
         sh = dist.shard(prog, r0, r1)
         self._arrays = dict(

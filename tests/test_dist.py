@@ -136,3 +136,64 @@ def test_nccl_graph_path_bit_identical_to_host_loop(monkeypatch):
     assert "graph build failed" not in ea, ea
     assert np.array_equal(xa, xb) and np.array_equal(ya, yb)
     assert sa["trials"] == sb["trials"] and sa["restarts"] == sb["restarts"]
+
+
+def _shard_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    from instances import mixed_full_layout, gen_mixed_shard
+
+    def allreduce(a):
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        dist.all_reduce(t)
+        return t.numpy()
+
+    L = mixed_full_layout(5e-4, seed=3)
+    parts = D.partition_rows(L.row_ptr, L.rk, L.rdim, world)
+    sh = gen_mixed_shard(L, parts[rank], allreduce=allreduce)
+    got = [None] * world
+    dist.all_gather_object(got, (sh.rows, sh.row_ptr, sh.col_idx, sh.vals, sh.h, sh.y_star, sh.c))
+    q.put((rank, got if rank == 0 else None, sh.nnz))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_rank_local_mixed_generator(world):
+    """BASELINE configs[4] generated rank-locally (instances.gen_mixed_shard):
+    each rank draws only its rows; c = G^T y* + lam* from an all-reduce of the
+    ranks' partials.  The assembled shards are the single-process instance
+    (G and h bitwise, c to rounding) and the planted pair is optimal: Eq. 9 at
+    (x*, y*) <= 1e-13 through the oracle, objective = c^T x*."""
+    from instances import ConicProgram, mixed_full_layout, gen_mixed_shard
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    got = res[0][1]
+    L = mixed_full_layout(5e-4, seed=3)
+    one = gen_mixed_shard(L, (0, L.m))
+    rows = [g[0] for g in got]
+    assert rows[0][0] == 0 and rows[-1][1] == L.m and all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+    col = np.concatenate([g[2] for g in got])
+    val = np.concatenate([g[3] for g in got])
+    h = np.concatenate([g[4] for g in got])
+    ys = np.concatenate([g[5] for g in got])
+    rp = np.concatenate([[0]] + [g[1][1:] + off for g, off in
+                                 zip(got, np.cumsum([0] + [int(g[1][-1]) for g in got[:-1]]))])
+    assert np.array_equal(rp, one.row_ptr) and np.array_equal(col, one.col_idx)
+    assert np.array_equal(val, one.vals) and np.array_equal(h, one.h) and np.array_equal(ys, one.y_star)
+    c = got[0][6]
+    assert all(np.array_equal(g[6], c) for g in got)                   # every rank holds the same c
+    np.testing.assert_allclose(c, one.c, rtol=1e-13, atol=1e-13 * np.abs(one.c).max())
+    prog = ConicProgram(m=L.m, n=L.n, n1=L.n1, row_ptr=rp, col_idx=col, vals=val, c=c, h=h, l=L.l, u=L.u,
+                        pk=L.pk, pdim=L.pdim, rk=L.rk, rdim=L.rdim)
+    k = O.OracleSolver(prog, ruiz_iters=0, pock_chambolle=0).kkt_point(L.x_star, ys)
+    assert max(k["err_p"], k["err_d"], k["err_gap"]) <= 1e-13, k
+    assert abs(k["pobj"] - float(c @ L.x_star)) <= 1e-12 * (1 + abs(k["pobj"]))

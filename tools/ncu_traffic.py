@@ -5,6 +5,8 @@
         iteration phase of the bench instance (NVTX range "iterate"; setup and
         autotune excluded) and writes profiles/ncu_traffic.json stamped with the
         commit it measured;
+    python tools/ncu_traffic.py parse --config lasso --commit HASH
+        re-reads gpurun_out/traffic_<config>.csv of an earlier run;
     python tools/ncu_traffic.py drive --config lasso
         the driver ncu profiles (host-driven loop, so every kernel is a launch).
 
@@ -28,9 +30,9 @@ sys.path.insert(0, ROOT)
 # the format the bench's autotune keeps per config
 TILED = {"lasso": "1", "fisher": "0", "mpo": "0", "mixed": "0"}
 SWEEPS = {"spmv_K_dual": ("k_tiled_sliced<2>", "k_tiled_tma<2>", "k_tiled_partial<2>",
-                          "k_tiled_combine<pdcs::EpiDualTrial", "spmv_kernel<pdcs::EpiDualTrial>"),
+                          "k_tiled_combine<EpiDualTrial", "spmv_kernel<EpiDualTrial>"),
           "spmv_KT_halpern": ("k_tiled_sliced<1>", "k_tiled_tma<1>", "k_tiled_partial<1>",
-                              "k_tiled_combine<pdcs::EpiHalpernX", "spmv_kernel<pdcs::EpiHalpernX>"),
+                              "k_tiled_combine<EpiHalpernX", "spmv_kernel<EpiHalpernX>"),
           "halpern_y": ("k_halpern_y",), "primal_elem": ("k_primal_elem",)}
 
 
@@ -49,10 +51,11 @@ def drive(config, iters):
     print("done", prog.name, prog.m, prog.n, prog.nnz)
 
 
-def run(configs, iters, out):
+def run(configs, iters, out, parse_only=False, commit=None):
     res = {}
-    head = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], cwd=ROOT, capture_output=True,
-                          text=True).stdout.strip() or "unknown"
+    head = commit or os.environ.get("PDCS_COMMIT") or subprocess.run(
+        ["git", "rev-parse", "--short=12", "HEAD"], cwd=ROOT, capture_output=True, text=True).stdout.strip() \
+        or "unknown"
     for cfg in configs:
         csvp = os.path.join(ROOT, "gpurun_out", f"traffic_{cfg}.csv")
         env = dict(os.environ, PDCS_NO_GRAPH="1", PDCS_TILED=TILED[cfg])
@@ -61,7 +64,8 @@ def run(configs, iters, out):
                "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
                "-k", "regex:k_tiled|spmv_kernel|k_halpern_y|k_primal_elem", "--log-file", csvp,
                sys.executable, os.path.abspath(__file__), "drive", "--config", cfg, "--iters", str(iters)]
-        subprocess.run(cmd, env=env, check=True)
+        if not parse_only:
+            subprocess.run(cmd, env=env, check=True)
         rows = [r for r in csv.reader(l for l in open(csvp) if not l.startswith("=="))]
         hdr = rows[0]
         ki, mi, vi, idi = (hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"),
@@ -105,7 +109,8 @@ def run(configs, iters, out):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["run", "drive"])
+    ap.add_argument("mode", choices=["run", "drive", "parse"])
+    ap.add_argument("--commit", default=None, help="commit the CSVs were measured at (parse)")
     ap.add_argument("--config", action="append")
     ap.add_argument("--iters", type=int, default=6)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "ncu_traffic.json"))
@@ -114,4 +119,4 @@ if __name__ == "__main__":
     if a.mode == "drive":
         drive(cfgs[0], a.iters)
     else:
-        run(cfgs, a.iters, a.out)
+        run(cfgs, a.iters, a.out, parse_only=a.mode == "parse", commit=a.commit)

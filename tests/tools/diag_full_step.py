@@ -1,5 +1,6 @@
+import os
 import sys, numpy as np
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle as O
 import paper_2505_00311_b200 as P
 from instances import CONFIGS

@@ -1,8 +1,8 @@
 """Mutation check of the oracle pins: apply each plausible slip to a copy of the
 oracle, run the -m "not gpu" pin suites, and report which test kills it.
-Usage: python tools/oracle_mutants.py [NAME ...]  (copies the repo under $TMPDIR)."""
+Usage: python tests/tools/oracle_mutants.py [NAME ...]  (copies the repo under $TMPDIR)."""
 import os, shutil, subprocess, sys, tempfile
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 WORK = tempfile.mkdtemp(prefix="oracle_mutants_")
 from concurrent.futures import ThreadPoolExecutor
 MUTS = {

@@ -16,7 +16,7 @@ the time, against MEASURED_PEAKS.json.  CPU baseline: the oracle's per-block
 projections (single thread) on a bounded sample of the same cones,
 extrapolated per element.
 
-    python tools/proj_bench.py [--fig soc|exp|both] [--reps 3] [--out profiles/r1_proj.json]
+    python tests/tools/proj_bench.py [--fig soc|exp|both] [--reps 3] [--out profiles/r1_proj.json]
 """
 import argparse
 import json
@@ -27,7 +27,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 SOC, EXP = 2, 4

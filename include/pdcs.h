@@ -242,7 +242,12 @@ void pdcs_enable_timing(pdcs_ctx *ctx, int on);
  * last line-search numerator and cross term, then setup diagnostics: tiled_K
  * (0/1), autotune ms (CSR, tiled) for K, the same three for K^T, host build
  * ms of the tiled K and K^T formats, wall ms of pdcs_create and of
- * pdcs_set_cones.  Returns the number of values written (<= 36). */
+ * pdcs_set_cones, and 1 if the box columns are stored in a locality order
+ * (every x-side array crossing this ABI stays in the
+ * caller's order), then the L2 column panels of K~ and K~^T (DESIGN.md
+ * §7.7): number of panels kept (0 = CSR / tiled sweep) and the autotune ms of
+ * the CSR and the panelled sweep, for K~ then K~^T.  Returns the number of
+ * values written (<= 43). */
 int pdcs_get_scalars(pdcs_ctx *ctx, double *out, int cap);
 
 /* Number of kernel launches issued by the last pdcs_iterate call. */

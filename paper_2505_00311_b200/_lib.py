@@ -128,7 +128,8 @@ SCALAR_KEYS = ["eta", "omega", "beta", "k", "total", "trials", "restarts", "e_an
                "e_prev", "best_e", "use_avg", "restart", "last_num", "last_cross",
                "tiled_K", "tune_K_csr_ms", "tune_K_tiled_ms", "tiled_KT", "tune_KT_csr_ms",
                "tune_KT_tiled_ms", "tiled_K_build_ms", "tiled_KT_build_ms", "setup_create_ms",
-               "setup_cones_ms"]
+               "setup_cones_ms", "colperm", "panels_K", "tune_K_csr_ms_p", "tune_K_panel_ms", "panels_KT",
+               "tune_KT_csr_ms_p", "tune_KT_panel_ms"]
 
 
 def _check(code, ctx=None):

@@ -23,6 +23,7 @@
 #include "../../include/pdcs.h"
 #include "ops.cuh"
 #include "tiled.cuh"
+#include "panels.cuh"
 #include "comm.h"
 
 using namespace pdcs;
@@ -610,6 +611,82 @@ void validate_csr(const int64_t* ptr, const int32_t* col, const double* val, int
   fail(PDCS_ERR_NONFINITE, "non-finite matrix entry in row " + row);
 }
 
+// Column order of the box coordinates for gather locality.
+// The SpMV sweeps gather 16-byte (x^_j, x_j) pairs, two per 32-byte sector.  A
+// long row (>= kPermLongRow entries, served by one CTA, so no other row reuses
+// its sectors) whose columns are strided pays a whole sector per entry; this is
+// Fisher's supply rows, sum_i X_ij = b_j, over a buyer-major X.  Box columns are
+// elementwise (their projection is a clip), so they may be stored in any order:
+// they are stably sorted by the longest row that holds them (ties: the lower
+// row), which puts each long row's box columns next to each other.  The order
+// is used when it cuts the sectors the long rows touch by >= 20%; cone columns
+// keep their places.  Returns false (identity) otherwise.
+constexpr int64_t kPermLongRow = 1024;
+
+int64_t long_row_sectors(const int64_t* ptr, const int32_t* col, int64_t m, const int32_t* u2i) {
+  int64_t total = 0;
+  std::vector<int32_t> buf;
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t a = ptr[i], b = ptr[i + 1];
+    if (b - a < kPermLongRow) continue;
+    buf.resize(b - a);
+    for (int64_t q = a; q < b; ++q) buf[q - a] = u2i ? u2i[col[q]] : col[q];
+    if (u2i) std::sort(buf.begin(), buf.end());
+    int64_t cnt = 0, last = -1;
+    for (int32_t c : buf)
+      if ((c >> 1) != last) { ++cnt; last = c >> 1; }
+    total += cnt;
+  }
+  return total;
+}
+
+bool plan_colperm(const int64_t* ptr, const int32_t* col, int64_t m, int64_t n, int64_t n1,
+                  std::vector<int32_t>& u2i, std::vector<int32_t>& i2u) {
+  if (n1 < 2) return false;
+  const int64_t before = long_row_sectors(ptr, col, m, nullptr);
+  if (before == 0) return false;
+  std::vector<int64_t> best(n1, -1), blen(n1, -1);
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t len = ptr[i + 1] - ptr[i];
+    for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q) {
+      const int32_t j = col[q];
+      if (j < n1 && len > blen[j]) { blen[j] = len; best[j] = i; }
+    }
+  }
+  std::vector<int32_t> order(n1);
+  for (int64_t j = 0; j < n1; ++j) order[j] = (int32_t)j;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return best[a] < best[b]; });
+  i2u.resize(n);
+  u2i.resize(n);
+  for (int64_t k = 0; k < n; ++k) i2u[k] = k < n1 ? order[k] : (int32_t)k;
+  for (int64_t k = 0; k < n; ++k) u2i[i2u[k]] = (int32_t)k;
+  const int64_t after = long_row_sectors(ptr, col, m, u2i.data());
+  if ((double)after > 0.8 * (double)before) { u2i.clear(); i2u.clear(); return false; }
+  return true;
+}
+
+// The CSR with column ids mapped through u2i, each row re-sorted (host threads).
+void permute_csr(const int64_t* ptr, const int32_t* col, const double* val, int64_t m,
+                 const std::vector<int32_t>& u2i, std::vector<int32_t>& pcol, std::vector<double>& pval) {
+  const int64_t nnz = ptr[m];
+  pcol.resize(nnz);
+  pval.resize(nnz);
+  const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(16, nnz / 2000000 + 1));
+  std::vector<std::thread> th;
+  for (int w = 0; w < nth; ++w)
+    th.emplace_back([&, w] {
+      std::vector<std::pair<int32_t, double>> buf;
+      for (int64_t i = m * w / nth; i < m * (w + 1) / nth; ++i) {
+        const int64_t a = ptr[i], b = ptr[i + 1];
+        buf.resize(b - a);
+        for (int64_t q = a; q < b; ++q) buf[q - a] = {u2i[col[q]], val[q]};
+        std::sort(buf.begin(), buf.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        for (int64_t q = a; q < b; ++q) { pcol[q] = buf[q - a].first; pval[q] = buf[q - a].second; }
+      }
+    });
+  for (auto& t : th) t.join();
+}
+
 // Size class of each cone block: 0 thread, 1 warp, 2 CTA,
 // 3 cluster, 4 grid.  Exp blocks and SOC/RSOC of dim <= 32 take one thread.
 // The warp class covers dims up to 512, or up to 16384 when it then holds
@@ -656,6 +733,11 @@ struct pdcs_ctx {
   std::vector<int64_t> hptr;       // local CSR row pointers (host)
   std::vector<double> hl, hu;      // original bounds
   double hnorm = 0.0, cnorm = 0.0; // ||h||_inf, ||c||_inf (original data)
+  // box-column order (plan_colperm): internal k holds the caller's column i2u[k]
+  bool colperm = false;
+  std::vector<int32_t> u2i, i2u;
+  DBuf<int32_t> u2i_d, i2u_d;
+  DBuf<double> permbuf;
 
   // device matrices
   DevCsr K, KT;
@@ -689,6 +771,18 @@ struct pdcs_ctx {
     float tune_csr_ms = 0.f, tune_tiled_ms = 0.f;
     double build_ms = 0.0;                     // host build of the format
   } tK, tKT;
+  // L2 column panels of K~ and K~^T (panels.cuh), kept by a setup autotune when
+  // the gathered vector exceeds L2
+  struct Panels {
+    bool on = false;
+    int P = 0;
+    int64_t rows = 0, pcols = 0;
+    int nx = 1;
+    DBuf<int32_t> ptr, col, prow;
+    DBuf<double> val, acc;
+    std::vector<DevCsr> part;
+    float tune_csr_ms = 0.f, tune_panel_ms = 0.f;
+  } pK, pKT;
   double t_create_ms = 0.0, t_cones_ms = 0.0;  // wall time of pdcs_create / pdcs_set_cones
   // host builds of the tiled formats (build_tiled), started in pdcs_create
   TiledHost hK, hKT;
@@ -788,10 +882,32 @@ struct pdcs_ctx {
   template <class Epi>
   void spmv(const char* name, const DevCsr& A, const double* x1, const double* x2, Epi epi, double* part,
             int64_t slot0) {
+    if (&A == &K && pK.on) { psweep(name, pK, x1, x2, epi, part, slot0); return; }
+    if (&A == &KT && pKT.on) { psweep(name, pKT, x1, x2, epi, part, slot0); return; }
     if (A.plan.total_cta == 0) return;
     launch(name, [&] {
       spmv_kernel<Epi><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, x1, x2, A.plan, epi, ctl,
                                                               part, slot0);
+    });
+  }
+  // A sweep through the L2 panels: one accumulating pass per panel, then the
+  // sweep's epilogue over the accumulated rows (panels.cuh).
+  template <class Epi>
+  void psweep(const char* name, Panels& PA, const double* x1, const double* x2, Epi epi, double* part,
+              int64_t slot0) {
+    const char* pname = &PA == &pK ? "panel_K_partial" : "panel_KT_partial";
+    for (int p = 0; p < PA.P; ++p) {
+      const DevCsr& A = PA.part[p];
+      if (A.plan.total_cta == 0) continue;
+      EpiPanelAcc<Epi> ea{epi, PA.acc.p, p == 0 ? 1 : 0};
+      launch(pname, [&] {
+        spmv_kernel<EpiPanelAcc<Epi>><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, x1, x2, A.plan, ea,
+                                                                             ctl, nullptr, 0);
+      });
+    }
+    launch(name, [&] {
+      k_panel_finish<Epi><<<(int)std::min<int64_t>(grid_for(PA.rows, sms), (int64_t)sms * 4), kThreads, 0, st>>>(
+          PA.rows, PA.acc.p, epi, ctl, part, slot0);
     });
   }
   void spmv_store(const DevCsr& A, const double* xin, double* out, bool accepted_only = false) {
@@ -839,6 +955,21 @@ struct pdcs_ctx {
     ++launches;
     const std::string e = comm->allreduce(buf, count, op, st);
     if (!e.empty()) fail(PDCS_ERR_NCCL, e);
+  }
+  // n-vectors between the stored column order and the caller's (plan_colperm;
+  // identity when no order was chosen).  to_caller returns a device pointer.
+  const double* to_caller(const double* src) {
+    if (!colperm) return src;
+    k_gather_vals<<<grid_for(n, sms), kThreads, 0, st>>>(n, u2i_d.p, src, permbuf.p);
+    CK(cudaGetLastError());
+    return permbuf.p;
+  }
+  void from_caller(double* dst, const double* src, cudaMemcpyKind kind) {
+    if (!n) return;
+    if (!colperm) { CK(cudaMemcpyAsync(dst, src, n * sizeof(double), kind, st)); return; }
+    CK(cudaMemcpyAsync(permbuf.p, src, n * sizeof(double), kind, st));
+    k_gather_vals<<<grid_for(n, sms), kThreads, 0, st>>>(n, i2u_d.p, permbuf.p, dst);
+    CK(cudaGetLastError());
   }
   // Time-limit stop, decided collectively so that every rank leaves at the
   // same Eq. 9 check (a rank-local clock would strand its peers in the next
@@ -1329,6 +1460,108 @@ struct pdcs_ctx {
     }
   }
 
+  // L2 column panels of A (rows x cols, gathering nx doubles per column) when
+  // the gathered vector exceeds L2 and the tiled copy is off (panels.cuh).
+  // PDCS_PANELS=0 disables, =P forces P panels (no autotune); PDCS_PANEL_MB
+  // sets the vector slice per panel (default 24 MB of the 126 MB L2).  Kept only
+  // if the setup autotune measures it >= 10% faster than the CSR sweep.
+  void build_panels(Panels& PA, const DevCsr& A, bool tiled_on, int nx) {
+    const char* e = std::getenv("PDCS_PANELS");
+    const int force = e ? std::atoi(e) : -1;
+    if (force == 0 || A.nnz == 0 || A.m == 0 || A.n == 0) return;
+    if (force < 0 && tiled_on) return;
+    const double vec_bytes = (double)A.n * 8.0 * nx;
+    const double panel_mb = std::getenv("PDCS_PANEL_MB") ? std::atof(std::getenv("PDCS_PANEL_MB")) : 24.0;
+    if (force < 0 && vec_bytes < 64.0 * (1 << 20)) return;
+    const int P = force > 0 ? force : (int)std::ceil(vec_bytes / (panel_mb * (1 << 20)));
+    if (P < 1 || (force < 0 && P < 2)) return;
+    const int64_t rows = A.m, pcols = (A.n + P - 1) / P;
+    PA.P = P; PA.rows = rows; PA.pcols = pcols; PA.nx = nx;
+    DBuf<int32_t> cnt;
+    cnt.alloc((int64_t)P * rows + 1);
+    CK(cudaMemsetAsync(cnt.p, 0, ((int64_t)P * rows + 1) * sizeof(int32_t), st));
+    k_panel_count<<<grid_for(rows, sms, 32), kThreads, 0, st>>>(rows, A.ptr, A.col, pcols, cnt.p);
+    PA.ptr.alloc((int64_t)P * rows + 1);
+    size_t tmpb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmpb, cnt.p, PA.ptr.p, (int)(P * rows + 1), st));
+    DBuf<char> tmp;
+    tmp.alloc((int64_t)tmpb);
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmpb, cnt.p, PA.ptr.p, (int)(P * rows + 1), st));
+    PA.col.alloc(A.nnz);
+    PA.val.alloc(A.nnz);
+    k_panel_scatter<<<grid_for(rows, sms, 32), kThreads, 0, st>>>(rows, A.ptr, A.col, A.val, pcols, PA.ptr.p,
+                                                                  PA.col.p, PA.val.p);
+    CK(cudaGetLastError());
+    std::vector<int32_t> hp((size_t)P * rows + 1);
+    CK(cudaMemcpyAsync(hp.data(), PA.ptr.p, hp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int32_t> rowstore;
+    std::vector<size_t> offs;
+    PA.part.assign(P, DevCsr{});
+    std::vector<int64_t> pp(rows + 1);
+    for (int p = 0; p < P; ++p) {
+      for (int64_t i = 0; i <= rows; ++i) pp[i] = hp[(size_t)p * rows + i] - hp[(size_t)p * rows];
+      DevCsr& D = PA.part[p];
+      D.m = rows; D.n = A.n; D.nnz = pp[rows];
+      D.ptr = PA.ptr.p + (size_t)p * rows; D.col = PA.col.p; D.val = PA.val.p;
+      build_plan(D, pp, rowstore, offs);
+    }
+    upload(PA.prow, rowstore, st);
+    for (DevCsr& D : PA.part)
+      for (int c = 0; c < D.plan.ncls; ++c)
+        if (D.plan.cls[c].rows) D.plan.cls[c].rows = PA.prow.p + ((size_t)(uintptr_t)D.plan.cls[c].rows - 1);
+    PA.acc.alloc(rows * nx);
+    PA.on = true;
+    if (force > 0) return;
+    // setup autotune: the panelled product against the CSR one, on this matrix
+    DBuf<double> xin, out;
+    xin.alloc(A.n * nx + 2);
+    out.alloc(rows);
+    k_fill<<<grid_for(A.n * nx, sms), kThreads, 0, st>>>(A.n * nx, 1.0, xin.p);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    auto timeit = [&](auto&& f) {   // median of 5 after 2 warm-ups
+      f();
+      f();
+      float v[5];
+      for (int i = 0; i < 5; ++i) {
+        CK(cudaEventRecord(a, st));
+        f();
+        CK(cudaEventRecord(b, st));
+        CK(cudaEventSynchronize(b));
+        CK(cudaEventElapsedTime(&v[i], a, b));
+      }
+      std::sort(v, v + 5);
+      return v[2];
+    };
+    const bool was_timing = timing;
+    timing = false;
+    float tc, tp;
+    if (nx == 2) {
+      EpiStore2 es{out.p};
+      tc = timeit([&] { spmv_kernel<EpiStore2><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, xin.p, nullptr,
+                                                                                 A.plan, es, ctl, nullptr, 0); });
+      tp = timeit([&] { psweep("autotune", PA, xin.p, nullptr, es, nullptr, 0); });
+    } else {
+      EpiStore es{out.p};
+      tc = timeit([&] { spmv_kernel<EpiStore><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, xin.p, nullptr,
+                                                                                A.plan, es, ctl, nullptr, 0); });
+      tp = timeit([&] { psweep("autotune", PA, xin.p, nullptr, es, nullptr, 0); });
+    }
+    timing = was_timing;
+    CK(cudaGetLastError());
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    PA.tune_csr_ms = tc;
+    PA.tune_panel_ms = tp;
+    if (!(tp < 0.9f * tc)) {
+      PA.on = false;
+      PA.ptr.free_(); PA.col.free_(); PA.val.free_(); PA.prow.free_(); PA.acc.free_();
+      PA.part.clear();
+    }
+  }
+
   // products of (x, y) into (kx, kty)
   void products(const double* xs, const double* ys, double* kxo, double* ktyo) {
     spmv_store(K, xs, kxo);
@@ -1583,6 +1816,20 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
       fail(PDCS_ERR_ARG, "null input pointer");
     }
     validate_csr(ctx->hptr.data(), hcolp, hvalp, m, n);
+    // box-column order for gather locality (single context only: every rank of a
+    // sharded run must store x identically, and the order depends on all rows)
+    std::vector<int32_t> pcol;
+    std::vector<double> pval;
+    {
+      const char* e = std::getenv("PDCS_COLPERM");
+      const bool allow = (e ? std::atoi(e) != 0 : true) && !ctx->dist;
+      if (allow && plan_colperm(ctx->hptr.data(), hcolp, m, n, n1, ctx->u2i, ctx->i2u)) {
+        permute_csr(ctx->hptr.data(), hcolp, hvalp, m, ctx->u2i, pcol, pval);
+        hcolp = pcol.data();
+        hvalp = pval.data();
+        ctx->colperm = true;
+      }
+    }
     // tiled format of K~ (structure only) on host threads, overlapping the uploads
     // and the device transpose below; joined before this call returns
     ctx->thK = std::thread([ctx, hcolp, m, n] {
@@ -1595,6 +1842,16 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     std::vector<double> hc = to_host(c, n, mem_kind), hh = to_host(h, m, mem_kind);
     ctx->hl = to_host(l, n1, mem_kind);
     ctx->hu = to_host(u, n1, mem_kind);
+    if (ctx->colperm) {                           // c, l, u in the stored column order
+      auto perm = [&](std::vector<double>& v, int64_t cnt) {
+        std::vector<double> o(cnt);
+        for (int64_t k = 0; k < cnt; ++k) o[k] = v[ctx->i2u[k]];
+        v.swap(o);
+      };
+      perm(hc, n);
+      perm(ctx->hl, n1);
+      perm(ctx->hu, n1);
+    }
     for (double v : hc) if (!std::isfinite(v)) fail(PDCS_ERR_NONFINITE, "non-finite c");
     for (double v : hh) if (!std::isfinite(v)) fail(PDCS_ERR_NONFINITE, "non-finite h");
     for (int64_t j = 0; j < n1; ++j) {
@@ -1615,8 +1872,14 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     ctx->Kcol.alloc(nnz);
     ctx->Kval.alloc(nnz);
     if (nnz) {
-      CK(cudaMemcpyAsync(ctx->Kcol.p, col_idx, nnz * sizeof(int32_t), cudaMemcpyDefault, st));
-      CK(cudaMemcpyAsync(ctx->Kval.p, vals, nnz * sizeof(double), cudaMemcpyDefault, st));
+      CK(cudaMemcpyAsync(ctx->Kcol.p, ctx->colperm ? hcolp : col_idx, nnz * sizeof(int32_t), cudaMemcpyDefault, st));
+      CK(cudaMemcpyAsync(ctx->Kval.p, ctx->colperm ? hvalp : vals, nnz * sizeof(double), cudaMemcpyDefault, st));
+    }
+    if (ctx->colperm) {
+      upload(ctx->u2i_d, ctx->u2i, st);
+      upload(ctx->i2u_d, ctx->i2u, st);
+      ctx->permbuf.alloc(n);
+      CK(cudaStreamSynchronize(st));             // pcol / pval are pageable and die with this scope
     }
     upload(ctx->c0, hc, st);
     upload(ctx->h0, hh, st);
@@ -1926,6 +2189,9 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
       ctx->hKTptr = std::vector<int64_t>();
       ctx->hKTcol = std::vector<int32_t>();
     }
+    // L2 column panels where the gathered vector exceeds L2 (panels.cuh)
+    ctx->build_panels(ctx->pK, ctx->K, ctx->tK.on, 2);
+    ctx->build_panels(ctx->pKT, ctx->KT, ctx->tKT.on, 1);
     // scaled data (reading A2): c~ = c/q, h~ = h/r, l~ = q l, u~ = q u
     k_ewise<<<Gn, kThreads, 0, st>>>(n, ctx->c0.p, ctx->q.p, 0, ctx->ct.p);
     k_ewise<<<Gm, kThreads, 0, st>>>(m, ctx->h0.p, ctx->r.p, 0, ctx->ht.p);
@@ -2016,7 +2282,7 @@ pdcs_status pdcs_set_iterate(pdcs_ctx* ctx, const double* x, const double* y) {
     const int64_t n = ctx->n, m = ctx->m;
     const cudaMemcpyKind kind = ctx->mem_kind == PDCS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (x) {
-      CK(cudaMemcpyAsync(ctx->tmpn.p, x, n * sizeof(double), kind, st));
+      ctx->from_caller(ctx->tmpn.p, x, kind);
       k_ewise<<<grid_for(n, ctx->sms), kThreads, 0, st>>>(n, ctx->tmpn.p, ctx->q.p, 1, ctx->x.p);
     }
     if (y) {
@@ -2233,7 +2499,7 @@ pdcs_status pdcs_get_iterate(pdcs_ctx* ctx, int which, int space, double* x, dou
       fail(PDCS_ERR_ARG, "bad space");
     }
     const cudaMemcpyKind kind = ctx->mem_kind == PDCS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    if (x && n) CK(cudaMemcpyAsync(x, xo, n * sizeof(double), kind, st));
+    if (x && n) CK(cudaMemcpyAsync(x, ctx->to_caller(xo), n * sizeof(double), kind, st));
     if (y && m) CK(cudaMemcpyAsync(y, yo, m * sizeof(double), kind, st));
     CK(cudaStreamSynchronize(st));
   });
@@ -2249,8 +2515,11 @@ pdcs_status pdcs_get_state(pdcs_ctx* ctx, double* x, double* y, double* x0, doub
     auto get = [&](double* dst, const DBuf<double>& src, int64_t cnt) {
       if (dst && cnt) CK(cudaMemcpyAsync(dst, src.p, cnt * sizeof(double), kind, ctx->st));
     };
-    get(x, ctx->x, n); get(y, ctx->y, m); get(x0, ctx->x0, n); get(y0, ctx->y0, m);
-    get(xsum, ctx->xsum, n); get(ysum, ctx->ysum, m);
+    auto getx = [&](double* dst, const DBuf<double>& src) {
+      if (dst && n) CK(cudaMemcpyAsync(dst, ctx->to_caller(src.p), n * sizeof(double), kind, ctx->st));
+    };
+    getx(x, ctx->x); get(y, ctx->y, m); getx(x0, ctx->x0); get(y0, ctx->y0, m);
+    getx(xsum, ctx->xsum); get(ysum, ctx->ysum, m);
     ctx->read_ctl();
     if (sc) {
       const Ctl& C = *ctx->hctl;
@@ -2272,8 +2541,8 @@ pdcs_status pdcs_set_state(pdcs_ctx* ctx, const double* x, const double* y, cons
     auto put = [&](DBuf<double>& dst, const double* src, int64_t cnt) {
       if (cnt) CK(cudaMemcpyAsync(dst.p, src, cnt * sizeof(double), kind, st));
     };
-    put(ctx->x, x, n); put(ctx->y, y, m); put(ctx->x0, x0, n); put(ctx->y0, y0, m);
-    put(ctx->xsum, xsum, n); put(ctx->ysum, ysum, m);
+    ctx->from_caller(ctx->x.p, x, kind); put(ctx->y, y, m); ctx->from_caller(ctx->x0.p, x0, kind);
+    put(ctx->y0, y0, m); ctx->from_caller(ctx->xsum.p, xsum, kind); put(ctx->ysum, ysum, m);
     ctx->products(ctx->x.p, ctx->y.p, ctx->kxh.p, ctx->kty.p);
     auto cp = [&](double* d, const double* s_, int64_t cnt) {
       if (cnt) CK(cudaMemcpyAsync(d, s_, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -2297,7 +2566,7 @@ pdcs_status pdcs_get_scaling(pdcs_ctx* ctx, double* r, double* q) {
     if (!ctx->cones_set) fail(PDCS_ERR_STATE, "call pdcs_set_cones first");
     const cudaMemcpyKind kind = ctx->mem_kind == PDCS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (r && ctx->m) CK(cudaMemcpyAsync(r, ctx->r.p, ctx->m * sizeof(double), kind, ctx->st));
-    if (q && ctx->n) CK(cudaMemcpyAsync(q, ctx->q.p, ctx->n * sizeof(double), kind, ctx->st));
+    if (q && ctx->n) CK(cudaMemcpyAsync(q, ctx->to_caller(ctx->q.p), ctx->n * sizeof(double), kind, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
   });
 }
@@ -2325,15 +2594,18 @@ int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
   if (!ctx || !out || !ctx->ctl) return 0;
   if (guard(ctx, [&] { ctx->read_ctl(); }) != PDCS_OK) return 0;
   const Ctl& C = *ctx->hctl;
-  double v[36] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
+  double v[43] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
                   (double)C.restarts, C.e_anchor, C.Wsum, C.eta_init,
                   C.kkt[0][0], C.kkt[0][1], C.kkt[0][2], C.kkt[0][3], C.kkt[0][4],
                   C.kkt[1][0], C.kkt[1][1], C.kkt[1][2], C.kkt[1][3], C.kkt[1][4],
                   C.e_prev, C.best_e, (double)C.use_avg, (double)C.restart, C.last_num, C.last_cross,
                   (double)ctx->tK.on, ctx->tK.tune_csr_ms, ctx->tK.tune_tiled_ms,
                   (double)ctx->tKT.on, ctx->tKT.tune_csr_ms, ctx->tKT.tune_tiled_ms,
-                  ctx->tK.build_ms, ctx->tKT.build_ms, ctx->t_create_ms, ctx->t_cones_ms};
-  const int k = std::min(cap, 36);
+                  ctx->tK.build_ms, ctx->tKT.build_ms, ctx->t_create_ms, ctx->t_cones_ms,
+                  (double)ctx->colperm, (double)(ctx->pK.on ? ctx->pK.P : 0), ctx->pK.tune_csr_ms,
+                  ctx->pK.tune_panel_ms, (double)(ctx->pKT.on ? ctx->pKT.P : 0), ctx->pKT.tune_csr_ms,
+                  ctx->pKT.tune_panel_ms};
+  const int k = std::min(cap, 43);
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }

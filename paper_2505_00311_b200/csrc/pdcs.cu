@@ -754,6 +754,13 @@ struct pdcs_ctx {
   bool dist = false;
   std::unique_ptr<Comm> comm;
   DBuf<double> ktyp;                           // local K~^T y partial before the all-reduce
+  // the K~^T y partial in row chunks, each all-reduced on comm_st while the next
+  // chunk's rows are summed (PDCS_AR_CHUNKS, default 4; CSR K~^T only)
+  std::vector<SpmvPlan> ktc_plan;
+  std::vector<int64_t> ktc_row;                // chunk c = rows [ktc_row[c], ktc_row[c+1])
+  cudaStream_t comm_st = nullptr;
+  std::vector<cudaEvent_t> ev_ar;
+  cudaEvent_t ev_ar_done = nullptr;
   // column-tiled copies of K~ (pair gather) and K~^T (y gather), tiled.cuh
   struct TiledDev {
     bool on = false;
@@ -836,6 +843,9 @@ struct pdcs_ctx {
       if (ev_join[c]) cudaEventDestroy(ev_join[c]);
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
+    for (auto e : ev_ar) cudaEventDestroy(e);
+    if (ev_ar_done) cudaEventDestroy(ev_ar_done);
+    if (comm_st) cudaStreamDestroy(comm_st);
     if (ctl) cudaFree(ctl);
     if (hctl) cudaFreeHost(hctl);
     for (auto e : evpool) cudaEventDestroy(e);
@@ -950,10 +960,10 @@ struct pdcs_ctx {
     CK(cudaStreamSynchronize(st));
   }
   // In-place all-reduce over the row shards (no-op on a single rank).
-  void allreduce(double* buf, size_t count, RedOp op) {
+  void allreduce(double* buf, size_t count, RedOp op, cudaStream_t s_ = nullptr) {
     if (!dist || count == 0) return;
     ++launches;
-    const std::string e = comm->allreduce(buf, count, op, st);
+    const std::string e = comm->allreduce(buf, count, op, s_ ? s_ : st);
     if (!e.empty()) fail(PDCS_ERR_NCCL, e);
   }
   // n-vectors between the stored column order and the caller's (plan_colperm;
@@ -1115,10 +1125,27 @@ struct pdcs_ctx {
         launch("spmv_KT_partial", [&] {
           k_tiled_combine<EpiStoreAcc, 1><<<tKT.g_combine, kThreads, 0, st>>>(tKT.M, tKT.scratch.p, ea, ctl, nullptr, 0);
         });
+      } else if (!ktc_plan.empty() && !pKT.on) {
+        // chunk c's rows summed, then all-reduced on comm_st while chunk c+1 runs
+        for (size_t c = 0; c < ktc_plan.size(); ++c) {
+          const SpmvPlan& pl = ktc_plan[c];
+          EpiStoreAcc ea{ktyp.p, 0};
+          if (pl.total_cta)
+            launch("spmv_KT_partial", [&] {
+              spmv_kernel<EpiStoreAcc><<<pl.total_cta, kThreads, 0, st>>>(KT.ptr, KT.col, KT.val, y.p, nullptr, pl, ea,
+                                                                          ctl, nullptr, 0);
+            });
+          CK(cudaEventRecord(ev_ar[c], st));
+          CK(cudaStreamWaitEvent(comm_st, ev_ar[c], 0));
+          allreduce(ktyp.p + ktc_row[c], (size_t)(ktc_row[c + 1] - ktc_row[c]), RedOp::Sum, comm_st);
+        }
+        CK(cudaEventRecord(ev_ar_done, comm_st));
+        CK(cudaStreamWaitEvent(st, ev_ar_done, 0));
       } else {
         spmv_store(KT, y.p, ktyp.p, true);
+        allreduce(ktyp.p, n, RedOp::Sum);
       }
-      allreduce(ktyp.p, n, RedOp::Sum);
+      if (tKT.on) allreduce(ktyp.p, n, RedOp::Sum);
       launch("halpern_x", [&] {
         k_halpern_x<<<g_pe, kThreads, 0, st>>>(n, xh.p, x0.p, ktyp.p, x.p, kty.p, xsum.p, ctl);
       });
@@ -1571,8 +1598,8 @@ struct pdcs_ctx {
 
   // ---------------------------------------------------------------- setup helpers
   void build_plan(DevCsr& A, const std::vector<int64_t>& ptr, std::vector<int32_t>& rowstore,
-                  std::vector<size_t>& offs) {
-    const int64_t rows = (int64_t)ptr.size() - 1;
+                  std::vector<size_t>& offs, int64_t row_a = 0, int64_t row_b = -1) {
+    const int64_t rows = row_b >= 0 ? row_b : (int64_t)ptr.size() - 1;
     // V classes: 1, 4, 8, 16, 32 lanes per row, 0 = one CTA per row.  Upper
     // row-length bounds per class (PDCS_SPMV_BINS="b1,b4,b8,b16,b32" overrides).
     const int Vs[kMaxClasses] = {1, 4, 8, 16, 32, 0};
@@ -1586,7 +1613,7 @@ struct pdcs_ctx {
       }
     }
     std::vector<int64_t> lists[kMaxClasses];
-    for (int64_t i = 0; i < rows; ++i) {
+    for (int64_t i = row_a; i < rows; ++i) {
       const int64_t L = ptr[i + 1] - ptr[i];
       int c = 5;
       for (int k = 0; k < 5; ++k)
@@ -1931,6 +1958,23 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     std::vector<size_t> offs;
     ctx->build_plan(ctx->K, ctx->hptr, rowstore, offs);
     ctx->build_plan(ctx->KT, tptr, rowstore, offs);
+    // sharded: K~^T in row chunks whose all-reduces overlap the next chunk's sums
+    if (ctx->dist) {
+      const char* e = std::getenv("PDCS_AR_CHUNKS");
+      const int C = e ? std::max(1, std::atoi(e)) : (n * 8 >= (8 << 20) ? 4 : 1);
+      if (C > 1 && n >= C) {
+        for (int c = 0; c <= C; ++c) ctx->ktc_row.push_back(n * c / C);
+        for (int c = 0; c < C; ++c) {
+          DevCsr tmpA;
+          ctx->build_plan(tmpA, tptr, rowstore, offs, ctx->ktc_row[c], ctx->ktc_row[c + 1]);
+          ctx->ktc_plan.push_back(tmpA.plan);
+        }
+        CK(cudaStreamCreateWithFlags(&ctx->comm_st, cudaStreamNonBlocking));
+        ctx->ev_ar.resize(C);
+        for (auto& ev : ctx->ev_ar) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_ar_done, cudaEventDisableTiming));
+      }
+    }
     // tiled format of K~^T from the transposed structure, in the background
     // (joined in pdcs_set_cones, which uses it after the Ruiz scaling)
     ctx->hKTptr = std::move(tptr);
@@ -1942,6 +1986,12 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     upload(ctx->planrows, rowstore, st);
     ctx->patch_plan(ctx->K);
     ctx->patch_plan(ctx->KT);
+    for (SpmvPlan& pl : ctx->ktc_plan) {
+      DevCsr tmpA;
+      tmpA.plan = pl;
+      ctx->patch_plan(tmpA);
+      pl = tmpA.plan;
+    }
     // ---- L1 / shared-memory split for the gathering kernels (PDCS_CARVEOUT, % smem)
     if (const char* env = std::getenv("PDCS_CARVEOUT")) {
       const int pc = std::atoi(env);

@@ -125,6 +125,7 @@ def test_nccl_graph_path_bit_identical_to_host_loop(monkeypatch):
     import paper_2505_00311_b200 as P
     prog = gen_mixed(400, 60, 200, seed=12, soc_dims=(3, 60))
     out = {}
+    monkeypatch.setenv("PDCS_AR_CHUNKS", "3")      # the chunked, overlapped all-reduce inside the graph
     for mode in ("1", "0"):
         monkeypatch.setenv("PDCS_DIST_GRAPH", mode)
         g = P.PdcsSolver(prog, nccl_id=P.pdcs_nccl_unique_id(), rank=0, world=1)

@@ -209,3 +209,27 @@ def test_loopback_failing_rank_does_not_hang_peers(P, monkeypatch):
         t.join(timeout=120)
     assert not any(t.is_alive() for t in ts)
     assert isinstance(out[0], P.PdcsError) and isinstance(out[1], P.PdcsError), out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_chunked_overlapped_allreduce_is_bit_identical(P, world, monkeypatch):
+    """The K^T y partial all-reduced in row chunks on a second stream, each
+    overlapping the next chunk's sums (PDCS_AR_CHUNKS), gives the same bits as
+    one all-reduce of the whole vector: the reduction is elementwise."""
+    monkeypatch.setenv("PDCS_TILED", "0")
+    prog = CASES["mixed"]()
+    out = {}
+    for chunks in ("1", "3"):
+        monkeypatch.setenv("PDCS_AR_CHUNKS", chunks)
+        group, parts, ranks = make_ranks(P, prog, world)
+        on_all([lambda g=g: g.iterate(150) for g in ranks])
+        assert_ranks_identical(ranks)
+        out[chunks] = (ranks[0].get_state(), [g.get_iterate(P.CURRENT)[1] for g in ranks])
+        for g in ranks:
+            g.close()
+        P.pdcs_loopback_destroy(group)
+    (sa, ya), (sb, yb) = out["1"], out["3"]
+    assert np.array_equal(sa["sc"], sb["sc"])
+    for k in ("x", "x0", "xsum"):
+        assert np.array_equal(sa[k], sb[k]), k
+    assert all(np.array_equal(a, b) for a, b in zip(ya, yb))

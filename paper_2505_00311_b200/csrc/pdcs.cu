@@ -773,6 +773,7 @@ struct pdcs_ctx {
     DBuf<int32_t> rowptr, col_d, blkb;
     DBuf<uint16_t> col_s, srow;
     DBuf<double> val_s, val_d, scratch;
+    DBuf<TCItem> citem;
     int g_partial = 0, g_combine = 0;
     int64_t slot = 0;
     float tune_csr_ms = 0.f, tune_tiled_ms = 0.f;
@@ -1423,10 +1424,17 @@ struct pdcs_ctx {
       else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_partial<1>, kTThreads, tiled_smem(D)));
     }
     D.g_partial = (int)std::max<int64_t>(1, std::min<int64_t>(M.nwork, (int64_t)sms * std::max(occ, 1)));
-    int64_t slabs = 0;
-    for (const TChunk& c : H.chunk) slabs += (c.nrows + kThreads - 1) / kThreads;
+    std::vector<TCItem> citems;                // combine items (k_tiled_combine)
+    for (size_t c = 0; c < H.chunk.size(); ++c) {
+      const TChunk& C = H.chunk[c];
+      const int step = C.ngroups >= kCombWideG ? kCombRowsWide : kThreads;
+      for (int32_t r0 = 0; r0 < C.nrows; r0 += step) citems.push_back(TCItem{(int32_t)c, r0});
+    }
+    upload(D.citem, citems, st);
+    M.citem = D.citem.p;
+    M.ncitem = (int64_t)citems.size();
     H = TiledHost();                           // host copy no longer needed
-    D.g_combine = (int)std::max<int64_t>(1, std::min<int64_t>(slabs, (int64_t)sms * 4));
+    D.g_combine = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)citems.size(), (int64_t)sms * 4));
     // Setup-time autotune: keep the tiled copy only if it beats the CSR kernel
     // by >= 10% on this matrix (gather locality decides).
     if (!env) {
@@ -1482,7 +1490,7 @@ struct pdcs_ctx {
         D.on = false;
         D.work.free_(); D.chunk.free_(); D.seg.free_(); D.rowptr.free_(); D.srow.free_(); D.col_d.free_(); D.col_s.free_();
         D.blkb.free_();
-        D.val_s.free_(); D.val_d.free_(); D.scratch.free_();
+        D.val_s.free_(); D.val_d.free_(); D.scratch.free_(); D.citem.free_();
       }
     }
   }

@@ -46,6 +46,15 @@ struct TChunk {
   int32_t ngroups;
   int64_t scratch;   // offset (in doubles) of the chunk's partials: ngroups * nrows * ELEM
 };
+// One item of the combine: rows [r0, r0 + kThreads) of a chunk with few groups,
+// or rows [r0, r0 + kCombRowsWide) of a chunk with >= kCombWideG groups, whose
+// group sums are split over kCombLanes lanes per row (Lasso K^T: ~150 groups).
+struct TCItem {
+  int32_t chunk, r0;
+};
+constexpr int kCombLanes = 8;
+constexpr int kCombRowsWide = 256 / kCombLanes;
+constexpr int kCombWideG = 16;
 struct TWork {
   int32_t chunk, group, s0, s1;   // segments [s0, s1): direct ones run first, staged via batches
   int32_t b0, b1;                 // TMA batches [b0, b1) of the staged segments
@@ -72,6 +81,8 @@ struct TiledMat {
   const int32_t* col_d = nullptr;
   const TBatch* batch = nullptr;
   const int32_t* blkb = nullptr;      // sliced staged segments: first quad of every warp block
+  const TCItem* citem = nullptr;      // combine items (k_tiled_combine)
+  int64_t ncitem = 0;
 };
 
 // Shared-memory loads with 32-bit shared addresses (the tile pointer would
@@ -637,6 +648,12 @@ __global__ void __launch_bounds__(kTThreads, ELEM == 1 ? PDCS_TS_MINB1 : PDCS_TP
 }
 
 // Sum the partials of every row (fixed order) and run the fused epilogue.
+// Items of chunks with few groups: one thread per row, the groups summed in
+// order with loads batched 8 deep.  Items of chunks with many groups (the long
+// rows of Lasso's K^T have ~150 per chunk; one thread per row serialised ~20
+// dependent load batches and made the tail of the kernel): kCombLanes lanes per
+// row, lane l summing groups l, l+8, ..., then a fixed shuffle tree.  Both
+// orders are fixed, so results are reproducible run to run.
 template <class Epi, int ELEM>
 __global__ void __launch_bounds__(kThreads) k_tiled_combine(TiledMat M, const double* __restrict__ scratch,
                                                             Epi epi, const Ctl* ctl, double* part,
@@ -645,37 +662,64 @@ __global__ void __launch_bounds__(kThreads) k_tiled_combine(TiledMat M, const do
   if (!epi.active()) return;
   Acc<Epi::NA> acc;
   acc.zero();
-  // items are (chunk, slab of blockDim rows); slabs of one chunk are consecutive
-  const int64_t per = (kTRows + blockDim.x - 1) / blockDim.x;   // slabs per chunk (upper bound)
-  for (int64_t it = blockIdx.x; it < M.nchunk * per; it += gridDim.x) {
-    const int64_t c = it / per;
-    const int slab = (int)(it % per);
-    const TChunk C = M.chunk[c];
-    const int r = slab * blockDim.x + threadIdx.x;
-    if (r < C.nrows) {
-      const double* src = scratch + C.scratch;
-      // groups summed in order; loads batched 8 deep (chunks of long rows have
-      // ~100 groups, a load-add chain would serialise their latencies)
+  for (int64_t it = blockIdx.x; it < M.ncitem; it += gridDim.x) {
+    const TCItem I = M.citem[it];
+    const TChunk C = M.chunk[I.chunk];
+    const double* src = scratch + C.scratch;
+    if (C.ngroups < kCombWideG) {
+      const int r = I.r0 + threadIdx.x;
+      if (r < C.nrows) {
+        double s1 = 0.0, s2 = 0.0;
+        int g = 0;
+        for (; g + 8 <= C.ngroups; g += 8) {
+          double u1[8], u2[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            u1[k] = src[((int64_t)(g + k) * C.nrows + r) * ELEM];
+            if (ELEM == 2) u2[k] = src[((int64_t)(g + k) * C.nrows + r) * ELEM + 1];
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            s1 += u1[k];
+            if (ELEM == 2) s2 += u2[k];
+          }
+        }
+        for (; g < C.ngroups; ++g) {
+          s1 += src[((int64_t)g * C.nrows + r) * ELEM];
+          if (ELEM == 2) s2 += src[((int64_t)g * C.nrows + r) * ELEM + 1];
+        }
+        epi.row(C.row0 + r, s1, s2, acc);
+      }
+    } else {
+      const int lane = threadIdx.x % kCombLanes;
+      const int r = I.r0 + threadIdx.x / kCombLanes;
       double s1 = 0.0, s2 = 0.0;
-      int g = 0;
-      for (; g + 8 <= C.ngroups; g += 8) {
-        double u1[8], u2[8];
+      if (r < C.nrows) {
+        int g = lane;
+        for (; g + 3 * kCombLanes < C.ngroups; g += 4 * kCombLanes) {
+          double u1[4], u2[4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          u1[k] = src[((int64_t)(g + k) * C.nrows + r) * ELEM];
-          if (ELEM == 2) u2[k] = src[((int64_t)(g + k) * C.nrows + r) * ELEM + 1];
+          for (int k = 0; k < 4; ++k) {
+            u1[k] = src[((int64_t)(g + k * kCombLanes) * C.nrows + r) * ELEM];
+            if (ELEM == 2) u2[k] = src[((int64_t)(g + k * kCombLanes) * C.nrows + r) * ELEM + 1];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            s1 += u1[k];
+            if (ELEM == 2) s2 += u2[k];
+          }
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          s1 += u1[k];
-          if (ELEM == 2) s2 += u2[k];
+        for (; g < C.ngroups; g += kCombLanes) {
+          s1 += src[((int64_t)g * C.nrows + r) * ELEM];
+          if (ELEM == 2) s2 += src[((int64_t)g * C.nrows + r) * ELEM + 1];
         }
       }
-      for (; g < C.ngroups; ++g) {
-        s1 += src[((int64_t)g * C.nrows + r) * ELEM];
-        if (ELEM == 2) s2 += src[((int64_t)g * C.nrows + r) * ELEM + 1];
+#pragma unroll
+      for (int o = kCombLanes / 2; o >= 1; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o, kCombLanes);
+        if (ELEM == 2) s2 += __shfl_xor_sync(0xffffffffu, s2, o, kCombLanes);
       }
-      epi.row(C.row0 + r, s1, s2, acc);
+      if (lane == 0 && r < C.nrows) epi.row(C.row0 + r, s1, s2, acc);
     }
   }
   if (part) cta_write_partials<Epi::NA>(acc, part, slot0 + blockIdx.x);

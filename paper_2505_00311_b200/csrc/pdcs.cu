@@ -1427,14 +1427,14 @@ struct pdcs_ctx {
     std::vector<TCItem> citems;                // combine items (k_tiled_combine)
     for (size_t c = 0; c < H.chunk.size(); ++c) {
       const TChunk& C = H.chunk[c];
-      const int step = C.ngroups >= kCombWideG ? kCombRowsWide : kThreads;
+      const int step = C.ngroups >= kCombWideG ? kCombRowsWide : C.ngroups <= 2 ? kCombRowsNarrow : kThreads;
       for (int32_t r0 = 0; r0 < C.nrows; r0 += step) citems.push_back(TCItem{(int32_t)c, r0});
     }
     upload(D.citem, citems, st);
     M.citem = D.citem.p;
     M.ncitem = (int64_t)citems.size();
     H = TiledHost();                           // host copy no longer needed
-    D.g_combine = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)citems.size(), (int64_t)sms * 4));
+    D.g_combine = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)citems.size(), (int64_t)sms * 8));
     // Setup-time autotune: keep the tiled copy only if it beats the CSR kernel
     // by >= 10% on this matrix (gather locality decides).
     if (!env) {
@@ -2168,7 +2168,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     int64_t s = 0;
     ctx->slot_pe = s; s += ctx->g_pe;
     for (int c = 0; c < kNClass; ++c) if (ctx->pcls[c].count) { ctx->pcls[c].slot = s; s += ctx->pcls[c].grid; }
-    ctx->slot_spmv = s; s += std::max<int64_t>(ctx->K.plan.total_cta, (int64_t)ctx->sms * 4);
+    ctx->slot_spmv = s; s += std::max<int64_t>(ctx->K.plan.total_cta, (int64_t)ctx->sms * 8);   // also the tiled combine and panel finish grids
     for (int c = 0; c < kNClass; ++c) if (ctx->rcls[c].count) { ctx->rcls[c].slot = s; s += ctx->rcls[c].grid; }
     ctx->nslot_trial = s;
     int64_t ks = 0;

@@ -46,15 +46,17 @@ struct TChunk {
   int32_t ngroups;
   int64_t scratch;   // offset (in doubles) of the chunk's partials: ngroups * nrows * ELEM
 };
-// One item of the combine: rows [r0, r0 + kThreads) of a chunk with few groups,
-// or rows [r0, r0 + kCombRowsWide) of a chunk with >= kCombWideG groups, whose
-// group sums are split over kCombLanes lanes per row (Lasso K^T: ~150 groups).
+// One item of the combine: rows [r0, r0 + kCombRowsNarrow) of a chunk with <= 2
+// groups (4 rows per thread), rows [r0, r0 + kThreads) of a chunk with a few
+// more, or rows [r0, r0 + kCombRowsWide) of a chunk with >= kCombWideG groups,
+// whose group sums are split over kCombLanes lanes per row (Lasso K^T: ~150).
 struct TCItem {
   int32_t chunk, r0;
 };
 constexpr int kCombLanes = 8;
 constexpr int kCombRowsWide = 256 / kCombLanes;
 constexpr int kCombWideG = 16;
+constexpr int kCombRowsNarrow = 4 * 256;   // rows of an item of a chunk with <= 2 groups
 struct TWork {
   int32_t chunk, group, s0, s1;   // segments [s0, s1): direct ones run first, staged via batches
   int32_t b0, b1;                 // TMA batches [b0, b1) of the staged segments
@@ -666,7 +668,32 @@ __global__ void __launch_bounds__(kThreads) k_tiled_combine(TiledMat M, const do
     const TCItem I = M.citem[it];
     const TChunk C = M.chunk[I.chunk];
     const double* src = scratch + C.scratch;
-    if (C.ngroups < kCombWideG) {
+    if (C.ngroups <= 2) {
+      // the common case (most chunks hold one or two work items): the item is
+      // kCombRowsNarrow rows, kCombRowsNarrow / blockDim per thread, every
+      // partial load of the thread issued before the first epilogue
+      constexpr int RPT = kCombRowsNarrow / kThreads;
+      double s1[RPT], s2[RPT];
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        const int r = I.r0 + threadIdx.x + k * kThreads;
+        s1[k] = 0.0;
+        s2[k] = 0.0;
+        if (r < C.nrows) {
+          s1[k] = src[(int64_t)r * ELEM];
+          if (ELEM == 2) s2[k] = src[(int64_t)r * ELEM + 1];
+          if (C.ngroups == 2) {
+            s1[k] += src[((int64_t)C.nrows + r) * ELEM];
+            if (ELEM == 2) s2[k] += src[((int64_t)C.nrows + r) * ELEM + 1];
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        const int r = I.r0 + threadIdx.x + k * kThreads;
+        if (r < C.nrows) epi.row(C.row0 + r, s1[k], s2[k], acc);
+      }
+    } else if (C.ngroups < kCombWideG) {
       const int r = I.r0 + threadIdx.x;
       if (r < C.nrows) {
         double s1 = 0.0, s2 = 0.0;

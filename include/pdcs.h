@@ -265,6 +265,17 @@ void pdcs_destroy(pdcs_ctx *ctx);
 int pdcs_tiled_build_host(const int64_t *row_ptr, const int32_t *col, int64_t rows, int64_t nvec, int elem,
                           double *out);
 
+/* Device diagnostic (needs a GPU): build the column-tiled layout both ways the
+ * library can, all on the host, and deferred (host structure, shared-memory
+ * bank balancing and sliced re-layout on the device; the solver's default,
+ * PDCS_TILE_DEVICE=0 turns it off), and compare them entry by entry.
+ * out[0] = mismatching entries (column ids, value permutation, row pointers,
+ * block bases, segment descriptors); out[1] = all-host ms; out[2] = deferred
+ * host ms; out[3] = device ms; out[4] = layout entries.  Returns 5, 0 on bad
+ * arguments (or when the deferred build does not apply), -1 on a CUDA error. */
+int pdcs_tiled_device_check(const int64_t *row_ptr, const int32_t *col, int64_t rows, int64_t nvec, int elem,
+                            double *out);
+
 /* Host-only diagnostic, no GPU needed: build the column-tiled layout
  * of a CSR structure (row_ptr[rows+1], col[nnz], valid and
  * sorted; elem = 2 for the (x^, x) pair gather of K, 1 for the y gather of

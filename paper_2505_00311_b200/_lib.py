@@ -102,6 +102,8 @@ def lib():
         L.pdcs_tiled_layout_stats.restype = C.c_int
         L.pdcs_tiled_build_host.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
         L.pdcs_tiled_build_host.restype = C.c_int
+        L.pdcs_tiled_device_check.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+        L.pdcs_tiled_device_check.restype = C.c_int
         L.pdcs_proj_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, P_I32, P_I64, C.c_int64, C.c_int]
         L.pdcs_proj_run.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.pdcs_proj_info.argtypes = [C.c_void_p, P_I64, P_I64]
@@ -117,7 +119,7 @@ EXPORTED = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterat
             "pdcs_destroy", "pdcs_nccl_unique_id", "pdcs_get_scalars", "pdcs_get_state",
             "pdcs_set_state", "pdcs_tiled_layout_stats", "pdcs_proj_create", "pdcs_proj_run",
             "pdcs_proj_info", "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host",
-            "pdcs_loopback_create", "pdcs_loopback_destroy", "pdcs_create_loopback"]
+            "pdcs_loopback_create", "pdcs_loopback_destroy", "pdcs_create_loopback", "pdcs_tiled_device_check"]
 
 STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e_prev", "best_e", "k",
               "total", "trials", "restarts"]
@@ -223,6 +225,16 @@ def pdcs_tiled_build_host(row_ptr, col, rows, nvec, elem) -> dict:
     if n != 3:
         raise ValueError("pdcs_tiled_build_host: bad arguments")
     return dict(build_ms=out[0], ranges_ms=out[1], staged=int(out[2]))
+
+
+def pdcs_tiled_device_check(row_ptr, col, rows, nvec, elem) -> dict:
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    c = np.ascontiguousarray(col, np.int32)
+    out = np.zeros(5)
+    k = lib().pdcs_tiled_device_check(_ptr(rp), _ptr(c), rows, nvec, elem, out.ctypes.data_as(P_D))
+    if k != 5:
+        raise PdcsError(7 if k < 0 else 1, "pdcs_tiled_device_check failed" if k < 0 else "not applicable")
+    return dict(mismatches=out[0], host_ms=out[1], deferred_host_ms=out[2], device_ms=out[3], entries=out[4])
 
 
 def pdcs_set_tolerance(ctx, tol, time_limit_s=0.0):

@@ -104,6 +104,16 @@ struct TiledHost {
   std::vector<TiledHost> parts;
   std::vector<size_t> o_s, o_d, o_rp, o_bb;
   size_t tot_s = 0, tot_d = 0, tot_rp = 0, tot_bb = 0;
+  // Deferred build (device bank balancing + slicing): col_s /
+  // perm_s hold the unbalanced row-major quads ("pre"); fin_s is the size of
+  // the final sliced layout; dseg the staged segments, dblk their warp blocks
+  // (dseg index, block).  Parts mode: o_pre offsets of the pre arrays.
+  bool defer = false;
+  int64_t fin_s = 0;
+  std::vector<TDefer> dseg;
+  std::vector<int2> dblk;
+  std::vector<size_t> o_pre;
+  size_t tot_pre = 0;
   size_t n_s() const { return parts.empty() ? col_s.size() : tot_s; }
   size_t n_d() const { return parts.empty() ? col_d.size() : tot_d; }
 };
@@ -205,6 +215,43 @@ void slice_segments(TiledHost& H, int32_t s0, int32_t s1, int32_t nr) {
   H.perm_s.resize(base);
   H.col_s.insert(H.col_s.end(), nc.begin(), nc.end());
   H.perm_s.insert(H.perm_s.end(), np.begin(), np.end());
+}
+
+// The deferred build's counterpart of slice_segments: the final (sliced)
+// offsets, warp-block bases and the device work list of the staged segments
+// among [s0, s1), with the same sizes and alignment as slice_segments; no data
+// moves (k_tile_balance / k_tile_slice do that on the device).
+void slice_plan(TiledHost& H, int32_t s0, int32_t s1, int32_t nr) {
+  bool any = false;
+  for (int32_t si = s0; si < s1; ++si) any |= H.seg[si].tile >= 0;
+  if (!any) return;
+  const int64_t base = (H.fin_s + 7) & ~(int64_t)7;     // the first staged segment's start when built in place
+  int64_t cur = 0;
+  for (int32_t si = s0; si < s1; ++si) {
+    TSeg& S = H.seg[si];
+    if (S.tile < 0) continue;
+    const int32_t* rp = H.rowptr.data() + S.rp;
+    const int64_t off = ((base + cur + 63) & ~(int64_t)63) - base;
+    const int rpw = 32 / S.V;
+    const int nblk = tiled_blocks(nr, S.V);
+    S.bb = (int64_t)H.blkb.size();
+    const int32_t di = (int32_t)H.dseg.size();
+    int64_t q = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+      H.blkb.push_back((int32_t)q);
+      int32_t tmax = 0;
+      for (int a = 0; a < rpw && blk * rpw + a < nr; ++a) {
+        const int32_t nq = rp[blk * rpw + a + 1] - rp[blk * rpw + a];
+        tmax = std::max(tmax, (nq + S.V - 1) / S.V);
+      }
+      q += 32 * (int64_t)tmax;
+      H.dblk.push_back(make_int2(di, blk));
+    }
+    H.dseg.push_back(TDefer{S.nz, base + off, S.rp, S.bb, nr, S.V});
+    cur = off + 4 * q;
+    S.nz = base + off;
+  }
+  H.fin_s = base + cur;
 }
 
 // Shared-memory bank balancing of one staged segment (in place).  At every
@@ -427,13 +474,14 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
         }
       }
     const bool balance = !std::getenv("PDCS_TILE_BALANCE") || std::atoi(std::getenv("PDCS_TILE_BALANCE"));
-    if (balance)
+    if (balance && !H.defer)
       for (int k = 0; k < nseg; ++k) {
         const TSeg& S = H.seg[s_begin + k];
         if (S.tile < 0 || S.V > 32) continue;
         balance_banks(H.col_s.data() + S.nz, H.perm_s.data() + S.nz, H.rowptr.data() + rpbase[k], nr, S.V, elem);
       }
-    if (H.sliced) slice_segments(H, s_begin, s_begin + nseg, nr);
+    if (H.defer) slice_plan(H, s_begin, s_begin + nseg, nr);
+    else if (H.sliced) slice_segments(H, s_begin, s_begin + nseg, nr);
     // work items: consecutive segments up to group_nz nonzeros; the staged
     // segments of an item are cut into TMA batches of <= kBQ quads (row-major
     // layout only, PDCS_TMA=1)
@@ -483,7 +531,7 @@ void build_tiled_range(const int64_t* ptr, const int32_t* col, int64_t row_a, in
 // built on host threads (build_tiled_range) and concatenated in order with
 // their offsets rebased, so the result does not depend on the thread count.
 void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
-                 TiledHost& H, bool keep_parts = false) {
+                 TiledHost& H, bool keep_parts = false, bool defer = false) {
   const auto t_start = std::chrono::steady_clock::now();
   // work-item size: enough items to fill the GPU several times over, no more
   // partial groups per chunk than needed (PDCS_TILE_GROUP overrides)
@@ -505,8 +553,13 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
   H.elem = elem;
   H.tma = tiled_tma_env();
   H.sliced = tiled_sliced();
+  // the deferred build needs the parts mode (the device assembles) and the
+  // sliced, bank-balanced layout; PDCS_TILE_DEVICE=0 keeps the host build
+  const bool bal_env = !std::getenv("PDCS_TILE_BALANCE") || std::atoi(std::getenv("PDCS_TILE_BALANCE"));
+  H.defer = defer && keep_parts && H.sliced && bal_env &&
+            !(std::getenv("PDCS_TILE_DEVICE") && std::atoi(std::getenv("PDCS_TILE_DEVICE")) == 0);
   std::vector<TiledHost> part(nth);
-  for (auto& P : part) { P.T = H.T; P.sliced = H.sliced; P.tma = H.tma; }
+  for (auto& P : part) { P.T = H.T; P.sliced = H.sliced; P.tma = H.tma; P.defer = H.defer; }
   std::vector<std::thread> th;
   for (int w = 0; w < nth; ++w)
     th.emplace_back([&, w] { build_tiled_range(ptr, col, cut[w], cut[w + 1], nvec, elem, group_nz, part[w]); });
@@ -518,13 +571,15 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
   // row pointers, block bases) are copied verbatim, one thread per part, into
   // vectors sized once (the serial inserts had taken ~25% of the build).
   const int np = (int)part.size();
-  std::vector<size_t> o_s(np), o_d(np), o_rp(np), o_bb(np);
-  size_t ns = 0, nd = 0, nrp = 0, nbb = 0;
+  std::vector<size_t> o_s(np), o_d(np), o_rp(np), o_bb(np), o_pre(np);
+  size_t ns = 0, nd = 0, nrp = 0, nbb = 0, npre = 0;
   for (int w = 0; w < np; ++w) {
     const TiledHost& P = part[w];
     ns = (ns + 63) & ~(size_t)63;              // keep segment starts 512-B aligned (values)
-    o_s[w] = ns; o_d[w] = nd; o_rp[w] = nrp; o_bb[w] = nbb;
-    ns += P.col_s.size(); nd += P.col_d.size(); nrp += P.rowptr.size(); nbb += P.blkb.size();
+    o_s[w] = ns; o_d[w] = nd; o_rp[w] = nrp; o_bb[w] = nbb; o_pre[w] = npre;
+    ns += H.defer ? (size_t)P.fin_s : P.col_s.size();
+    nd += P.col_d.size(); nrp += P.rowptr.size(); nbb += P.blkb.size();
+    npre += H.defer ? P.col_s.size() : 0;
   }
   for (int w = 0; w < np; ++w) {
     TiledHost& P = part[w];
@@ -544,6 +599,12 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
     for (TChunk C : P.chunk) { C.scratch += H.scratch; H.chunk.push_back(C); }
     H.scratch += P.scratch;
     H.staged += P.staged;
+    const int32_t dbase = (int32_t)H.dseg.size();
+    for (TDefer D : P.dseg) {
+      D.src += (int64_t)o_pre[w]; D.dst += (int64_t)o_s[w]; D.rp += (int64_t)o_rp[w]; D.bb += (int64_t)o_bb[w];
+      H.dseg.push_back(D);
+    }
+    for (int2 b : P.dblk) H.dblk.push_back(make_int2(b.x + dbase, b.y));
   }
   if (keep_parts) {
     H.o_s = std::move(o_s); H.o_d = std::move(o_d); H.o_rp = std::move(o_rp); H.o_bb = std::move(o_bb);
@@ -551,7 +612,11 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
     H.tot_d = nd;
     H.tot_rp = nrp + 8;        // TMA row-pointer slices are rounded up to 16 B
     H.tot_bb = nbb + 1;        // never empty (device upload)
-    for (auto& P : part) { P.seg.clear(); P.batch.clear(); P.work.clear(); P.chunk.clear(); }
+    H.o_pre = std::move(o_pre);
+    H.tot_pre = npre;
+    for (auto& P : part) {
+      P.seg.clear(); P.batch.clear(); P.work.clear(); P.chunk.clear(); P.dseg.clear(); P.dblk.clear();
+    }
     H.parts = std::move(part);
     H.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     return;
@@ -778,6 +843,7 @@ struct pdcs_ctx {
     int64_t slot = 0;
     float tune_csr_ms = 0.f, tune_tiled_ms = 0.f;
     double build_ms = 0.0;                     // host build of the format
+    double device_build_ms = 0.0;              // deferred build: device balancing + slicing
   } tK, tKT;
   // L2 column panels of K~ and K~^T (panels.cuh), kept by a setup autotune when
   // the gathered vector exceeds L2
@@ -1366,14 +1432,45 @@ struct pdcs_ctx {
       auto put = [&](auto* dst, const auto& v, size_t off) {
         if (!v.empty()) CK(cudaMemcpyAsync(dst + off, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, st));
       };
+      DBuf<uint16_t> pcol;                     // deferred build: the unbalanced row-major quads
+      DBuf<int32_t> pperm;
+      if (H.defer) {
+        pcol.alloc(std::max<size_t>(H.tot_pre, 1));
+        pperm.alloc(std::max<size_t>(H.tot_pre, 1));
+      }
       for (size_t w = 0; w < H.parts.size(); ++w) {
         const TiledHost& P = H.parts[w];
         put(D.rowptr.p, P.rowptr, H.o_rp[w]);
         put(D.srow.p, P.srow, H.o_rp[w]);
-        put(D.col_s.p, P.col_s, H.o_s[w]);
-        put(perm.p, P.perm_s, H.o_s[w]);
+        if (H.defer) {
+          put(pcol.p, P.col_s, H.o_pre[w]);
+          put(pperm.p, P.perm_s, H.o_pre[w]);
+        } else {
+          put(D.col_s.p, P.col_s, H.o_s[w]);
+          put(perm.p, P.perm_s, H.o_s[w]);
+        }
         put(D.col_d.p, P.col_d, H.o_d[w]);
         put(D.blkb.p, P.blkb, H.o_bb[w]);
+      }
+      if (H.defer && !H.dblk.empty()) {
+        // bank balancing and sliced re-layout on the device (tiled.cuh)
+        const auto t0 = std::chrono::steady_clock::now();
+        DBuf<TDefer> dseg;
+        DBuf<int2> dblk;
+        upload(dseg, H.dseg, st);
+        upload(dblk, H.dblk, st);
+        DBuf<uint16_t> bcol, ncol;
+        DBuf<int32_t> bperm, nperm;
+        bcol.alloc(H.tot_pre); ncol.alloc(H.tot_pre); bperm.alloc(H.tot_pre); nperm.alloc(H.tot_pre);
+        const int64_t nb = (int64_t)H.dblk.size();
+        const int tb = 128;
+        k_tile_balance<<<(int)((nb + tb - 1) / tb), tb, 0, st>>>(dseg.p, dblk.p, nb, elem, D.rowptr.p, pcol.p,
+                                                                 pperm.p, bcol.p, bperm.p, ncol.p, nperm.p);
+        k_tile_slice<<<(int)((nb + tb - 1) / tb), tb, 0, st>>>(dseg.p, dblk.p, nb, D.rowptr.p, D.blkb.p, ncol.p,
+                                                               nperm.p, D.col_s.p, perm.p);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        D.device_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       }
     }
     D.val_s.alloc(std::max<size_t>(H.n_s(), 1));
@@ -1427,7 +1524,7 @@ struct pdcs_ctx {
     std::vector<TCItem> citems;                // combine items (k_tiled_combine)
     for (size_t c = 0; c < H.chunk.size(); ++c) {
       const TChunk& C = H.chunk[c];
-      const int step = C.ngroups >= kCombWideG ? kCombRowsWide : C.ngroups <= 2 ? kCombRowsNarrow : kThreads;
+      const int step = C.ngroups >= kCombWideG ? kCombRowsWide : C.ngroups <= kCombNarrowG ? kCombRowsNarrow : kThreads;
       for (int32_t r0 = 0; r0 < C.nrows; r0 += step) citems.push_back(TCItem{(int32_t)c, r0});
     }
     upload(D.citem, citems, st);
@@ -1868,7 +1965,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     // tiled format of K~ (structure only) on host threads, overlapping the uploads
     // and the device transpose below; joined before this call returns
     ctx->thK = std::thread([ctx, hcolp, m, n] {
-      build_tiled(ctx->hptr.data(), hcolp, m, n, 2, ctx->hK, true);
+      build_tiled(ctx->hptr.data(), hcolp, m, n, 2, ctx->hK, true, true);
     });
     struct Joiner {
       std::thread& t;
@@ -1989,7 +2086,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     ctx->hKTcol.resize(nnz);
     if (nnz) CK(cudaMemcpy(ctx->hKTcol.data(), ctx->KTcol.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
     ctx->thKT = std::thread([ctx, m, n] {
-      build_tiled(ctx->hKTptr.data(), ctx->hKTcol.data(), n, m, 1, ctx->hKT, true);
+      build_tiled(ctx->hKTptr.data(), ctx->hKTcol.data(), n, m, 1, ctx->hKT, true, true);
     });
     upload(ctx->planrows, rowstore, st);
     ctx->patch_plan(ctx->K);
@@ -2682,6 +2779,80 @@ int pdcs_tiled_build_host(const int64_t* row_ptr, const int32_t* col, int64_t ro
   build_tiled(row_ptr, col, rows, nvec, elem, H, true);
   out[0] = H.build_ms; out[1] = H.ranges_ms; out[2] = (double)H.staged;
   return 3;
+}
+
+// Device check of the deferred tiled build: the layout built by the host with
+// the bank balancing and slicing on the device (the solver's default) against
+// the all-host build, entry by entry.  out[0] = mismatching entries over the
+// column ids, value permutation, row pointers, block bases and segment
+// descriptors; out[1] = all-host build ms; out[2] = deferred host ms; out[3] =
+// device ms; out[4] = final layout entries.  Returns 5, 0 on bad arguments, -1
+// on a CUDA error.
+int pdcs_tiled_device_check(const int64_t* row_ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
+                            double* out) {
+  if (!row_ptr || (!col && row_ptr[rows] > 0) || rows < 0 || nvec <= 0 || (elem != 1 && elem != 2) || !out)
+    return 0;
+  try {
+    TiledHost A, B;
+    build_tiled(row_ptr, col, rows, nvec, elem, A);                  // all host
+    build_tiled(row_ptr, col, rows, nvec, elem, B, true, true);      // deferred, parts
+    if (!B.defer) return 0;
+    cudaStream_t st = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    DBuf<int32_t> rp, bb, perm, pperm, bperm, nperm;
+    DBuf<uint16_t> cs, pcol, bcol, ncol;
+    rp.alloc(B.tot_rp); bb.alloc(B.tot_bb); cs.alloc(B.tot_s); perm.alloc(B.tot_s);
+    pcol.alloc(std::max<size_t>(B.tot_pre, 1)); pperm.alloc(std::max<size_t>(B.tot_pre, 1));
+    CK(cudaMemset(rp.p, 0, B.tot_rp * sizeof(int32_t)));
+    CK(cudaMemset(bb.p, 0, B.tot_bb * sizeof(int32_t)));
+    CK(cudaMemset(cs.p, 0, B.tot_s * sizeof(uint16_t)));
+    CK(cudaMemset(perm.p, 0xff, B.tot_s * sizeof(int32_t)));
+    auto put = [&](auto* dst, const auto& v, size_t off) {
+      if (!v.empty()) CK(cudaMemcpy(dst + off, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice));
+    };
+    for (size_t w = 0; w < B.parts.size(); ++w) {
+      put(rp.p, B.parts[w].rowptr, B.o_rp[w]);
+      put(bb.p, B.parts[w].blkb, B.o_bb[w]);
+      put(pcol.p, B.parts[w].col_s, B.o_pre[w]);
+      put(pperm.p, B.parts[w].perm_s, B.o_pre[w]);
+    }
+    const int64_t nb = (int64_t)B.dblk.size();
+    if (nb) {
+      DBuf<TDefer> dseg;
+      DBuf<int2> dblk;
+      upload(dseg, B.dseg, st);
+      upload(dblk, B.dblk, st);
+      bcol.alloc(B.tot_pre); ncol.alloc(B.tot_pre); bperm.alloc(B.tot_pre); nperm.alloc(B.tot_pre);
+      k_tile_balance<<<(int)((nb + 127) / 128), 128>>>(dseg.p, dblk.p, nb, elem, rp.p, pcol.p, pperm.p, bcol.p,
+                                                       bperm.p, ncol.p, nperm.p);
+      k_tile_slice<<<(int)((nb + 127) / 128), 128>>>(dseg.p, dblk.p, nb, rp.p, bb.p, ncol.p, nperm.p, cs.p, perm.p);
+      CK(cudaGetLastError());
+    }
+    CK(cudaDeviceSynchronize());
+    const double dev_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<uint16_t> hc(B.tot_s);
+    std::vector<int32_t> hp(B.tot_s), hr(B.tot_rp), hb(B.tot_bb);
+    CK(cudaMemcpy(hc.data(), cs.p, B.tot_s * sizeof(uint16_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hp.data(), perm.p, B.tot_s * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hr.data(), rp.p, B.tot_rp * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hb.data(), bb.p, B.tot_bb * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    double bad = 0;
+    if (A.col_s.size() != hc.size() || A.rowptr.size() != hr.size() || A.blkb.size() != hb.size() ||
+        A.seg.size() != B.seg.size())
+      bad = 1e18;
+    else {
+      for (size_t i = 0; i < hc.size(); ++i) bad += (A.col_s[i] != hc[i]) + (A.perm_s[i] != hp[i]);
+      for (size_t i = 0; i < hr.size(); ++i) bad += A.rowptr[i] != hr[i];
+      for (size_t i = 0; i < hb.size(); ++i) bad += A.blkb[i] != hb[i];
+      for (size_t i = 0; i < A.seg.size(); ++i)
+        bad += A.seg[i].nz != B.seg[i].nz || A.seg[i].bb != B.seg[i].bb || A.seg[i].rp != B.seg[i].rp ||
+               A.seg[i].V != B.seg[i].V || A.seg[i].tile != B.seg[i].tile;
+    }
+    out[0] = bad; out[1] = A.build_ms; out[2] = B.build_ms; out[3] = dev_ms; out[4] = (double)hc.size();
+    return 5;
+  } catch (...) {
+    return -1;
+  }
 }
 
 int pdcs_tiled_layout_stats(const int64_t* row_ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,

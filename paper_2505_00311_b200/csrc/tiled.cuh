@@ -40,13 +40,21 @@ struct TSeg {
   int64_t nz;        // offset of the segment's entries in its pool (staged: in entries, = 4 * quads)
   int64_t bb;        // staged, >= 0: sliced layout, offset of the segment's warp-block bases in blkb
 };
+// A staged segment of the deferred build: its bank balancing and
+// sliced re-layout run on the device.  src: first entry of its unbalanced
+// row-major quads in the "pre" arrays; dst: first entry in the final sliced
+// arrays; rp / bb: its row pointers and warp-block bases; nr rows, V lanes.
+struct TDefer {
+  int64_t src, dst, rp, bb;
+  int32_t nr, V;
+};
 struct TChunk {
   int64_t row0;
   int32_t nrows;
   int32_t ngroups;
   int64_t scratch;   // offset (in doubles) of the chunk's partials: ngroups * nrows * ELEM
 };
-// One item of the combine: rows [r0, r0 + kCombRowsNarrow) of a chunk with <= 2
+// One item of the combine: rows [r0, r0 + kCombRowsNarrow) of a chunk with <= 4
 // groups (4 rows per thread), rows [r0, r0 + kThreads) of a chunk with a few
 // more, or rows [r0, r0 + kCombRowsWide) of a chunk with >= kCombWideG groups,
 // whose group sums are split over kCombLanes lanes per row (Lasso K^T: ~150).
@@ -56,7 +64,8 @@ struct TCItem {
 constexpr int kCombLanes = 8;
 constexpr int kCombRowsWide = 256 / kCombLanes;
 constexpr int kCombWideG = 16;
-constexpr int kCombRowsNarrow = 4 * 256;   // rows of an item of a chunk with <= 2 groups
+constexpr int kCombRowsNarrow = 4 * 256;   // rows of an item of a chunk with <= kCombNarrowG groups
+constexpr int kCombNarrowG = 4;
 struct TWork {
   int32_t chunk, group, s0, s1;   // segments [s0, s1): direct ones run first, staged via batches
   int32_t b0, b1;                 // TMA batches [b0, b1) of the staged segments
@@ -649,6 +658,152 @@ __global__ void __launch_bounds__(kTThreads, ELEM == 1 ? PDCS_TS_MINB1 : PDCS_TP
   cp_async_wait_all();
 }
 
+// ---- Deferred build on the device -------------------------
+// The host builds the segments' unbalanced row-major quads; these two kernels
+// do what balance_banks and slice_segments (pdcs.cu) do on the host, one
+// thread per warp block, with the same arithmetic and tie-breaks, so the final
+// layout is bit-identical (tests/test_tiled_layout.py, device check).
+//
+// Bank balancing of one warp block (balance_banks): at every time step each
+// lane reads one quad, and position k of those quads is one warp-wide
+// ld.shared served in 32/G phases of G lanes; per phase, lanes with the fewest
+// choices go first and take the free bank group with the most entries left.
+// pcol / pperm: the pre layout (read); bcol / bperm: bucket scratch at the same
+// offsets; ncol / nperm: the balanced quads at the same offsets (written).
+__global__ void k_tile_balance(const TDefer* __restrict__ dseg, const int2* __restrict__ dblk, int64_t nblk, int elem,
+                               const int32_t* __restrict__ rowptr, const uint16_t* __restrict__ pcol,
+                               const int32_t* __restrict__ pperm, uint16_t* __restrict__ bcol,
+                               int32_t* __restrict__ bperm, uint16_t* __restrict__ ncol, int32_t* __restrict__ nperm) {
+  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= nblk) return;
+  const int2 db = dblk[it];
+  const TDefer S = dseg[db.x];
+  const int V = S.V, G = elem == 2 ? 8 : 16, rpw = 32 / V;
+  const int32_t* rp = rowptr + S.rp;
+  const int32_t i0 = db.y * rpw;
+  const int R = min(rpw, S.nr - i0);
+  const uint16_t* cols = pcol + S.src;
+  const int32_t* perm = pperm + S.src;
+  const int64_t bbase = S.src + 4 * (int64_t)rp[i0];    // this block's region (bucket scratch)
+  int32_t bstart[32 * 16 + 1];
+  int32_t bleft[32 * 16];
+  int32_t left[32], slots[32];
+  uint32_t mask[32];
+  int rem[16];
+  for (int z = 0; z <= R * G; ++z) bstart[z] = 0;
+  for (int g = 0; g < 16; ++g) rem[g] = 0;
+  int32_t tmax = 0;
+  for (int a = 0; a < R; ++a) {
+    const int32_t q0 = rp[i0 + a], q1 = rp[i0 + a + 1];
+    tmax = max(tmax, (q1 - q0 + V - 1) / V);
+    slots[a] = 4 * (q1 - q0);
+    left[a] = 0;
+    mask[a] = 0;
+    for (int64_t e = 4 * (int64_t)q0; e < 4 * (int64_t)q1; ++e)
+      if (perm[e] >= 0) {
+        const int g = cols[e] % G;
+        ++bstart[a * G + g + 1];
+        mask[a] |= 1u << g;
+        ++rem[g];
+        ++left[a];
+      }
+  }
+  for (int z = 1; z <= R * G; ++z) bstart[z] += bstart[z - 1];
+  for (int z = 0; z < R * G; ++z) bleft[z] = bstart[z];
+  for (int a = 0; a < R; ++a)
+    for (int64_t e = 4 * (int64_t)rp[i0 + a]; e < 4 * (int64_t)rp[i0 + a + 1]; ++e)
+      if (perm[e] >= 0) {
+        const int32_t z = bleft[a * G + cols[e] % G]++;
+        bcol[bbase + z] = cols[e];
+        bperm[bbase + z] = perm[e];
+      }
+  int unit_a[16];
+  int64_t unit_slot[16];
+  for (int32_t t = 0; t < tmax; ++t)
+    for (int k = 0; k < 4; ++k)
+      for (int ph = 0; ph < 32 / G; ++ph) {
+        int nu = 0;
+        for (int lane = ph * G; lane < ph * G + G; ++lane) {
+          const int a = lane / V, l = lane % V;
+          if (a >= R) continue;
+          const int32_t q = l + t * V;
+          if (q >= rp[i0 + a + 1] - rp[i0 + a]) continue;
+          unit_a[nu] = a;
+          unit_slot[nu] = 4 * (int64_t)(rp[i0 + a] + q) + k;
+          ++nu;
+        }
+        if (nu > 1) {                                     // fewest choices first (counting sort)
+          int pc[16], cnt[18], sa[16];
+          int64_t ss[16];
+          for (int z = 0; z < 18; ++z) cnt[z] = 0;
+          for (int x = 0; x < nu; ++x) { pc[x] = __popc(mask[unit_a[x]]); ++cnt[pc[x] + 1]; }
+          for (int z = 1; z < 18; ++z) cnt[z] += cnt[z - 1];
+          for (int x = 0; x < nu; ++x) { const int z = cnt[pc[x]]++; sa[z] = unit_a[x]; ss[z] = unit_slot[x]; }
+          for (int x = 0; x < nu; ++x) { unit_a[x] = sa[x]; unit_slot[x] = ss[x]; }
+        }
+        uint32_t used = 0;
+        int any_col = -1;
+        for (int x = 0; x < nu; ++x) {
+          const int a = unit_a[x];
+          const int64_t slot = unit_slot[x];
+          const uint32_t avail = mask[a] & ~used;
+          int g = -1;
+          if (avail || (left[a] > 0 && slots[a] == left[a])) {
+            uint32_t from = avail ? avail : mask[a];
+            for (; from; from &= from - 1) {
+              const int h = __ffs(from) - 1;
+              if (g < 0 || rem[h] > rem[g]) g = h;
+            }
+          }
+          if (g >= 0) {
+            const int bi = a * G + g;
+            const int32_t z = --bleft[bi];
+            ncol[S.src + slot] = bcol[bbase + z];
+            nperm[S.src + slot] = bperm[bbase + z];
+            if (bleft[bi] == bstart[bi]) mask[a] &= ~(1u << g);
+            --rem[g];
+            --left[a];
+            used |= 1u << g;
+            if (any_col < 0) any_col = ncol[S.src + slot];
+          } else {                                        // pad: re-read an address
+            ncol[S.src + slot] = (uint16_t)(any_col >= 0 ? any_col : 0);
+            nperm[S.src + slot] = -1;
+            if (any_col < 0) any_col = 0;
+          }
+          --slots[a];
+        }
+      }
+}
+
+// Sliced re-layout of one warp block (slice_segments / quad_slot): quad j of
+// block row a goes to blkb[block] + a V + j % V + 32 (j / V).
+__global__ void k_tile_slice(const TDefer* __restrict__ dseg, const int2* __restrict__ dblk, int64_t nblk,
+                             const int32_t* __restrict__ rowptr, const int32_t* __restrict__ blkb,
+                             const uint16_t* __restrict__ ncol, const int32_t* __restrict__ nperm,
+                             uint16_t* __restrict__ col_s, int32_t* __restrict__ perm_s) {
+  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= nblk) return;
+  const int2 db = dblk[it];
+  const TDefer S = dseg[db.x];
+  const int V = S.V, rpw = 32 / V;
+  const int32_t* rp = rowptr + S.rp;
+  const int32_t i0 = db.y * rpw;
+  const int R = min(rpw, S.nr - i0);
+  const int64_t base = blkb[S.bb + db.y];
+  for (int a = 0; a < R; ++a) {
+    const int32_t pos = i0 + a, nq = rp[pos + 1] - rp[pos];
+    for (int32_t j = 0; j < nq; ++j) {
+      const int64_t to = S.dst + 4 * (base + a * V + j % V + 32 * (int64_t)(j / V));
+      const int64_t from = S.src + 4 * ((int64_t)rp[pos] + j);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        col_s[to + k] = ncol[from + k];
+        perm_s[to + k] = nperm[from + k];
+      }
+    }
+  }
+}
+
 // Sum the partials of every row (fixed order) and run the fused epilogue.
 // Items of chunks with few groups: one thread per row, the groups summed in
 // order with loads batched 8 deep.  Items of chunks with many groups (the long
@@ -668,24 +823,30 @@ __global__ void __launch_bounds__(kThreads) k_tiled_combine(TiledMat M, const do
     const TCItem I = M.citem[it];
     const TChunk C = M.chunk[I.chunk];
     const double* src = scratch + C.scratch;
-    if (C.ngroups <= 2) {
-      // the common case (most chunks hold one or two work items): the item is
+    if (C.ngroups <= kCombNarrowG) {
+      // the common case (chunks of a few work items): the item is
       // kCombRowsNarrow rows, kCombRowsNarrow / blockDim per thread, every
       // partial load of the thread issued before the first epilogue
       constexpr int RPT = kCombRowsNarrow / kThreads;
-      double s1[RPT], s2[RPT];
+      double u1[RPT][kCombNarrowG], u2[RPT][kCombNarrowG];
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         const int r = I.r0 + threadIdx.x + k * kThreads;
+#pragma unroll
+        for (int g = 0; g < kCombNarrowG; ++g) {
+          const bool ok = r < C.nrows && g < C.ngroups;
+          u1[k][g] = ok ? src[((int64_t)g * C.nrows + r) * ELEM] : 0.0;
+          u2[k][g] = ok && ELEM == 2 ? src[((int64_t)g * C.nrows + r) * ELEM + 1] : 0.0;
+        }
+      }
+      double s1[RPT], s2[RPT];
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
         s1[k] = 0.0;
         s2[k] = 0.0;
-        if (r < C.nrows) {
-          s1[k] = src[(int64_t)r * ELEM];
-          if (ELEM == 2) s2[k] = src[(int64_t)r * ELEM + 1];
-          if (C.ngroups == 2) {
-            s1[k] += src[((int64_t)C.nrows + r) * ELEM];
-            if (ELEM == 2) s2[k] += src[((int64_t)C.nrows + r) * ELEM + 1];
-          }
+#pragma unroll
+        for (int g = 0; g < kCombNarrowG; ++g) {       // groups added in order (zeros past the end)
+          if (g < C.ngroups) { s1[k] += u1[k][g]; s2[k] += u2[k][g]; }
         }
       }
 #pragma unroll

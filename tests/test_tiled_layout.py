@@ -117,3 +117,27 @@ def test_parts_mode_build_matches_concatenated(monkeypatch):
             assert b["staged"] == ref["staged"] and b["build_ms"] >= b["ranges_ms"] >= 0.0
     with pytest.raises(ValueError):
         _lib.pdcs_tiled_build_host(K.indptr.astype(np.int64), K.indices.astype(np.int32), K.shape[0], 0, 2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kb,elem,which", [("1", 2, "K"), ("2", 1, "KT"), ("32", 2, "K"), ("32", 1, "KT"),
+                                           ("4", 2, "rand"), ("4", 1, "rand")])
+def test_device_balanced_build_is_bit_identical(monkeypatch, kb, elem, which):
+    """The solver's deferred build (host structure; shared-memory bank balancing
+    and the sliced re-layout on the device, tiled.cuh k_tile_balance /
+    k_tile_slice) gives the all-host build's layout entry for entry: column
+    ids, value permutation, row pointers, block bases, segment descriptors
+    (pdcs_tiled_device_check), with 1 and 5 host build threads."""
+    monkeypatch.setenv("PDCS_TILE_KB", kb)
+    if which == "rand":
+        A = _random_csr(np.random.default_rng(4), 3000, 9000, (1, 300))
+        nvec = 9000
+    else:
+        K, KT = _csr(gen_lasso(3000, 300, 0.2, seed=6))
+        A = K if which == "K" else KT
+        nvec = A.shape[1]
+    for threads in ("1", "5"):
+        monkeypatch.setenv("PDCS_BUILD_THREADS", threads)
+        r = _lib.pdcs_tiled_device_check(A.indptr.astype(np.int64), A.indices.astype(np.int32), A.shape[0],
+                                         nvec, elem)
+        assert r["mismatches"] == 0 and r["entries"] > 0, r

@@ -1871,6 +1871,19 @@ const char* pdcs_last_error(const pdcs_ctx* ctx) {
 
 }  // extern "C"
 
+// PDCS_SETUP_TRACE=1: wall ms of the setup phases on stderr (diagnostics).
+struct SetupTrace {
+  bool on = std::getenv("PDCS_SETUP_TRACE") && std::atoi(std::getenv("PDCS_SETUP_TRACE"));
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, cudaStream_t st = nullptr, bool sync = true) {
+    if (!on) return;
+    if (sync) cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pdcs setup] %-28s %9.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 // pdcs_create / pdcs_create_loopback: the communicator is NCCL (nccl_unique_id),
 // an in-process loopback group (loop), or none.
 static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int64_t n1, int64_t row_begin,
@@ -1947,7 +1960,9 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     } else if (nnz && (!col_idx || !vals)) {
       fail(PDCS_ERR_ARG, "null input pointer");
     }
+    SetupTrace tr;
     validate_csr(ctx->hptr.data(), hcolp, hvalp, m, n);
+    tr.mark("validate", nullptr, false);
     // box-column order for gather locality (single context only: every rank of a
     // sharded run must store x identically, and the order depends on all rows)
     std::vector<int32_t> pcol;
@@ -1997,6 +2012,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     ctx->hnorm = hn;
     ctx->cnorm = cn;
     cudaStream_t st = ctx->st;
+    tr.mark("colperm + host data", nullptr, false);
     // ---- device CSR(K)
     std::vector<int32_t> p32(m + 1);
     for (int64_t i = 0; i <= m; ++i) p32[i] = (int32_t)ctx->hptr[i];
@@ -2019,6 +2035,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     upload(ctx->u0, ctx->hu, st);
     ctx->K.m = m; ctx->K.n = n; ctx->K.nnz = nnz;
     ctx->K.ptr = ctx->Kptr.p; ctx->K.col = ctx->Kcol.p; ctx->K.val = ctx->Kval.p;
+    tr.mark("upload K", st);
     // ---- device CSR(K^T) by a stable radix sort of the entries on column id
     ctx->KTptr.alloc(n + 1);
     ctx->KTcol.alloc(nnz);
@@ -2055,6 +2072,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     }
     ctx->KT.m = n; ctx->KT.n = m; ctx->KT.nnz = nnz;
     ctx->KT.ptr = ctx->KTptr.p; ctx->KT.col = ctx->KTcol.p; ctx->KT.val = ctx->KTval.p;
+    tr.mark("transpose", st);
     // ---- SpMV plans (row-length binning)
     std::vector<int32_t> tptr32(n + 1);
     CK(cudaMemcpy(tptr32.data(), ctx->KTptr.p, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
@@ -2109,7 +2127,9 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     CK(cudaMallocHost(&ctx->hctl, sizeof(Ctl)));
     std::memset(ctx->hctl, 0, sizeof(Ctl));
     CK(cudaStreamSynchronize(st));
+    tr.mark("plans + K^T to host", st);
     ctx->thK.join();
+    tr.mark("join tiled K build", nullptr, false);
     ctx->tK.build_ms = ctx->hK.build_ms;
     ctx->t_create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   });
@@ -2316,6 +2336,8 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
                     &ctx->ktya, &ctx->bx, &ctx->candx, &ctx->lam0, &ctx->lam1})
       CK(cudaMemsetAsync(b->p, 0, b->n * sizeof(double), st));
     const bool van = ctx->prm.vanilla_pdhg != 0;
+    SetupTrace tr;
+    tr.mark("set_cones: cones + slots", st);
     // ---- Ruiz + Pock-Chambolle (readings A2, A3, A21)
     const int Grm = grid_for(m * 32, ctx->sms, 16), Grn = grid_for(n * 32, ctx->sms, 16);
     if (!van) {
@@ -2337,16 +2359,21 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     CK(cudaGetLastError());
     // column-tiled copies of K~ and K~^T for the hot SpMVs (tiled.cuh)
     {
+      tr.mark("ruiz", st);
       ctx->make_tiled(ctx->tK, ctx->hK, m, n, 2, ctx->K.val);
+      tr.mark("tiled K (device part)", st);
       if (ctx->thKT.joinable()) ctx->thKT.join();
+      tr.mark("join tiled K^T build", nullptr, false);
       ctx->tKT.build_ms = ctx->hKT.build_ms;
       ctx->make_tiled(ctx->tKT, ctx->hKT, n, m, 1, ctx->KT.val);
       ctx->hKTptr = std::vector<int64_t>();
       ctx->hKTcol = std::vector<int32_t>();
     }
     // L2 column panels where the gathered vector exceeds L2 (panels.cuh)
+    tr.mark("tiled K^T (device part)", st);
     ctx->build_panels(ctx->pK, ctx->K, ctx->tK.on, 2);
     ctx->build_panels(ctx->pKT, ctx->KT, ctx->tKT.on, 1);
+    tr.mark("panels", st);
     // scaled data (reading A2): c~ = c/q, h~ = h/r, l~ = q l, u~ = q u
     k_ewise<<<Gn, kThreads, 0, st>>>(n, ctx->c0.p, ctx->q.p, 0, ctx->ct.p);
     k_ewise<<<Gm, kThreads, 0, st>>>(m, ctx->h0.p, ctx->r.p, 0, ctx->ht.p);
@@ -2425,6 +2452,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     // anchor / products / e_anchor
     reset_from_current(ctx);
     CK(cudaStreamSynchronize(st));
+    tr.mark("eta0/omega0 + anchor KKT", st);
     ctx->t_cones_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   });
 }

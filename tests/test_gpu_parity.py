@@ -473,3 +473,26 @@ def test_set_iterate_mid_run_starts_new_epoch(P):
     g.iterate(40)
     o.iterate(40)
     assert parity(*g.get_iterate(P.CURRENT), *o.get_iterate(0)) <= TOL
+
+
+@pytest.mark.parametrize("make", [lambda: gen_lasso(100, 50, 1.0, seed=0, dense=True),
+                                  lambda: gen_mixed(200, 30, 80, seed=4, soc_dims=(3, 20))])
+def test_set_tolerance_continuation_against_oracle(P, make):
+    """pdcs_set_tolerance on the GPU against the oracle (not only GPU against GPU):
+    solve to 1e-3, continue to 1e-6.  At each stage the returned point is
+    certified by the ORACLE's Eq. 9 at that point (<= the stage's tolerance), and
+    its objective agrees with the oracle's own solve to the same tolerance."""
+    prog = make()
+    g = P.PdcsSolver(prog, tol=1e-3, max_iters=400000)
+    o_check = O.OracleSolver(prog)
+    for tol, otol in ((1e-3, 5e-3), (1e-6, 1e-5)):
+        if tol < 1e-3:
+            g.set_tolerance(tol)
+        r = g.solve()
+        assert r["status"] == "OPTIMAL", r
+        xb, yb = g.get_iterate(P.BEST, P.ORIGINAL)
+        k = o_check.kkt_point(xb, yb)
+        assert max(k["err_p"], k["err_d"], k["err_gap"]) <= tol * (1 + 1e-9), (tol, k)
+        ro = O.OracleSolver(prog, tol=tol, max_iters=400000).solve()
+        assert ro.status == 0
+        assert abs(r["pobj"] - ro.kkt.pobj) <= otol * (1 + abs(ro.kkt.pobj)), (tol, r["pobj"], ro.kkt.pobj)

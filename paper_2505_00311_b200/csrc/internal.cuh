@@ -49,12 +49,6 @@ struct SpmvClass {
   int64_t nrows;
   int64_t range_begin;
   const int32_t* rows;
-  // V == 0 only: each row cut into `split` entry ranges (one CTA each); the
-  // last CTA of a row (scnt) adds the ranges' sums from spart in order and
-  // runs the epilogue.  split <= 1 or spart == nullptr: one CTA per row.
-  int32_t split;
-  double* spart;
-  int32_t* scnt;
 };
 constexpr int kMaxClasses = 6;
 struct SpmvPlan {

@@ -1757,40 +1757,12 @@ struct pdcs_ctx {
       }
       int64_t rows_per_cta = K_.V == 0 ? 1 : K_.V == 1 ? kThreads : kThreads / K_.V;
       int64_t g = (K_.nrows + rows_per_cta - 1) / rows_per_cta;
-      K_.split = 1;
-      K_.spart = nullptr;
-      K_.scnt = nullptr;
-      if (K_.V == 0) {
-        // split the long rows so that the class fills >= 4 waves of the ~4
-        // resident CTAs per SM, each range >= 1024 entries (scratch: alloc_split)
-        int64_t tot = 0;
-        for (int64_t r_ : lists[c]) tot += ptr[r_ + 1] - ptr[r_];
-        const int64_t avg = tot / K_.nrows;
-        const int64_t want = (16 * (int64_t)sms + K_.nrows - 1) / K_.nrows;
-        K_.split = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, avg / 1024));
-        g *= K_.split;
-      }
       const int64_t cap = K_.V == 0 ? (int64_t)sms * 4 : (int64_t)sms * 8;
       K_.ncta = (int32_t)std::max<int64_t>(1, std::min(g, cap));
       total += K_.ncta;
     }
     P.total_cta = total;
     A.plan = P;
-  }
-  // scratch of the split long rows (V == 0 classes, SpmvClass::split)
-  struct SplitBuf { DBuf<double> part; DBuf<int32_t> cnt; };
-  SplitBuf splitK, splitKT;
-  void alloc_split(DevCsr& A, SplitBuf& B) {
-    for (int c = 0; c < A.plan.ncls; ++c) {
-      SpmvClass& K_ = A.plan.cls[c];
-      if (K_.V != 0 || K_.split <= 1) continue;
-      B.part.alloc(K_.nrows * K_.split * 2);
-      B.cnt.alloc(K_.nrows);
-      CK(cudaMemsetAsync(B.cnt.p, 0, K_.nrows * sizeof(int32_t), st));
-      K_.spart = B.part.p;
-      K_.scnt = B.cnt.p;
-      return;                                   // one V == 0 class per plan
-    }
   }
   void patch_plan(DevCsr& A) {
     for (int c = 0; c < A.plan.ncls; ++c)
@@ -2137,8 +2109,6 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     upload(ctx->planrows, rowstore, st);
     ctx->patch_plan(ctx->K);
     ctx->patch_plan(ctx->KT);
-    ctx->alloc_split(ctx->K, ctx->splitK);
-    ctx->alloc_split(ctx->KT, ctx->splitKT);
     for (SpmvPlan& pl : ctx->ktc_plan) {
       DevCsr tmpA;
       tmpA.plan = pl;

@@ -70,29 +70,15 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
 #define PDCS_CSR_U 8                  // entries in flight per lane, V >= 8 (B200: 4 -> 8 with the 64-register cap, MPO +13%, mixed +7%)
 #endif
 template <int V, int NX>
-__device__ __forceinline__ void row_dot_range(const int32_t* __restrict__ col, const double* __restrict__ val,
-                                              const double* __restrict__ x1, const double* __restrict__ x2,
-                                              int32_t b, int32_t e, bool valid, int lane, double& s1, double& s2);
-
-template <int V, int NX>
 __device__ __forceinline__ void row_dot(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                                         const double* __restrict__ val, const double* __restrict__ x1,
                                         const double* __restrict__ x2, int64_t row, int lane, double& s1,
                                         double& s2) {
-  const int32_t b = row >= 0 ? __ldg(ptr + row) : 0, e = row >= 0 ? __ldg(ptr + row + 1) : 0;
-  row_dot_range<V, NX>(col, val, x1, x2, b, e, row >= 0, lane, s1, s2);
-}
-
-// The dot products over the entries [b, e) of a row (the whole row, or one
-// range of a split long row).
-template <int V, int NX>
-__device__ __forceinline__ void row_dot_range(const int32_t* __restrict__ col, const double* __restrict__ val,
-                                              const double* __restrict__ x1, const double* __restrict__ x2,
-                                              int32_t b, int32_t e, bool valid, int lane, double& s1, double& s2) {
   constexpr int U = (V >= 8 && V <= 32) ? PDCS_CSR_U : 4;   // entries in flight per lane
   s1 = 0.0;
   s2 = 0.0;
-  if (valid) {
+  if (row >= 0) {
+    const int32_t b = __ldg(ptr + row), e = __ldg(ptr + row + 1);
     int32_t p = b + lane;
     int32_t c[U];
     double a[U];
@@ -168,20 +154,12 @@ __global__ void __launch_bounds__(kThreads, PDCS_CSR_MINB) spmv_kernel(const int
   const int lcta = blockIdx.x - base;
   auto rowid = [&](int64_t idx) -> int64_t { return K.rows ? (int64_t)K.rows[idx] : K.range_begin + idx; };
   if (K.V == 0) {
-    // one CTA per row, or per entry range of a row split `split` ways (few
-    // very long rows: 1000 rows on ~600 resident CTAs left a 1.7-wave tail);
-    // the last CTA to finish a row adds its ranges' sums in range order
+    // one CTA per row
     __shared__ double red[2][kThreads / 32];
-    const int S = K.split > 1 && K.spart ? K.split : 1;
-    for (int64_t u = lcta; u < K.nrows * S; u += K.ncta) {
-      const int64_t idx = u / S;
-      const int sg = (int)(u % S);
+    for (int64_t idx = lcta; idx < K.nrows; idx += K.ncta) {
       const int64_t row = rowid(idx);
-      const int32_t b = __ldg(ptr + row), e = __ldg(ptr + row + 1);
-      const int32_t len = e - b;
       double s1, s2;
-      row_dot_range<kThreads, NX>(col, val, x1, x2, b + (int32_t)((int64_t)len * sg / S),
-                                  b + (int32_t)((int64_t)len * (sg + 1) / S), true, threadIdx.x, s1, s2);
+      row_dot<kThreads, NX>(ptr, col, val, x1, x2, row, threadIdx.x, s1, s2);
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) {
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
@@ -192,24 +170,7 @@ __global__ void __launch_bounds__(kThreads, PDCS_CSR_MINB) spmv_kernel(const int
       if (threadIdx.x == 0) {
         double t1 = 0.0, t2 = 0.0;
         for (int w = 0; w < kThreads / 32; ++w) { t1 += red[0][w]; t2 += red[1][w]; }
-        if (S == 1) {
-          epi.row(row, t1, t2, acc);
-        } else {
-          K.spart[(idx * S + sg) * 2] = t1;
-          K.spart[(idx * S + sg) * 2 + 1] = t2;
-          __threadfence();
-          const int c = atomicAdd(K.scnt + idx, 1);
-          if (c == S - 1) {
-            __threadfence();
-            double a1 = 0.0, a2 = 0.0;
-            for (int k = 0; k < S; ++k) {
-              a1 += __ldcg(K.spart + (idx * S + k) * 2);
-              a2 += __ldcg(K.spart + (idx * S + k) * 2 + 1);
-            }
-            K.scnt[idx] = 0;                 // ready for the next launch
-            epi.row(row, a1, a2, acc);
-          }
-        }
+        epi.row(row, t1, t2, acc);
       }
       __syncthreads();
     }

@@ -631,13 +631,14 @@ __global__ void __launch_bounds__(kTThreads, ELEM == 1 ? PDCS_TS_MINB1 : PDCS_TP
           inflight = next_staged(M, W2.s0, W2.s1);
         }
         if (inflight >= 0) tile_fetch_async<ELEM>(M, x, M.seg[inflight].tile, tiles + buf * TE);
+#define PDCS_SLB sliced_blocks
         switch (S.V) {
-          case 1: sliced_blocks<1, ELEM>(M, S, C.nrows, xs_s, acc); break;
-          case 2: sliced_blocks<2, ELEM>(M, S, C.nrows, xs_s, acc); break;
-          case 4: sliced_blocks<4, ELEM>(M, S, C.nrows, xs_s, acc); break;
-          case 8: sliced_blocks<8, ELEM>(M, S, C.nrows, xs_s, acc); break;
-          case 16: sliced_blocks<16, ELEM>(M, S, C.nrows, xs_s, acc); break;
-          default: sliced_blocks<32, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          case 1: PDCS_SLB<1, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          case 2: PDCS_SLB<2, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          case 4: PDCS_SLB<4, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          case 8: PDCS_SLB<8, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          case 16: PDCS_SLB<16, ELEM>(M, S, C.nrows, xs_s, acc); break;
+          default: PDCS_SLB<32, ELEM>(M, S, C.nrows, xs_s, acc); break;
         }
       } else {
         switch (S.V) {

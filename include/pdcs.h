@@ -31,6 +31,7 @@
 #ifndef PDCS_H_
 #define PDCS_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -323,6 +324,18 @@ void pdcs_proj_destroy(pdcs_proj *plan);
 
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 broadcasts it). */
 pdcs_status pdcs_nccl_unique_id(void *out128);
+
+/* ---- Device memory: a caller allocator for every later
+ * context's device buffers (matrices, tiled formats, vectors, scratch).
+ * alloc(bytes, user) returns device memory on the context's device or NULL
+ * (the call then fails with PDCS_ERR_CUDA); free(ptr, user) releases it.
+ * Process-wide; set it before pdcs_create and keep it until every context
+ * using it is destroyed.  NULL, NULL restores cudaMalloc / cudaFree.
+ * Buffers are allocated at create / set_cones time only, never per iteration.
+ * Errors: ARG (one function NULL, the other not). */
+typedef void *(*pdcs_alloc_fn)(size_t bytes, void *user);
+typedef void (*pdcs_free_fn)(void *ptr, void *user);
+pdcs_status pdcs_set_allocator(pdcs_alloc_fn alloc, pdcs_free_fn free_fn, void *user);
 
 /* ---- In-process loopback ranks (SURVEY §8(e) tests on one GPU).
  * A loopback group stands in for NCCL when `world` row-sharded contexts live

@@ -50,6 +50,10 @@ class pdcs_result_t(C.Structure):
                 ("omega", C.c_double), ("beta", C.c_double), ("solve_seconds", C.c_double)]
 
 
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
 class PdcsError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"{STATUS.get(code, code)}: {msg}")
@@ -78,6 +82,7 @@ def lib():
                                            C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(pdcs_params),
                                            C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        L.pdcs_set_allocator.argtypes = [ALLOC_FN, FREE_FN, C.c_void_p]
         L.pdcs_loopback_create.argtypes = [C.POINTER(C.c_void_p), C.c_int]
         L.pdcs_loopback_destroy.argtypes = [C.c_void_p]
         L.pdcs_set_cones.argtypes = [C.c_void_p, P_I32, P_I64, C.c_int64, P_I32, P_I64, C.c_int64]
@@ -119,7 +124,8 @@ EXPORTED = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterat
             "pdcs_destroy", "pdcs_nccl_unique_id", "pdcs_get_scalars", "pdcs_get_state",
             "pdcs_set_state", "pdcs_tiled_layout_stats", "pdcs_proj_create", "pdcs_proj_run",
             "pdcs_proj_info", "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host",
-            "pdcs_loopback_create", "pdcs_loopback_destroy", "pdcs_create_loopback", "pdcs_tiled_device_check"]
+            "pdcs_loopback_create", "pdcs_loopback_destroy", "pdcs_create_loopback", "pdcs_tiled_device_check",
+            "pdcs_set_allocator"]
 
 STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e_prev", "best_e", "k",
               "total", "trials", "restarts"]
@@ -184,6 +190,23 @@ def pdcs_create_loopback(m_global, n, n1, row_begin, row_end, row_ptr, col_idx, 
     del keep
     _check(code)
     return ctx
+
+
+_allocator_refs = None
+
+
+def pdcs_set_allocator(alloc=None, free=None):
+    """alloc(nbytes) -> int device pointer, free(ptr) -> None (Python callables,
+    e.g. torch's caching allocator); None, None restores cudaMalloc."""
+    global _allocator_refs
+    if alloc is None and free is None:
+        _check(lib().pdcs_set_allocator(ALLOC_FN(), FREE_FN(), None))
+        _allocator_refs = None
+        return
+    fa = ALLOC_FN(lambda nbytes, user: alloc(int(nbytes)) or None)
+    ff = FREE_FN(lambda ptr, user: free(int(ptr)))
+    _check(lib().pdcs_set_allocator(fa, ff, None))
+    _allocator_refs = (fa, ff)          # keep the trampolines alive
 
 
 def pdcs_loopback_create(world: int):

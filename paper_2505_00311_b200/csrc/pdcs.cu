@@ -8,6 +8,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -50,6 +51,26 @@ struct StatusErr {
 };
 [[noreturn]] void fail(pdcs_status st, const std::string& msg) { throw StatusErr{st, msg}; }
 
+// Device memory of every context (include/pdcs.h, pdcs_set_allocator): the
+// caller's allocator when one is set, else cudaMalloc / cudaFree.
+std::atomic<pdcs_alloc_fn> g_alloc{nullptr};
+std::atomic<pdcs_free_fn> g_free{nullptr};
+std::atomic<void*> g_alloc_user{nullptr};
+void* dev_alloc(size_t bytes) {
+  if (pdcs_alloc_fn f = g_alloc.load()) {
+    void* p = f(bytes, g_alloc_user.load());
+    if (!p) fail(PDCS_ERR_CUDA, "caller allocator returned NULL for " + std::to_string(bytes) + " bytes");
+    return p;
+  }
+  void* p = nullptr;
+  CK(cudaMalloc(&p, bytes));
+  return p;
+}
+void dev_free(void* p) {
+  if (pdcs_free_fn f = g_free.load()) f(p, g_alloc_user.load());
+  else cudaFree(p);
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -57,10 +78,10 @@ struct DBuf {
   void alloc(size_t count) {
     free_();
     n = count;
-    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
   }
   void free_() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p);
     p = nullptr;
     n = 0;
   }
@@ -2161,6 +2182,17 @@ pdcs_status pdcs_create_loopback(pdcs_ctx** out, int64_t m_global, int64_t n, in
   LoopbackGroup* g = reinterpret_cast<LoopbackGroup*>(group);
   return create_impl(out, m_global, n, n1, row_begin, row_end, row_ptr, col_idx, vals, c, h, l, u, p, device,
                      cuda_stream, mem_kind, nullptr, g, rank, g->world);
+}
+
+pdcs_status pdcs_set_allocator(pdcs_alloc_fn alloc, pdcs_free_fn free_fn, void* user) {
+  if ((alloc == nullptr) != (free_fn == nullptr)) {
+    g_create_error = "pdcs_set_allocator needs both functions or neither";
+    return PDCS_ERR_ARG;
+  }
+  g_alloc_user.store(user);
+  g_free.store(free_fn);
+  g_alloc.store(alloc);
+  return PDCS_OK;
 }
 
 pdcs_status pdcs_loopback_create(pdcs_loopback** out, int world) {

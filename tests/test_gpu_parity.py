@@ -496,3 +496,40 @@ def test_set_tolerance_continuation_against_oracle(P, make):
         ro = O.OracleSolver(prog, tol=tol, max_iters=400000).solve()
         assert ro.status == 0
         assert abs(r["pobj"] - ro.kkt.pobj) <= otol * (1 + abs(ro.kkt.pobj)), (tol, r["pobj"], ro.kkt.pobj)
+
+
+def test_caller_allocator(P):
+    """pdcs_set_allocator: every device buffer of a context comes from the
+    caller's allocator (here torch's caching allocator through ctypes
+    callbacks), all of it is returned at destroy, and the iterates are the
+    default allocator's bits."""
+    import torch
+    live = {}
+    stats = {"alloc": 0, "free": 0}
+
+    def alloc(nbytes):
+        p = torch.cuda.caching_allocator_alloc(nbytes)
+        live[p] = nbytes
+        stats["alloc"] += 1
+        return p
+
+    def free(ptr):
+        live.pop(ptr)
+        torch.cuda.caching_allocator_delete(ptr)
+        stats["free"] += 1
+
+    prog = mixed(6)
+    P.pdcs_set_allocator(alloc, free)
+    try:
+        g = P.PdcsSolver(prog)
+        g.iterate(100)
+        xa, ya = g.get_iterate(P.CURRENT)
+        assert stats["alloc"] > 20 and live
+        g.close()
+        assert not live and stats["free"] == stats["alloc"]
+    finally:
+        P.pdcs_set_allocator(None, None)
+    g = P.PdcsSolver(prog)
+    g.iterate(100)
+    xb, yb = g.get_iterate(P.CURRENT)
+    assert np.array_equal(xa, xb) and np.array_equal(ya, yb)

@@ -28,4 +28,21 @@ for name, env, make in runs:
     r = g.iterate(int(os.environ.get("SAN_ITERS", "45")))
     print(name, "iters", r["iters"], "restarts", r["restarts"], flush=True)
     g.close()
+# the standalone projection with every team forced (cluster and grid included)
+import numpy as np
+import torch
+from instances import SOC, RSOC, EXP
+kinds = np.array([SOC, RSOC, EXP, SOC], np.int32)
+dims = np.array([5000, 700, 3, 40], np.int64)
+rng = np.random.default_rng(0)
+v = torch.from_numpy(rng.standard_normal(int(dims.sum()))).cuda()
+D = torch.from_numpy(rng.uniform(0.5, 2.0, int(dims.sum()))).cuda()
+D[5001] = D[5000]
+for team in ("auto", "thread", "warp", "cta", "cluster", "grid"):
+    plan = P.pdcs_proj_create(kinds, dims, team=team)
+    out = torch.empty_like(v)
+    P.pdcs_proj_run(plan, D, v, out)
+    torch.cuda.synchronize()
+    P.pdcs_proj_destroy(plan)
+    print("proj", team, flush=True)
 print("done")

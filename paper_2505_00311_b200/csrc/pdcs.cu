@@ -726,9 +726,15 @@ int64_t long_row_sectors(const int64_t* ptr, const int32_t* col, int64_t m, cons
   return total;
 }
 
-bool plan_colperm(const int64_t* ptr, const int32_t* col, int64_t m, int64_t n, int64_t n1,
+bool plan_colperm(const int64_t* ptr, const int32_t* col, int64_t m, int64_t n, int64_t n1, int sms,
                   std::vector<int32_t>& u2i, std::vector<int32_t>& i2u) {
   if (n1 < 2) return false;
+  // only the few-long-rows case (the CSR plan's one-CTA-per-row class, < 16
+  // per SM): many long rows run side by side and share sectors anyway, and
+  // checking them would cost O(nnz log) host time (Lasso 4e5 x 7e6: 1400 per row)
+  int64_t nlong = 0;
+  for (int64_t i = 0; i < m; ++i) nlong += ptr[i + 1] - ptr[i] >= kPermLongRow;
+  if (nlong == 0 || nlong >= 16 * (int64_t)sms) return false;
   const int64_t before = long_row_sectors(ptr, col, m, nullptr);
   if (before == 0) return false;
   std::vector<int64_t> best(n1, -1), blen(n1, -1);
@@ -1991,7 +1997,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     {
       const char* e = std::getenv("PDCS_COLPERM");
       const bool allow = (e ? std::atoi(e) != 0 : true) && !ctx->dist;
-      if (allow && plan_colperm(ctx->hptr.data(), hcolp, m, n, n1, ctx->u2i, ctx->i2u)) {
+      if (allow && plan_colperm(ctx->hptr.data(), hcolp, m, n, n1, ctx->sms, ctx->u2i, ctx->i2u)) {
         permute_csr(ctx->hptr.data(), hcolp, hvalp, m, ctx->u2i, pcol, pval);
         hcolp = pcol.data();
         hvalp = pval.data();

@@ -1000,10 +1000,11 @@ struct pdcs_ctx {
   void psweep(const char* name, Panels& PA, const double* x1, const double* x2, Epi epi, double* part,
               int64_t slot0) {
     const char* pname = &PA == &pK ? "panel_K_partial" : "panel_KT_partial";
+    int passes = 0;
     for (int p = 0; p < PA.P; ++p) {
       const DevCsr& A = PA.part[p];
       if (A.plan.total_cta == 0) continue;
-      EpiPanelAcc<Epi> ea{epi, PA.acc.p, p == 0 ? 1 : 0};
+      EpiPanelAcc<Epi> ea{epi, PA.acc.p, passes++ == 0 ? 1 : 0};
       launch(pname, [&] {
         spmv_kernel<EpiPanelAcc<Epi>><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, x1, x2, A.plan, ea,
                                                                              ctl, nullptr, 0);

@@ -233,3 +233,34 @@ def test_chunked_overlapped_allreduce_is_bit_identical(P, world, monkeypatch):
     for k in ("x", "x0", "xsum"):
         assert np.array_equal(sa[k], sb[k]), k
     assert all(np.array_equal(a, b) for a, b in zip(ya, yb))
+
+
+def test_rank_local_configs4_shards_through_libpdcs(P, monkeypatch):
+    """configs[4]'s recipe generated rank-locally (instances.gen_mixed_shard: each
+    rank draws only its rows, c from summed partials) and solved as 3 loopback
+    ranks: the same iterates as the one-process instance on one context (first
+    120 iterations, 1e-9), identical decisions on every rank."""
+    from instances import ConicProgram, mixed_full_layout, gen_mixed_shard
+    from paper_2505_00311_b200 import dist as D
+    monkeypatch.setenv("PDCS_TILED", "0")
+    L = mixed_full_layout(2e-4, seed=5)
+    world = 3
+    parts = D.partition_rows(L.row_ptr, L.rk, L.rdim, world)
+    partial = [gen_mixed_shard(L, pr) for pr in parts]
+    csum = sum(sh.c - L.lam for sh in partial)            # the all-reduce of the G^T y* partials
+    shards = [gen_mixed_shard(L, pr, allreduce=lambda a: csum.copy()) for pr in parts]
+    group = P.pdcs_loopback_create(world)
+    ranks = on_all([lambda r=r: P.PdcsSolver(shards[r], rank=r, world=world, loopback=group)
+                    for r in range(world)])
+    whole = gen_mixed_shard(L, (0, L.m))
+    one = ConicProgram(m=L.m, n=L.n, n1=L.n1, row_ptr=whole.row_ptr, col_idx=whole.col_idx, vals=whole.vals,
+                       c=shards[0].c, h=whole.h, l=L.l, u=L.u, pk=L.pk, pdim=L.pdim, rk=L.rk, rdim=L.rdim)
+    g0 = P.PdcsSolver(one)
+    for _ in range(3):
+        on_all([lambda g=g: g.iterate(40) for g in ranks])
+        g0.iterate(40)
+        assert_ranks_identical(ranks)
+        x0, y0 = g0.get_iterate(P.CURRENT)
+        its = [g.get_iterate(P.CURRENT) for g in ranks]
+        assert rel(its[0][0], x0) <= TOL and rel(np.concatenate([y for _, y in its]), y0) <= TOL
+    assert ranks[0].scalars()["restarts"] == g0.scalars()["restarts"]

@@ -395,8 +395,9 @@ def main():
     # partial kernel + the combine/epilogue kernel on the tiled path)
     peak, peak_src = load_peaks()
     algb = spmv_alg_bytes(prog)
-    groups = {"spmv_K_dual": ["spmv_K_dual", "tiled_K_partial", "panel_K_partial"],
-              "spmv_KT_halpern": ["spmv_KT_halpern", "tiled_KT_partial", "panel_KT_partial"]}
+    groups = {"spmv_K_dual": ["spmv_K_dual", "tiled_K_partial", "panel_K_partial", "tiled_K_wide_combine"],
+              "spmv_KT_halpern": ["spmv_KT_halpern", "tiled_KT_partial", "panel_KT_partial",
+                                  "tiled_KT_wide_combine"]}
     sweeps = {}
     for name, parts in groups.items():
         if name in ktimes:

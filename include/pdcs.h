@@ -247,8 +247,9 @@ void pdcs_enable_timing(pdcs_ctx *ctx, int on);
  * (every x-side array crossing this ABI stays in the
  * caller's order), then the L2 column panels of K~ and K~^T (DESIGN.md
  * §7.7): number of panels kept (0 = CSR / tiled sweep) and the autotune ms of
- * the CSR and the panelled sweep, for K~ then K~^T.  Returns the number of
- * values written (<= 43). */
+ * the CSR and the panelled sweep, for K~ then K~^T, then the fused combine
+ * of the tiled sweeps: kept (0/1) and its autotune ms, for
+ * K~ then K~^T.  Returns the number of values written (<= 47). */
 int pdcs_get_scalars(pdcs_ctx *ctx, double *out, int cap);
 
 /* Number of kernel launches issued by the last pdcs_iterate call. */
@@ -276,6 +277,18 @@ int pdcs_tiled_build_host(const int64_t *row_ptr, const int32_t *col, int64_t ro
  * arguments (or when the deferred build does not apply), -1 on a CUDA error. */
 int pdcs_tiled_device_check(const int64_t *row_ptr, const int32_t *col, int64_t rows, int64_t nvec, int elem,
                             double *out);
+
+/* Diagnostic: the device structure build of the column-tiled layout (the
+ * solver's default: the entries of the CSR never pass through
+ * the host) against the all-host build, entry by entry: column ids and value
+ * permutation of staged and direct entries, row pointers, row order, block
+ * bases, segment descriptors, work items, batches, chunks.  row_ptr[rows+1],
+ * col[nnz] are HOST arrays (copied to the device here).  out[0] = mismatches;
+ * out[1] = all-host ms; out[2] = device-build ms; out[3] = staged entries;
+ * out[4] = layout entries.  Returns 5, 0 on bad arguments (or when the
+ * sliced, balanced layout is switched off), -1 on a CUDA error. */
+int pdcs_tiled_devbuild_check(const int64_t *row_ptr, const int32_t *col, int64_t rows, int64_t nvec, int elem,
+                              double *out);
 
 /* Host-only diagnostic, no GPU needed: build the column-tiled layout
  * of a CSR structure (row_ptr[rows+1], col[nnz], valid and

@@ -109,6 +109,8 @@ def lib():
         L.pdcs_tiled_build_host.restype = C.c_int
         L.pdcs_tiled_device_check.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
         L.pdcs_tiled_device_check.restype = C.c_int
+        L.pdcs_tiled_devbuild_check.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+        L.pdcs_tiled_devbuild_check.restype = C.c_int
         L.pdcs_proj_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, P_I32, P_I64, C.c_int64, C.c_int]
         L.pdcs_proj_run.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.pdcs_proj_info.argtypes = [C.c_void_p, P_I64, P_I64]
@@ -125,6 +127,7 @@ EXPORTED = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterat
             "pdcs_set_state", "pdcs_tiled_layout_stats", "pdcs_proj_create", "pdcs_proj_run",
             "pdcs_proj_info", "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host",
             "pdcs_loopback_create", "pdcs_loopback_destroy", "pdcs_create_loopback", "pdcs_tiled_device_check",
+            "pdcs_tiled_devbuild_check",
             "pdcs_set_allocator"]
 
 STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e_prev", "best_e", "k",
@@ -137,7 +140,8 @@ SCALAR_KEYS = ["eta", "omega", "beta", "k", "total", "trials", "restarts", "e_an
                "tiled_K", "tune_K_csr_ms", "tune_K_tiled_ms", "tiled_KT", "tune_KT_csr_ms",
                "tune_KT_tiled_ms", "tiled_K_build_ms", "tiled_KT_build_ms", "setup_create_ms",
                "setup_cones_ms", "colperm", "panels_K", "tune_K_csr_ms_p", "tune_K_panel_ms", "panels_KT",
-               "tune_KT_csr_ms_p", "tune_KT_panel_ms"]
+               "tune_KT_csr_ms_p", "tune_KT_panel_ms", "fused_K", "tune_K_fused_ms", "fused_KT",
+               "tune_KT_fused_ms"]
 
 
 def _check(code, ctx=None):
@@ -258,6 +262,16 @@ def pdcs_tiled_device_check(row_ptr, col, rows, nvec, elem) -> dict:
     if k != 5:
         raise PdcsError(7 if k < 0 else 1, "pdcs_tiled_device_check failed" if k < 0 else "not applicable")
     return dict(mismatches=out[0], host_ms=out[1], deferred_host_ms=out[2], device_ms=out[3], entries=out[4])
+
+
+def pdcs_tiled_devbuild_check(row_ptr, col, rows, nvec, elem) -> dict:
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    c = np.ascontiguousarray(col, np.int32)
+    out = np.zeros(5)
+    k = lib().pdcs_tiled_devbuild_check(_ptr(rp), _ptr(c), rows, nvec, elem, out.ctypes.data_as(P_D))
+    if k != 5:
+        raise PdcsError(7 if k < 0 else 1, "pdcs_tiled_devbuild_check failed" if k < 0 else "not applicable")
+    return dict(mismatches=out[0], host_ms=out[1], device_ms=out[2], staged=out[3], entries=out[4])
 
 
 def pdcs_set_tolerance(ctx, tol, time_limit_s=0.0):

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <cstdlib>
 #include <functional>
 #include <map>
@@ -94,11 +95,34 @@ void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
   if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
 }
 
+template <class T>
+void take(DBuf<T>& to, DBuf<T>& from) {
+  to.free_();
+  std::swap(to.p, from.p);
+  std::swap(to.n, from.n);
+}
+
+// staged share of the entries above which the tiled copy is built
+constexpr double kTiledMinFrac = 0.3;
+
 int grid_for(int64_t n, int sms, int per_sm = 8) {
   int64_t g = (n + kThreads - 1) / kThreads;
   g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sms * per_sm));
   return (int)g;
 }
+
+// PDCS_SETUP_TRACE=1: wall ms of the setup phases on stderr (diagnostics).
+struct SetupTrace {
+  bool on = std::getenv("PDCS_SETUP_TRACE") && std::atoi(std::getenv("PDCS_SETUP_TRACE"));
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, cudaStream_t st = nullptr, bool sync = true) {
+    if (!on) return;
+    if (sync) cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pdcs setup] %-28s %9.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // ---------------------------------------------------------------- tiled format builder
 // Host construction of the column-tiled format of tiled.cuh from a CSR
@@ -130,6 +154,7 @@ struct TiledHost {
   // the final sliced layout; dseg the staged segments, dblk their warp blocks
   // (dseg index, block).  Parts mode: o_pre offsets of the pre arrays.
   bool defer = false;
+  bool devbuilt = false;           // built on the device (build_tiled_device)
   int64_t fin_s = 0;
   std::vector<TDefer> dseg;
   std::vector<int2> dblk;
@@ -669,6 +694,359 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
   H.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
 }
 
+// ---------------------------------------------------------------- device structure build
+// The tiled format of a DEVICE CSR (tiled.cuh: k_tile_hist / k_tile_rowcnt /
+// k_tile_fill, then k_tile_balance / k_tile_slice): the entries never pass
+// through the host.  The host sees the (chunk, tile) counts and the per-row
+// segment counts only, and runs build_tiled_range's decisions on them (staged
+// tiles, segment order, rows longest first, lanes per row, quad padding, the
+// sliced plan, work items and batches) in the same order, so the layout is
+// the one build_tiled + the deferred device finish produce
+// (pdcs_tiled_devbuild_check compares them entry by entry).
+struct TiledDevArrays {
+  DBuf<int32_t> rowptr, col_d, blkb, perm_s, perm_d;
+  DBuf<uint16_t> srow, col_s;
+};
+
+template <class F>
+void parallel_chunks(int64_t n, const F& f) {
+  int nth = (int)std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()), 32,
+                                    std::max<int64_t>(1, n / 8)});
+  if (const char* e = std::getenv("PDCS_BUILD_THREADS")) nth = std::max(1, std::atoi(e));
+  if (nth <= 1) { f((int64_t)0, n); return; }
+  // dynamic: chunks differ widely in work (Lasso K^T: 20 of ~1000 hold half the entries)
+  std::atomic<int64_t> next{0};
+  const int64_t grain = std::max<int64_t>(1, n / (nth * 16));
+  std::vector<std::thread> th;
+  for (int w = 0; w < nth; ++w)
+    th.emplace_back([&] {
+      for (int64_t a; (a = next.fetch_add(grain)) < n;) f(a, std::min(n, a + grain));
+    });
+  for (auto& t : th) t.join();
+}
+
+// Whether the solver's builds take this path: the sliced, bank-balanced layout
+// (the default); PDCS_TILE_DEVBUILD=0 keeps the host build.
+bool tiled_devbuild_env() {
+  const bool bal = !std::getenv("PDCS_TILE_BALANCE") || std::atoi(std::getenv("PDCS_TILE_BALANCE"));
+  const bool dev = !(std::getenv("PDCS_TILE_DEVICE") && std::atoi(std::getenv("PDCS_TILE_DEVICE")) == 0);
+  const bool db = !(std::getenv("PDCS_TILE_DEVBUILD") && std::atoi(std::getenv("PDCS_TILE_DEVBUILD")) == 0);
+  return tiled_sliced() && bal && dev && db;
+}
+
+// dptr / dcol: the device CSR (int32 row pointers); hptr: its row pointers on
+// the host.  Fills H's descriptors (seg, work, chunk, batch, scratch, staged,
+// sizes) and the device arrays of A; A.perm_s / perm_d are the CSR positions
+// the values are gathered from.  H.devbuilt stays false (nothing built) when
+// the staged share is below min_frac: the caller keeps the CSR kernel then.
+void build_tiled_device(const int32_t* dptr, const int32_t* dcol, const int64_t* hptr, int64_t rows, int64_t nvec,
+                        int elem, double min_frac, TiledHost& H, TiledDevArrays& A, cudaStream_t st, int sms) {
+  const auto t_start = std::chrono::steady_clock::now();
+  SetupTrace tr;
+  if (const char* e = std::getenv("PDCS_STACK_LIMIT")) CK(cudaDeviceSetLimit(cudaLimitStackSize, (size_t)std::atol(e)));
+  H = TiledHost();
+  H.T = tiled_tile_bytes() / (8 * elem);
+  H.elem = elem;
+  H.tma = false;
+  H.sliced = true;
+  H.defer = true;
+  H.nnz = hptr[rows];
+  const int32_t T = H.T;
+  const int64_t stage_min = (int64_t)T * 8 * elem / 16;
+  const int64_t ntiles = (nvec + T - 1) / T;
+  const int64_t nchunk = (rows + kTRows - 1) / kTRows;
+  const int64_t group_nz = std::getenv("PDCS_TILE_GROUP") ? std::atol(std::getenv("PDCS_TILE_GROUP"))
+                                                          : std::max<int64_t>(32768, H.nnz / 3000);
+  if (H.nnz == 0 || rows == 0) return;
+  // ---- (chunk, tile) counts -> staged tiles per chunk
+  std::vector<std::vector<int32_t>> stiles(nchunk);
+  std::vector<std::vector<int64_t>> scnt(nchunk);
+  std::vector<int64_t> dnz(nchunk, 0);
+  {
+    const int64_t per = std::max<int64_t>(1, std::min<int64_t>(nchunk, ((int64_t)16 << 20) / std::max<int64_t>(ntiles, 1)));
+    DBuf<int32_t> dc;
+    dc.alloc((size_t)per * ntiles);
+    std::vector<int32_t> hc((size_t)per * ntiles);
+    const bool smem = ntiles <= 12288;
+    for (int64_t c0 = 0; c0 < nchunk; c0 += per) {
+      const int64_t nc = std::min(per, nchunk - c0);
+      if (!smem) CK(cudaMemsetAsync(dc.p, 0, (size_t)nc * ntiles * sizeof(int32_t), st));
+      k_tile_hist<<<(unsigned)nc, 256, smem ? ntiles * sizeof(int32_t) : 0, st>>>(dptr, dcol, rows, T, ntiles, c0,
+                                                                                  dc.p, smem ? 1 : 0);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(hc.data(), dc.p, (size_t)nc * ntiles * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      parallel_chunks(nc, [&](int64_t a, int64_t b) {
+        for (int64_t c = a; c < b; ++c) {
+          const int32_t* h = hc.data() + (size_t)c * ntiles;
+          for (int64_t t = 0; t < ntiles; ++t) {
+            if (!h[t]) continue;
+            if (h[t] >= stage_min) { stiles[c0 + c].push_back((int32_t)t); scnt[c0 + c].push_back(h[t]); }
+            else dnz[c0 + c] += h[t];
+          }
+        }
+      });
+    }
+  }
+  tr.mark("    devbuild: tile counts", st);
+  std::vector<TBChunk> cb(nchunk);
+  std::vector<int32_t> stl;
+  int64_t nseg = 0;
+  for (int64_t c = 0; c < nchunk; ++c) {
+    cb[c].sbase = nseg;
+    cb[c].soff = (int32_t)stl.size();
+    cb[c].nst = (int32_t)stiles[c].size();
+    cb[c].direct = dnz[c] ? 1 : 0;
+    cb[c].pad = 0;
+    stl.insert(stl.end(), stiles[c].begin(), stiles[c].end());
+    nseg += cb[c].direct + cb[c].nst;
+    for (int64_t v : scnt[c]) H.staged += v;
+  }
+  const double frac = (double)H.staged / (double)H.nnz;
+  const char* env = std::getenv("PDCS_TILED");
+  if (!(env ? std::atoi(env) != 0 : frac >= min_frac)) return;
+  // ---- per-row segment counts
+  DBuf<TBChunk> dcb;
+  DBuf<int32_t> dstl, drc;
+  upload(dcb, cb, st);
+  dstl.alloc(std::max<size_t>(stl.size(), 1));
+  if (!stl.empty()) CK(cudaMemcpyAsync(dstl.p, stl.data(), stl.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  drc.alloc((size_t)nseg * kTRows);
+  CK(cudaMemsetAsync(drc.p, 0, (size_t)nseg * kTRows * sizeof(int32_t), st));
+  const int gw = (int)std::min<int64_t>((rows + 7) / 8, (int64_t)sms * 16);
+  k_tile_rowcnt<<<gw, 256, 0, st>>>(dptr, dcol, rows, T, dcb.p, dstl.p, drc.p);
+  CK(cudaGetLastError());
+  std::vector<int32_t> rc((size_t)nseg * kTRows);
+  CK(cudaMemcpyAsync(rc.data(), drc.p, rc.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  drc.free_();
+  tr.mark("    devbuild: row counts", st);
+  // ---- per chunk: build_tiled_range's layout decisions on the counts
+  struct CL {
+    std::vector<TSeg> seg;                 // rp relative to the chunk; bb: first block slot (chunk-local)
+    std::vector<int64_t> pre;              // staged: pre offset (chunk-local entries); direct: col_d offset
+    std::vector<int32_t> rowptr;
+    std::vector<uint16_t> srow;
+    std::vector<int32_t> blkq;             // block quad bases of the staged segments
+    std::vector<int64_t> fin;              // staged: sliced size (entries, 4 * quads); direct: 0
+    std::vector<TBatch> batch;             // seg: chunk-local
+    std::vector<TWork> work;               // s0/s1/b0/b1 chunk-local
+    int32_t ngroups = 0, nr = 0;
+    int64_t npre = 0, nd = 0;
+  };
+  std::vector<CL> cl(nchunk);
+  parallel_chunks(nchunk, [&](int64_t ca, int64_t cbnd) {
+    std::vector<int32_t> order;
+    for (int64_t c = ca; c < cbnd; ++c) {
+      CL& L = cl[c];
+      const int32_t nr = (int32_t)std::min<int64_t>(kTRows, rows - c * kTRows);
+      L.nr = nr;
+      const TBChunk& C = cb[c];
+      const int ns = C.direct + C.nst;
+      std::vector<int64_t> seg_nz;
+      if (C.direct) { L.seg.push_back(TSeg{-1, 1, 0, 0, -1}); seg_nz.push_back(dnz[c]); }
+      for (int k = 0; k < C.nst; ++k) { L.seg.push_back(TSeg{stiles[c][k], 1, 0, 0, -1}); seg_nz.push_back(scnt[c][k]); }
+      order.resize(nr);
+      for (int k = 0; k < ns; ++k) {
+        TSeg& S = L.seg[k];
+        const bool stg = S.tile >= 0;
+        const int32_t* rck = rc.data() + (size_t)(C.sbase + k) * kTRows;
+        for (int32_t i = 0; i < nr; ++i) order[i] = i;
+        if (stg) std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return rck[a] > rck[b]; });
+        S.rp = (int64_t)L.rowptr.size();
+        L.rowptr.resize(L.rowptr.size() + nr + 1, 0);
+        L.srow.resize(L.rowptr.size(), 0);
+        int64_t units = 0;
+        for (int32_t pos = 0; pos < nr; ++pos) {
+          const int32_t i = order[pos];
+          const int32_t u = stg ? (rck[i] + 3) / 4 : rck[i];
+          L.rowptr[S.rp + pos + 1] = L.rowptr[S.rp + pos] + u;
+          L.srow[S.rp + pos] = (uint16_t)i;
+          units += u;
+        }
+        S.V = pick_v(stg ? (double)units / nr : (double)seg_nz[k] / nr, elem);
+        if (stg) {
+          L.npre = (L.npre + 7) & ~(int64_t)7;
+          L.pre.push_back(L.npre);
+          L.npre += 4 * units;
+          // slice_plan: warp-block quad bases
+          const int rpw = 32 / S.V;
+          const int nblk = tiled_blocks(nr, S.V);
+          const int32_t* rp = L.rowptr.data() + S.rp;
+          S.bb = (int64_t)L.blkq.size();
+          int64_t q = 0;
+          for (int blk = 0; blk < nblk; ++blk) {
+            L.blkq.push_back((int32_t)q);
+            int32_t tmax = 0;
+            for (int a = 0; a < rpw && blk * rpw + a < nr; ++a) {
+              const int32_t nq = rp[blk * rpw + a + 1] - rp[blk * rpw + a];
+              tmax = std::max(tmax, (nq + S.V - 1) / S.V);
+            }
+            q += 32 * (int64_t)tmax;
+          }
+          L.fin.push_back(4 * q);
+        } else {
+          L.pre.push_back(L.nd);
+          L.nd += units;
+          L.fin.push_back(0);
+        }
+      }
+      // work items and batches (build_tiled_range's emit_item)
+      auto emit_item = [&](int32_t gg, int32_t sa, int32_t sb) {
+        const int32_t b0 = (int32_t)L.batch.size();
+        int32_t ord = -1;
+        for (int32_t si = sa; si < sb; ++si) {
+          const TSeg& S = L.seg[si];
+          if (S.tile < 0) continue;
+          ++ord;
+          const int32_t* rp = L.rowptr.data() + S.rp;
+          int first = 1;
+          int32_t ra = 0, qa = rp[0];
+          auto emit = [&](int32_t r_a, int32_t r_b, int32_t q_a, int32_t q_b) {
+            if (q_b > q_a) { L.batch.push_back(TBatch{si, r_a, r_b, q_a, q_b, first, ord, 0}); first = 0; }
+          };
+          for (int32_t r = 0; r < nr; ++r) {
+            const int32_t rq0 = rp[r], rq1 = rp[r + 1];
+            while (rq1 - qa > kBQ) {
+              if (rq0 > qa) { emit(ra, r, qa, rq0); qa = rq0; ra = r; }
+              else { emit(r, r + 1, qa, qa + kBQ); qa += kBQ; ra = r; }
+            }
+          }
+          emit(ra, nr, qa, rp[nr]);
+        }
+        L.work.push_back(TWork{0, gg, sa, sb, b0, (int32_t)L.batch.size()});
+      };
+      int32_t g = 0, ws = 0;
+      int64_t acc = 0;
+      for (int k = 0; k < ns; ++k) {
+        acc += seg_nz[k];
+        if (acc >= group_nz || k == ns - 1) { emit_item(g++, ws, k + 1); ws = k + 1; acc = 0; }
+      }
+      if (ns == 0) emit_item(g++, 0, 0);
+      L.ngroups = g;
+    }
+  });
+  tr.mark("    devbuild: host layout", nullptr, false);
+  // ---- global offsets, in chunk order (the concatenation of build_tiled)
+  std::vector<int64_t> o_rp(nchunk), o_bb(nchunk);
+  std::vector<TFillSeg> fsv;
+  fsv.reserve(nseg);
+  int64_t nrp = 0, nbb = 0, npre = 0, nd = 0, fin = 0;
+  for (int64_t c = 0; c < nchunk; ++c) {
+    CL& L = cl[c];
+    o_rp[c] = nrp;
+    o_bb[c] = nbb;
+    npre = (npre + 7) & ~(int64_t)7;
+    const int32_t sbase = (int32_t)H.seg.size(), bbase = (int32_t)H.batch.size();
+    for (size_t k = 0; k < L.seg.size(); ++k) {
+      TSeg S = L.seg[k];
+      S.rp += nrp;
+      TFillSeg F{0, S.rp, S.tile, L.nr};
+      if (S.tile >= 0) {
+        const int64_t src = npre + L.pre[k];
+        fin = (fin + 63) & ~(int64_t)63;
+        S.bb += nbb;
+        H.dseg.push_back(TDefer{src, fin, S.rp, S.bb, L.nr, S.V});
+        const int32_t di = (int32_t)H.dseg.size() - 1;
+        for (int blk = 0; blk < tiled_blocks(L.nr, S.V); ++blk) H.dblk.push_back(make_int2(di, blk));
+        S.nz = fin;
+        fin += L.fin[k];
+        F.off = src;
+      } else {
+        S.nz = nd + L.pre[k];
+        F.off = S.nz;
+      }
+      H.seg.push_back(S);
+      fsv.push_back(F);
+    }
+    for (TBatch B : L.batch) { B.seg += sbase; H.batch.push_back(B); }
+    for (TWork W : L.work) {
+      W.chunk = (int32_t)c; W.s0 += sbase; W.s1 += sbase; W.b0 += bbase; W.b1 += bbase;
+      H.work.push_back(W);
+    }
+    H.chunk.push_back(TChunk{c * kTRows, L.nr, L.ngroups, H.scratch});
+    H.scratch += (int64_t)L.ngroups * L.nr * elem;
+    nrp += (int64_t)L.rowptr.size();
+    nbb += (int64_t)L.blkq.size();
+    npre += L.npre;
+    nd += L.nd;
+  }
+  H.tot_rp = nrp + 8;
+  H.tot_bb = nbb + 1;
+  H.tot_s = fin + 8;
+  H.tot_d = nd;
+  H.tot_pre = npre;
+  H.fin_s = fin;
+  // ---- host structure arrays to the device; the inverse row order on the device
+  A.rowptr.alloc(H.tot_rp); A.srow.alloc(H.tot_rp); A.blkb.alloc(H.tot_bb);
+  DBuf<uint16_t> dposof;
+  dposof.alloc(H.tot_rp);
+  {
+    std::vector<int32_t> hrp(H.tot_rp), hbb(H.tot_bb);
+    std::vector<uint16_t> hsr(H.tot_rp);
+    parallel_chunks(nchunk, [&](int64_t a, int64_t b) {
+      for (int64_t c = a; c < b; ++c) {
+        const CL& L = cl[c];
+        std::copy(L.rowptr.begin(), L.rowptr.end(), hrp.begin() + o_rp[c]);
+        std::copy(L.srow.begin(), L.srow.end(), hsr.begin() + o_rp[c]);
+        std::copy(L.blkq.begin(), L.blkq.end(), hbb.begin() + o_bb[c]);
+      }
+    });
+    for (int64_t i = nrp; i < H.tot_rp; ++i) { hrp[i] = 0; hsr[i] = 0; }
+    hbb[H.tot_bb - 1] = 0;
+    CK(cudaMemcpyAsync(A.rowptr.p, hrp.data(), H.tot_rp * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(A.blkb.p, hbb.data(), H.tot_bb * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(A.srow.p, hsr.data(), H.tot_rp * 2, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  cl = std::vector<CL>();
+  tr.mark("    devbuild: offsets + uploads", st);
+  // ---- fill: entries to their pre / direct slots
+  DBuf<TFillSeg> dfs;
+  upload(dfs, fsv, st);
+  DBuf<uint16_t> pcol;
+  DBuf<int32_t> pperm;
+  const int64_t npre1 = std::max<int64_t>(npre, 1);
+  pcol.alloc(npre1);
+  pperm.alloc(npre1);
+  CK(cudaMemsetAsync(pcol.p, 0, npre1 * sizeof(uint16_t), st));
+  CK(cudaMemsetAsync(pperm.p, 0xff, npre1 * sizeof(int32_t), st));
+  A.col_d.alloc(std::max<int64_t>(nd, 1));
+  A.perm_d.alloc(std::max<int64_t>(nd, 1));
+  k_tile_posof<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(nseg, (int64_t)sms * 32)), 256, 0, st>>>(
+      dfs.p, nseg, A.srow.p, dposof.p);
+  k_tile_fill<<<gw, 256, 0, st>>>(dptr, dcol, rows, T, dcb.p, dstl.p, dfs.p, A.rowptr.p, dposof.p, pcol.p, pperm.p,
+                                  A.col_d.p, A.perm_d.p);
+  CK(cudaGetLastError());
+  tr.mark("    devbuild: fill", st);
+  // ---- bank balancing + sliced re-layout (the deferred build's kernels)
+  A.col_s.alloc(H.tot_s);
+  A.perm_s.alloc(H.tot_s);
+  CK(cudaMemsetAsync(A.col_s.p, 0, H.tot_s * sizeof(uint16_t), st));
+  CK(cudaMemsetAsync(A.perm_s.p, 0xff, H.tot_s * sizeof(int32_t), st));
+  const int64_t nb = (int64_t)H.dblk.size();
+  if (nb) {
+    DBuf<TDefer> dseg;
+    DBuf<int2> dblk;
+    upload(dseg, H.dseg, st);
+    upload(dblk, H.dblk, st);
+    DBuf<uint16_t> bcol, ncol;
+    DBuf<int32_t> bperm, nperm;
+    bcol.alloc(npre1); ncol.alloc(npre1); bperm.alloc(npre1); nperm.alloc(npre1);
+    const int tb = 128;
+    k_tile_balance<<<(int)((nb + tb - 1) / tb), tb, 0, st>>>(dseg.p, dblk.p, nb, elem, A.rowptr.p, pcol.p, pperm.p,
+                                                             bcol.p, bperm.p, ncol.p, nperm.p);
+    tr.mark("    devbuild: balance", st);
+    k_tile_slice<<<(int)((nb + tb - 1) / tb), tb, 0, st>>>(dseg.p, dblk.p, nb, A.rowptr.p, A.blkb.p, ncol.p,
+                                                           nperm.p, A.col_s.p, A.perm_s.p);
+    CK(cudaGetLastError());
+    tr.mark("    devbuild: slice", st);
+  }
+  CK(cudaStreamSynchronize(st));
+  H.devbuilt = true;
+  H.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+}
+
 // Input checks of the CSR on host threads: column ids in
 // range and strictly increasing per row, finite values.  Reports the first
 // offending row (and, within it, the first offending entry's check).
@@ -812,6 +1190,7 @@ ClassPolicy class_policy(const std::vector<Block>& v, int sms) {
 }  // namespace
 
 // ============================================================================
+
 struct pdcs_ctx {
   // problem (host copies of what the setup needs)
   int64_t m = 0, n = 0, n1 = 0, mg = 0, row_begin = 0;
@@ -871,7 +1250,37 @@ struct pdcs_ctx {
     float tune_csr_ms = 0.f, tune_tiled_ms = 0.f;
     double build_ms = 0.0;                     // host build of the format
     double device_build_ms = 0.0;              // deferred build: device balancing + slicing
+    TiledDevArrays dv;                         // device structure build (build_tiled_device)
+    DBuf<int32_t> ccnt;                        // per-chunk arrival counters of the fused combine
+    DBuf<TCItem> citem_w;                      // combine items of the chunks the fused kernel leaves
+    TiledMat Mw;                               // M with citem = citem_w
+    int g_combine_w = 0;
+    bool fuse = false;                         // fused combine kept for this matrix
+    float tune_fused_ms = 0.f;
   } tK, tKT;
+  // Fused combine (tiled.cuh k_tiled_sliced<ELEM, Epi>): the last work item of a
+  // chunk runs its epilogue.  Kept per matrix by the setup autotune when it is
+  // >= 3% faster than partial + combine; PDCS_FUSED_COMBINE=1 / 0 forces it on / off.
+  static int fused_env() {
+    const char* e = std::getenv("PDCS_FUSED_COMBINE");
+    return e ? (std::atoi(e) ? 1 : 0) : -1;
+  }
+  static bool fused(const TiledDev& D) { return D.fuse && D.sliced && !D.tma; }
+  template <int ELEM, class Epi>
+  void tiled_fused(const char* name, const char* wname, TiledDev& D, const double* xin, int guard, const Epi& e,
+                   double* part, int64_t slot0) {
+    launch(name, [&] {
+      k_tiled_sliced<ELEM, Epi><<<D.g_partial, kTThreads, sliced_smem(D), st>>>(D.M, xin, D.scratch.p, ctl, guard, e,
+                                                                              D.ccnt.p, part, slot0);
+    });
+    if (D.Mw.ncitem)                           // chunks of many groups: combine over their items
+      launch(wname, [&] {
+        k_tiled_combine<Epi, ELEM><<<D.g_combine_w, kThreads, 0, st>>>(D.Mw, D.scratch.p, e, ctl, part,
+                                                                        slot0 + D.M.nchunk);
+      });
+  }
+  // accumulator slots a fused sweep writes (chunks, then the wide combine's CTAs)
+  static int64_t fused_slots(const TiledDev& D) { return D.M.nchunk + D.g_combine_w; }
   // L2 column panels of K~ and K~^T (panels.cuh), kept by a setup autotune when
   // the gathered vector exceeds L2
   struct Panels {
@@ -1183,7 +1592,10 @@ struct pdcs_ctx {
     };
     run_blocks(true, bargs(true, BOP_TRIAL_PRIMAL), false, 0, &pe);
     EpiDualTrial e{y.p, ht.p, rk.p, kxh.p, kxd.p, yh.p, 0.0, 0};
-    if (tK.on) {
+    if (tK.on && fused(tK)) {
+      tiled_fused<2>("spmv_K_dual", "tiled_K_wide_combine", tK, reinterpret_cast<const double*>(xx.p), 1, e,
+                     tpart.p, slot_spmv);
+    } else if (tK.on) {
       tiled_partial("tiled_K_partial", tK, 2, reinterpret_cast<const double*>(xx.p), 1);
       launch("spmv_K_dual", [&] {
         k_tiled_combine<EpiDualTrial, 2><<<tK.g_combine, kThreads, 0, st>>>(tK.M, tK.scratch.p, e, ctl, tpart.p,
@@ -1247,7 +1659,9 @@ struct pdcs_ctx {
       return;
     }
     EpiHalpernX e{xh.p, x0.p, x.p, kty.p, xsum.p, 0, 0, 0, 0, 0};
-    if (tKT.on) {
+    if (tKT.on && fused(tKT)) {
+      tiled_fused<1>("spmv_KT_halpern", "tiled_KT_wide_combine", tKT, y.p, 2, e, nullptr, 0);
+    } else if (tKT.on) {
       tiled_partial("tiled_KT_partial", tKT, 1, y.p, 2);
       launch("spmv_KT_halpern", [&] {
         k_tiled_combine<EpiHalpernX, 1><<<tKT.g_combine, kThreads, 0, st>>>(tKT.M, tKT.scratch.p, e, ctl, nullptr, 0);
@@ -1432,15 +1846,31 @@ struct pdcs_ctx {
   void make_tiled(TiledDev& D, TiledHost& H, int64_t rows, int64_t nvec, int elem, const double* dval) {
     const double frac = H.nnz ? (double)H.staged / (double)H.nnz : 0.0;
     const char* env = std::getenv("PDCS_TILED");
-    const bool want = env ? std::atoi(env) != 0 : frac >= 0.3;
+    const bool want = H.devbuilt || (env ? std::atoi(env) != 0 : frac >= kTiledMinFrac);
     D.on = want && H.nnz > 0;
     if (!D.on) { H = TiledHost(); return; }
+    SetupTrace tr;
     upload(D.work, H.work, st);
     upload(D.batch, H.batch, st);
     upload(D.chunk, H.chunk, st);
     upload(D.seg, H.seg, st);
     DBuf<int32_t> perm;
-    if (H.parts.empty()) {
+    if (H.devbuilt) {
+      // built on the device (build_tiled_device): take its arrays, gather the values
+      take(D.rowptr, D.dv.rowptr); take(D.srow, D.dv.srow); take(D.col_s, D.dv.col_s);
+      take(D.col_d, D.dv.col_d); take(D.blkb, D.dv.blkb);
+      D.val_s.alloc(std::max<size_t>(H.tot_s, 1));
+      D.val_d.alloc(std::max<size_t>(H.tot_d, 1));
+      if (H.tot_s)
+        k_gather_vals<<<grid_for((int64_t)H.tot_s, sms, 32), kThreads, 0, st>>>((int64_t)H.tot_s, D.dv.perm_s.p, dval, D.val_s.p);
+      if (H.tot_d)
+        k_gather_vals<<<grid_for((int64_t)H.tot_d, sms, 32), kThreads, 0, st>>>((int64_t)H.tot_d, D.dv.perm_d.p, dval, D.val_d.p);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(st));
+      D.dv.perm_s.free_();
+      D.dv.perm_d.free_();
+      tr.mark("  tiled: gather values (device-built)", st);
+    } else if (H.parts.empty()) {
       upload(D.rowptr, H.rowptr, st);
       upload(D.srow, H.srow, st);
       upload(D.col_s, H.col_s, st);
@@ -1480,6 +1910,7 @@ struct pdcs_ctx {
         put(D.col_d.p, P.col_d, H.o_d[w]);
         put(D.blkb.p, P.blkb, H.o_bb[w]);
       }
+      tr.mark("  tiled: part uploads", st);
       if (H.defer && !H.dblk.empty()) {
         // bank balancing and sliced re-layout on the device (tiled.cuh)
         const auto t0 = std::chrono::steady_clock::now();
@@ -1499,8 +1930,10 @@ struct pdcs_ctx {
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(st));
         D.device_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        tr.mark("  tiled: balance + slice", st);
       }
     }
+    if (!H.devbuilt) {
     D.val_s.alloc(std::max<size_t>(H.n_s(), 1));
     D.val_d.alloc(std::max<size_t>(H.n_d(), 1));
     if (H.n_s()) {
@@ -1520,6 +1953,8 @@ struct pdcs_ctx {
       k_gather_vals<<<grid_for((int64_t)H.n_d(), sms, 32), kThreads, 0, st>>>((int64_t)H.n_d(), perm.p, dval, D.val_d.p);
       CK(cudaStreamSynchronize(st));
     }
+    tr.mark("  tiled: gather values", st);
+    }
     D.scratch.alloc(std::max<int64_t>(H.scratch, 1));
     TiledMat& M = D.M;
     M.m = rows; M.nvec = nvec; M.nwork = (int64_t)H.work.size(); M.nchunk = (int64_t)H.chunk.size();
@@ -1536,6 +1971,8 @@ struct pdcs_ctx {
     if (elem == 2) {
       CK(cudaFuncSetAttribute(k_tiled_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_sliced<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
+      CK(cudaFuncSetAttribute(k_tiled_sliced<2, EpiDualTrial>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
+      CK(cudaFuncSetAttribute(k_tiled_sliced<2, EpiStore2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(D)));
       if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<2>, kTThreads, tma_smem(D)));
       else if (D.sliced) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_sliced<2>, kTThreads, sliced_smem(D)));
@@ -1543,6 +1980,8 @@ struct pdcs_ctx {
     } else {
       CK(cudaFuncSetAttribute(k_tiled_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_sliced<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
+      CK(cudaFuncSetAttribute(k_tiled_sliced<1, EpiHalpernX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
+      CK(cudaFuncSetAttribute(k_tiled_sliced<1, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(D)));
       if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<1>, kTThreads, tma_smem(D)));
       else if (D.sliced) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_sliced<1>, kTThreads, sliced_smem(D)));
@@ -1556,10 +1995,23 @@ struct pdcs_ctx {
       for (int32_t r0 = 0; r0 < C.nrows; r0 += step) citems.push_back(TCItem{(int32_t)c, r0});
     }
     upload(D.citem, citems, st);
+    {
+      std::vector<TCItem> wide;
+      for (const TCItem& I : citems)
+        if (H.chunk[I.chunk].ngroups >= kCombWideG) wide.push_back(I);
+      upload(D.citem_w, wide, st);
+      D.Mw = M;
+      D.Mw.citem = D.citem_w.p;
+      D.Mw.ncitem = (int64_t)wide.size();
+      D.g_combine_w = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)wide.size(), (int64_t)sms * 8));
+    }
+    D.ccnt.alloc(std::max<int64_t>(M.nchunk, 1));
+    CK(cudaMemsetAsync(D.ccnt.p, 0, std::max<int64_t>(M.nchunk, 1) * sizeof(int32_t), st));
     M.citem = D.citem.p;
     M.ncitem = (int64_t)citems.size();
     H = TiledHost();                           // host copy no longer needed
     D.g_combine = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)citems.size(), (int64_t)sms * 8));
+    D.fuse = fused_env() == 1;
     // Setup-time autotune: keep the tiled copy only if it beats the CSR kernel
     // by >= 10% on this matrix (gather locality decides).
     if (!env) {
@@ -1579,6 +2031,10 @@ struct pdcs_ctx {
           EpiStore e{out.p};
           spmv_kernel<EpiStore><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, xin.p, nullptr, A.plan, e, ctl, nullptr, 0);
         }
+      };
+      auto run_fused = [&] {
+        if (elem == 2) tiled_fused<2>("autotune", "autotune", D, xin.p, 0, EpiStore2{out.p}, nullptr, 0);
+        else tiled_fused<1>("autotune", "autotune", D, xin.p, 0, EpiStore{out.p}, nullptr, 0);
       };
       auto run_tiled = [&] {
         if (elem == 2) {
@@ -1605,7 +2061,14 @@ struct pdcs_ctx {
         std::sort(v, v + 5);
         return v[2];
       };
-      const float tc = timeit(run_csr), tt = timeit(run_tiled);
+      const float tc = timeit(run_csr);
+      float tt = timeit(run_tiled);
+      const int fe = fused_env();
+      if (D.sliced && !D.tma && fe != 0) {
+        D.tune_fused_ms = timeit(run_fused);
+        D.fuse = fe == 1 || D.tune_fused_ms < 0.97f * tt;
+        if (D.fuse) tt = std::min(tt, D.tune_fused_ms);
+      }
       CK(cudaGetLastError());
       cudaEventDestroy(a);
       cudaEventDestroy(b);
@@ -1899,18 +2362,6 @@ const char* pdcs_last_error(const pdcs_ctx* ctx) {
 
 }  // extern "C"
 
-// PDCS_SETUP_TRACE=1: wall ms of the setup phases on stderr (diagnostics).
-struct SetupTrace {
-  bool on = std::getenv("PDCS_SETUP_TRACE") && std::atoi(std::getenv("PDCS_SETUP_TRACE"));
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void mark(const char* what, cudaStream_t st = nullptr, bool sync = true) {
-    if (!on) return;
-    if (sync) cudaStreamSynchronize(st);
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[pdcs setup] %-28s %9.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-};
 
 // pdcs_create / pdcs_create_loopback: the communicator is NCCL (nccl_unique_id),
 // an in-process loopback group (loop), or none.
@@ -2007,9 +2458,13 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     }
     // tiled format of K~ (structure only) on host threads, overlapping the uploads
     // and the device transpose below; joined before this call returns
-    ctx->thK = std::thread([ctx, hcolp, m, n] {
-      build_tiled(ctx->hptr.data(), hcolp, m, n, 2, ctx->hK, true, true);
-    });
+    // (PDCS_TILE_DEVBUILD=0: on host threads, overlapping the uploads and the
+    // device transpose below; else on the device once K is there)
+    const bool devb = tiled_devbuild_env();
+    if (!devb)
+      ctx->thK = std::thread([ctx, hcolp, m, n] {
+        build_tiled(ctx->hptr.data(), hcolp, m, n, 2, ctx->hK, true, true);
+      });
     struct Joiner {
       std::thread& t;
       ~Joiner() { if (t.joinable()) t.join(); }
@@ -2064,6 +2519,11 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     ctx->K.m = m; ctx->K.n = n; ctx->K.nnz = nnz;
     ctx->K.ptr = ctx->Kptr.p; ctx->K.col = ctx->Kcol.p; ctx->K.val = ctx->Kval.p;
     tr.mark("upload K", st);
+    if (devb) {
+      build_tiled_device(ctx->Kptr.p, ctx->Kcol.p, ctx->hptr.data(), m, n, 2, kTiledMinFrac, ctx->hK, ctx->tK.dv, st,
+                         ctx->sms);
+      tr.mark("tiled K (device build)", st);
+    }
     // ---- device CSR(K^T) by a stable radix sort of the entries on column id
     ctx->KTptr.alloc(n + 1);
     ctx->KTcol.alloc(nnz);
@@ -2109,6 +2569,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     std::vector<size_t> offs;
     ctx->build_plan(ctx->K, ctx->hptr, rowstore, offs);
     ctx->build_plan(ctx->KT, tptr, rowstore, offs);
+    tr.mark("  SpMV plans", nullptr, false);
     // sharded: K~^T in row chunks whose all-reduces overlap the next chunk's sums
     if (ctx->dist) {
       const char* e = std::getenv("PDCS_AR_CHUNKS");
@@ -2128,12 +2589,19 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     }
     // tiled format of K~^T from the transposed structure, in the background
     // (joined in pdcs_set_cones, which uses it after the Ruiz scaling)
-    ctx->hKTptr = std::move(tptr);
-    ctx->hKTcol.resize(nnz);
-    if (nnz) CK(cudaMemcpy(ctx->hKTcol.data(), ctx->KTcol.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    ctx->thKT = std::thread([ctx, m, n] {
-      build_tiled(ctx->hKTptr.data(), ctx->hKTcol.data(), n, m, 1, ctx->hKT, true, true);
-    });
+    if (devb) {
+      build_tiled_device(ctx->KTptr.p, ctx->KTcol.p, tptr.data(), n, m, 1, kTiledMinFrac, ctx->hKT, ctx->tKT.dv, st,
+                         ctx->sms);
+      tr.mark("  tiled K^T (device build)", st);
+    } else {
+      ctx->hKTptr = std::move(tptr);
+      ctx->hKTcol.resize(nnz);
+      if (nnz) CK(cudaMemcpy(ctx->hKTcol.data(), ctx->KTcol.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      tr.mark("  K^T ids to host", nullptr, false);
+      ctx->thKT = std::thread([ctx, m, n] {
+        build_tiled(ctx->hKTptr.data(), ctx->hKTcol.data(), n, m, 1, ctx->hKT, true, true);
+      });
+    }
     upload(ctx->planrows, rowstore, st);
     ctx->patch_plan(ctx->K);
     ctx->patch_plan(ctx->KT);
@@ -2156,7 +2624,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     std::memset(ctx->hctl, 0, sizeof(Ctl));
     CK(cudaStreamSynchronize(st));
     tr.mark("plans + K^T to host", st);
-    ctx->thK.join();
+    if (ctx->thK.joinable()) ctx->thK.join();
     tr.mark("join tiled K build", nullptr, false);
     ctx->tK.build_ms = ctx->hK.build_ms;
     ctx->t_create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
@@ -2324,7 +2792,8 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     int64_t s = 0;
     ctx->slot_pe = s; s += ctx->g_pe;
     for (int c = 0; c < kNClass; ++c) if (ctx->pcls[c].count) { ctx->pcls[c].slot = s; s += ctx->pcls[c].grid; }
-    ctx->slot_spmv = s; s += std::max<int64_t>(ctx->K.plan.total_cta, (int64_t)ctx->sms * 8);   // also the tiled combine and panel finish grids
+    ctx->slot_spmv = s;   // also the tiled combine and panel finish grids, and the fused combine's chunks
+    s += std::max<int64_t>({ctx->K.plan.total_cta, (int64_t)ctx->sms * 8, ctx->tK.on ? pdcs_ctx::fused_slots(ctx->tK) : 0});
     for (int c = 0; c < kNClass; ++c) if (ctx->rcls[c].count) { ctx->rcls[c].slot = s; s += ctx->rcls[c].grid; }
     ctx->nslot_trial = s;
     int64_t ks = 0;
@@ -2816,7 +3285,7 @@ int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
   if (!ctx || !out || !ctx->ctl) return 0;
   if (guard(ctx, [&] { ctx->read_ctl(); }) != PDCS_OK) return 0;
   const Ctl& C = *ctx->hctl;
-  double v[43] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
+  double v[47] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
                   (double)C.restarts, C.e_anchor, C.Wsum, C.eta_init,
                   C.kkt[0][0], C.kkt[0][1], C.kkt[0][2], C.kkt[0][3], C.kkt[0][4],
                   C.kkt[1][0], C.kkt[1][1], C.kkt[1][2], C.kkt[1][3], C.kkt[1][4],
@@ -2826,8 +3295,9 @@ int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
                   ctx->tK.build_ms, ctx->tKT.build_ms, ctx->t_create_ms, ctx->t_cones_ms,
                   (double)ctx->colperm, (double)(ctx->pK.on ? ctx->pK.P : 0), ctx->pK.tune_csr_ms,
                   ctx->pK.tune_panel_ms, (double)(ctx->pKT.on ? ctx->pKT.P : 0), ctx->pKT.tune_csr_ms,
-                  ctx->pKT.tune_panel_ms};
-  const int k = std::min(cap, 43);
+                  ctx->pKT.tune_panel_ms, (double)pdcs_ctx::fused(ctx->tK), ctx->tK.tune_fused_ms,
+                  (double)pdcs_ctx::fused(ctx->tKT), ctx->tKT.tune_fused_ms};
+  const int k = std::min(cap, 47);
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }
@@ -2916,6 +3386,81 @@ int pdcs_tiled_device_check(const int64_t* row_ptr, const int32_t* col, int64_t 
                A.seg[i].V != B.seg[i].V || A.seg[i].tile != B.seg[i].tile;
     }
     out[0] = bad; out[1] = A.build_ms; out[2] = B.build_ms; out[3] = dev_ms; out[4] = (double)hc.size();
+    return 5;
+  } catch (...) {
+    return -1;
+  }
+}
+
+// Device structure build (build_tiled_device, the solver's default) against
+// the all-host build, entry by entry: column ids and value permutation of the
+// staged and direct entries, row pointers, row order, block bases, segment
+// descriptors, work items, batches and chunks.  out[0] = mismatches; out[1] =
+// all-host ms; out[2] = device-build ms; out[3] = staged entries; out[4] =
+// layout entries.  Returns 5, 0 on bad arguments (or when the layout is not
+// the sliced, balanced one), -1 on a CUDA error.
+int pdcs_tiled_devbuild_check(const int64_t* row_ptr, const int32_t* col, int64_t rows, int64_t nvec, int elem,
+                              double* out) {
+  if (!row_ptr || (!col && row_ptr[rows] > 0) || rows < 0 || nvec <= 0 || (elem != 1 && elem != 2) || !out)
+    return 0;
+  if (!tiled_devbuild_env() || row_ptr[rows] >= ((int64_t)1 << 31)) return 0;
+  try {
+    TiledHost A, B;
+    build_tiled(row_ptr, col, rows, nvec, elem, A);                  // all host
+    cudaStream_t st = nullptr;
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t nnz = row_ptr[rows];
+    std::vector<int32_t> p32(rows + 1);
+    for (int64_t i = 0; i <= rows; ++i) p32[i] = (int32_t)row_ptr[i];
+    DBuf<int32_t> dptr, dcol;
+    upload(dptr, p32, st);
+    dcol.alloc(std::max<int64_t>(nnz, 1));
+    if (nnz) CK(cudaMemcpy(dcol.p, col, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+    TiledDevArrays D;
+    build_tiled_device(dptr.p, dcol.p, row_ptr, rows, nvec, elem, -1.0, B, D, st, sms);
+    CK(cudaDeviceSynchronize());
+    double bad = 0;
+    auto dl = [](const auto& d, size_t n, auto* tag) {
+      std::vector<std::remove_pointer_t<decltype(tag)>> h(n);
+      if (n) CK(cudaMemcpy(h.data(), d.p, n * sizeof(h[0]), cudaMemcpyDeviceToHost));
+      return h;
+    };
+    const auto hc = dl(D.col_s, B.tot_s, (uint16_t*)nullptr);
+    const auto hp = dl(D.perm_s, B.tot_s, (int32_t*)nullptr);
+    const auto hr = dl(D.rowptr, B.tot_rp, (int32_t*)nullptr);
+    const auto hs = dl(D.srow, B.tot_rp, (uint16_t*)nullptr);
+    const auto hb = dl(D.blkb, B.tot_bb, (int32_t*)nullptr);
+    const auto hcd = dl(D.col_d, B.tot_d, (int32_t*)nullptr);
+    const auto hpd = dl(D.perm_d, B.tot_d, (int32_t*)nullptr);
+    // staged entries: equal up to the shorter array; the longer one's tail is
+    // padding (the host build rounds part ends up to 64 entries)
+    const size_t ns = std::min(A.col_s.size(), hc.size());
+    for (size_t i = 0; i < ns; ++i) bad += (A.col_s[i] != hc[i]) + (A.perm_s[i] != hp[i]);
+    for (size_t i = ns; i < A.col_s.size(); ++i) bad += A.col_s[i] != 0 || A.perm_s[i] != -1;
+    for (size_t i = ns; i < hc.size(); ++i) bad += hc[i] != 0 || hp[i] != -1;
+    if (A.rowptr.size() != hr.size() || A.srow.size() != hs.size() || A.blkb.size() != hb.size() ||
+        A.col_d.size() != hcd.size() || A.seg.size() != B.seg.size() || A.work.size() != B.work.size() ||
+        A.chunk.size() != B.chunk.size() || A.batch.size() != B.batch.size() || A.scratch != B.scratch ||
+        A.staged != B.staged)
+      bad += 1e18;
+    else {
+      for (size_t i = 0; i < hr.size(); ++i) bad += (A.rowptr[i] != hr[i]) + (A.srow[i] != hs[i]);
+      for (size_t i = 0; i < hb.size(); ++i) bad += A.blkb[i] != hb[i];
+      for (size_t i = 0; i < hcd.size(); ++i) bad += (A.col_d[i] != hcd[i]) + (A.perm_d[i] != hpd[i]);
+      for (size_t i = 0; i < A.seg.size(); ++i)
+        bad += A.seg[i].nz != B.seg[i].nz || A.seg[i].bb != B.seg[i].bb || A.seg[i].rp != B.seg[i].rp ||
+               A.seg[i].V != B.seg[i].V || A.seg[i].tile != B.seg[i].tile;
+      for (size_t i = 0; i < A.work.size(); ++i)
+        bad += std::memcmp(&A.work[i], &B.work[i], sizeof(TWork)) != 0;
+      for (size_t i = 0; i < A.batch.size(); ++i)
+        bad += std::memcmp(&A.batch[i], &B.batch[i], sizeof(TBatch)) != 0;
+      for (size_t i = 0; i < A.chunk.size(); ++i)
+        bad += A.chunk[i].row0 != B.chunk[i].row0 || A.chunk[i].nrows != B.chunk[i].nrows ||
+               A.chunk[i].ngroups != B.chunk[i].ngroups || A.chunk[i].scratch != B.chunk[i].scratch;
+    }
+    out[0] = bad; out[1] = A.build_ms; out[2] = B.build_ms; out[3] = (double)B.staged; out[4] = (double)hc.size();
     return 5;
   } catch (...) {
     return -1;

@@ -19,6 +19,7 @@
 // and applies the fused epilogue (dual update / Halpern step), so results are
 // deterministic.
 #pragma once
+#include <type_traits>
 #include "spmv.cuh"
 
 namespace pdcs {
@@ -596,11 +597,76 @@ __device__ __forceinline__ int32_t next_staged(const TiledMat& M, int32_t s, int
 #ifndef PDCS_TS_MINB1
 #define PDCS_TS_MINB1 2               // k_tiled_sliced<1>: 64 registers (40 spills)
 #endif
-template <int ELEM>
+// EpiNone: the partial kernel alone (k_tiled_combine runs the epilogue).
+struct EpiNone {
+  static constexpr int NA = 1;
+  static constexpr int NX = 1;
+  __device__ void init(const Ctl*) {}
+  __device__ bool active() const { return true; }
+  __device__ void row(int64_t, double, double, Acc<1>&) {}
+};
+
+// Fused combine (Epi != EpiNone): the CTA that completes a chunk's last work
+// item (per-chunk arrival counter, reset by that CTA) sums the chunk's group
+// partials in k_tiled_combine's order and runs the epilogue on its rows; the
+// epilogue's accumulators go to slot slot0 + chunk.  A chunk of one work item
+// takes its sums straight from shared memory.  Same sums, bit for bit, as
+// partial + combine; one launch and one scratch round trip fewer.  Chunks of
+// >= kCombWideG groups (Lasso K^T's long rows: ~150) would leave one CTA
+// reading ~1 MB of partials at the end of the sweep: their partials are
+// written as before and a combine launch over their items only follows.
+template <class Epi, int ELEM>
+__device__ __forceinline__ void chunk_epilogue(const TChunk& C, const double* __restrict__ src, const double* acc,
+                                               Epi& epi, double* part, int64_t slot) {
+  Acc<Epi::NA> a;
+  a.zero();
+  if (!src) {                                        // one group: the sums are in shared memory
+    for (int r = threadIdx.x; r < C.nrows; r += blockDim.x) {
+      double s1 = 0.0, s2 = 0.0;
+      s1 += acc[r * ELEM];
+      if (ELEM == 2) s2 += acc[r * ELEM + 1];
+      epi.row(C.row0 + r, s1, s2, a);
+    }
+  } else {                                           // groups added in order (ngroups < kCombWideG)
+    for (int r = threadIdx.x; r < C.nrows; r += blockDim.x) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int g = 0; g < C.ngroups; ++g) {
+        s1 += __ldcg(src + ((int64_t)g * C.nrows + r) * ELEM);
+        if (ELEM == 2) s2 += __ldcg(src + ((int64_t)g * C.nrows + r) * ELEM + 1);
+      }
+      epi.row(C.row0 + r, s1, s2, a);
+    }
+  }
+  if (part) {                                        // fixed-order CTA reduction (up to 32 warps)
+    __shared__ double red[Epi::NA][32];
+#pragma unroll
+    for (int i = 0; i < Epi::NA; ++i) {
+      double v = a.v[i];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0) red[i][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < Epi::NA) {
+      double v = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
+      part[slot * Epi::NA + threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+}
+
+template <int ELEM, class Epi = EpiNone>
 __global__ void __launch_bounds__(kTThreads, ELEM == 1 ? PDCS_TS_MINB1 : PDCS_TP_MINB)
-    k_tiled_sliced(TiledMat M, const double* __restrict__ x, double* __restrict__ scratch, const Ctl* ctl, int guard) {
+    k_tiled_sliced(TiledMat M, const double* __restrict__ x, double* __restrict__ scratch, const Ctl* ctl, int guard,
+                   Epi epi = Epi(), int32_t* chunk_cnt = nullptr, double* part = nullptr, int64_t slot0 = 0) {
+  constexpr bool kFused = !std::is_same<Epi, EpiNone>::value;
   if (guard >= 1 && ctl->status != 4) return;
   if (guard == 2 && !ctl->accepted) return;
+  if (kFused) {
+    epi.init(ctl);
+    if (!epi.active()) return;
+  }
   extern __shared__ __align__(128) double smem[];
   const int64_t TE = (int64_t)M.T * ELEM;
   double* tiles = smem;                              // 2 buffers of T * ELEM doubles
@@ -653,8 +719,29 @@ __global__ void __launch_bounds__(kTThreads, ELEM == 1 ? PDCS_TS_MINB1 : PDCS_TP
       __syncthreads();                                 // acc rows are shared across segments
     }
     double* out = scratch + C.scratch + (int64_t)W.group * C.nrows * ELEM;
-    for (int i = threadIdx.x; i < C.nrows * ELEM; i += blockDim.x) out[i] = acc[i];
-    __syncthreads();
+    if (!kFused || C.ngroups >= kCombWideG) {
+      // partials only (chunks of many groups: k_tiled_combine over their items)
+      for (int i = threadIdx.x; i < C.nrows * ELEM; i += blockDim.x) out[i] = acc[i];
+      __syncthreads();
+    } else if (C.ngroups == 1) {
+      chunk_epilogue<Epi, ELEM>(C, nullptr, acc, epi, part, slot0 + W.chunk);
+      __syncthreads();
+    } else {
+      __shared__ int s_last;
+      for (int i = threadIdx.x; i < C.nrows * ELEM; i += blockDim.x) __stcg(out + i, acc[i]);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_last = atomicAdd(chunk_cnt + W.chunk, 1) == C.ngroups - 1;
+        if (s_last) chunk_cnt[W.chunk] = 0;          // ready for the next launch
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        chunk_epilogue<Epi, ELEM>(C, scratch + C.scratch, acc, epi, part, slot0 + W.chunk);
+      }
+      __syncthreads();
+    }
   }
   cp_async_wait_all();
 }
@@ -801,6 +888,144 @@ __global__ void k_tile_slice(const TDefer* __restrict__ dseg, const int2* __rest
         col_s[to + k] = ncol[from + k];
         perm_s[to + k] = nperm[from + k];
       }
+    }
+  }
+}
+
+// ---- Device structure build -------------------------------
+// The column-tiled layout built from a device CSR without the entries passing
+// through the host: k_tile_hist counts the entries of every (chunk, tile),
+// the host picks the staged tiles per chunk; k_tile_rowcnt counts every row's
+// entries per segment, the host orders the rows and lays out the segments
+// (only O(segments x rows) work); k_tile_fill writes the column ids and CSR
+// positions of every entry at their slots of the unbalanced row-major quads
+// (staged segments) or of col_d (direct).  k_tile_balance / k_tile_slice then
+// finish as in the deferred build.  Same layout, bit for bit, as build_tiled
+// (tests/test_tiled_layout.py, pdcs_tiled_devbuild_check).
+struct TBChunk {
+  int64_t sbase;      // global index of the chunk's first segment
+  int32_t soff, nst;  // its staged tiles, ascending: stl[soff, soff + nst)
+  int32_t direct;     // 1: the chunk's segment 0 is its direct segment
+  int32_t pad;
+};
+struct TFillSeg {
+  int64_t off;        // staged: first entry of its pre quads; direct: first entry in col_d
+  int64_t rp;         // its row pointers (and posof)
+  int32_t tile;       // -1: direct
+  int32_t nr;         // rows of its chunk
+};
+
+// Chunk-local segment of an entry in tile t: the staged tile's slot, else the
+// direct segment (index 0; it exists whenever a touched tile is not staged).
+__device__ __forceinline__ int tb_seg_of(const TBChunk& C, const int32_t* __restrict__ stl, int32_t t) {
+  int lo = 0, hi = C.nst;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(stl + C.soff + mid) < t) lo = mid + 1; else hi = mid;
+  }
+  return (lo < C.nst && __ldg(stl + C.soff + lo) == t) ? C.direct + lo : 0;
+}
+
+// Entries per (chunk, tile) for chunks [c0, c1): out[(c - c0) * ntiles + t]
+// (zeroed by the caller); a shared-memory histogram when ntiles fits.
+__global__ void k_tile_hist(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col, int64_t rows,
+                            int32_t T, int64_t ntiles, int64_t c0, int32_t* __restrict__ out, int use_smem) {
+  extern __shared__ int32_t hist[];
+  const int64_t c = c0 + blockIdx.x;
+  const int64_t r0 = c * kTRows, r1 = (rows < r0 + kTRows) ? rows : r0 + kTRows;
+  int32_t* dst = out + (int64_t)blockIdx.x * ntiles;
+  if (use_smem) {
+    for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) hist[t] = 0;
+    __syncthreads();
+  }
+  for (int64_t p = __ldg(ptr + r0) + threadIdx.x; p < __ldg(ptr + r1); p += blockDim.x) {
+    const int32_t t = __ldg(col + p) / T;
+    atomicAdd(use_smem ? hist + t : dst + t, 1);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) dst[t] = hist[t];
+  }
+}
+
+// Entries of every row per segment: rc[(sbase + k) * kTRows + i] (zeroed by
+// the caller).  One warp per row; lanes of one segment add once.
+__global__ void k_tile_rowcnt(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col, int64_t rows,
+                              int32_t T, const TBChunk* __restrict__ cb, const int32_t* __restrict__ stl,
+                              int32_t* __restrict__ rc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarp) {
+    const TBChunk C = cb[r / kTRows];
+    const int64_t i = r % kTRows;
+    const int32_t b = __ldg(ptr + r), e = __ldg(ptr + r + 1);
+    for (int32_t p0 = b; p0 < e; p0 += 32) {
+      const int32_t p = p0 + lane;
+      const bool ok = p < e;
+      const int k = ok ? tb_seg_of(C, stl, __ldg(col + p) / T) : -1 - lane;
+      const unsigned same = __match_any_sync(0xffffffffu, k);
+      if (ok && lane == __ffs(same) - 1) atomicAdd(rc + (C.sbase + k) * kTRows + i, __popc(same));
+    }
+  }
+}
+
+// Inverse of every segment's row order: posof[rp + srow[rp + pos]] = pos.
+__global__ void k_tile_posof(const TFillSeg* __restrict__ fs, int64_t nseg, const uint16_t* __restrict__ srow,
+                             uint16_t* __restrict__ posof) {
+  for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+    const TFillSeg S = fs[g];
+    for (int pos = threadIdx.x; pos < S.nr; pos += blockDim.x) posof[S.rp + srow[S.rp + pos]] = (uint16_t)pos;
+  }
+}
+
+// Column id and CSR position of every entry at its slot: entry f of row i in
+// segment k (f counted in CSR order within the row) goes to unit
+// rowptr[rp + posof[rp + i]] of the segment (quads for staged segments).
+__global__ void k_tile_fill(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col, int64_t rows,
+                            int32_t T, const TBChunk* __restrict__ cb, const int32_t* __restrict__ stl,
+                            const TFillSeg* __restrict__ fs, const int32_t* __restrict__ rowptr,
+                            const uint16_t* __restrict__ posof, uint16_t* __restrict__ pcol,
+                            int32_t* __restrict__ pperm, int32_t* __restrict__ col_d, int32_t* __restrict__ perm_d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarp) {
+    const TBChunk C = cb[r / kTRows];
+    const int64_t i = r % kTRows;
+    const int32_t b = __ldg(ptr + r), e = __ldg(ptr + r + 1);
+    int32_t carry_t = -1, carry_start = 0, carry_d = 0;
+    for (int32_t p0 = b; p0 < e; p0 += 32) {
+      const int32_t p = p0 + lane;
+      const bool ok = p < e;
+      const unsigned act = __ballot_sync(0xffffffffu, ok);
+      const int32_t cv = ok ? __ldg(col + p) : 0;
+      const int32_t t = ok ? cv / T : -1 - lane;
+      const int k = ok ? tb_seg_of(C, stl, t) : 0;
+      const TFillSeg S = fs[C.sbase + k];
+      const bool staged = ok && S.tile >= 0;
+      // staged: position within the row's run of tile t (columns ascend, so a
+      // tile's entries are contiguous in the row)
+      const unsigned same = __match_any_sync(0xffffffffu, t);
+      const int lead = __ffs(same) - 1;
+      const int32_t start = (lead == 0 && t == carry_t) ? carry_start : p0 + lead;
+      // direct: rank among the row's direct entries
+      const unsigned dm = __ballot_sync(0xffffffffu, ok && !staged);
+      const int32_t fd = carry_d + __popc(dm & ((1u << lane) - 1u));
+      if (ok) {
+        const int32_t unit = __ldg(rowptr + S.rp + __ldg(posof + S.rp + i));
+        if (staged) {
+          const int64_t q = S.off + 4 * (int64_t)unit + (p - start);
+          pcol[q] = (uint16_t)(cv - t * T);
+          pperm[q] = p;
+        } else {
+          const int64_t q = S.off + unit + fd;
+          col_d[q] = cv;
+          perm_d[q] = p;
+        }
+      }
+      const int last = 31 - __clz(act);
+      carry_t = __shfl_sync(0xffffffffu, t, last);
+      carry_start = __shfl_sync(0xffffffffu, start, last);
+      carry_d += __popc(dm);
     }
   }
 }

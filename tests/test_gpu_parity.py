@@ -367,6 +367,34 @@ def test_tiled_build_threads_and_bank_balance(P, tiled_env, monkeypatch):
     assert parity(*runs["t1"], *o.get_iterate(0)) <= TOL
 
 
+def test_fused_combine_matches_partial_plus_combine(P, tiled_env, monkeypatch):
+    """The fused combine (the last work item of a chunk sums the chunk's group
+    partials and runs the epilogue, tiled.cuh k_tiled_sliced<ELEM, Epi>) adds
+    the same partials in the same order as k_tiled_combine: with fixed steps
+    (vanilla PDHG) the iterates are bit-identical; with the line search only
+    the epilogue's accumulator order differs (per chunk instead of per combine
+    CTA).  Chunks of one and of many work items (TILE_GROUP) both occur."""
+    monkeypatch.setenv("PDCS_TILE_KB", "2")
+    prog = gen_lasso(5000, 400, 0.05, seed=9)
+    for vanilla in (1, 0):
+        runs = {}
+        for fused in ("1", "0"):
+            for grp in ("4000", "1000000"):
+                monkeypatch.setenv("PDCS_FUSED_COMBINE", fused)
+                monkeypatch.setenv("PDCS_TILE_GROUP", grp)
+                g = P.PdcsSolver(prog, vanilla_pdhg=vanilla)
+                assert g.scalars()["tiled_K"] == 1.0 and g.scalars()["tiled_KT"] == 1.0
+                g.iterate(80)
+                runs[(fused, grp)] = g.get_iterate(P.CURRENT)
+                g.close()
+        for grp in ("4000", "1000000"):
+            a, b = runs[("1", grp)], runs[("0", grp)]
+            if vanilla:
+                assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+            else:
+                assert parity(*a, *b) <= 1e-11
+
+
 def test_cfg5_recipe_parity(P):
     """SURVEY §8(d) cfg 5 recipe (row lengths 20..180, values over 8 decades,
     all six cone kinds, log-uniform SOC dims up to 4096 -> thread/warp/CTA

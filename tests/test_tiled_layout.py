@@ -141,3 +141,51 @@ def test_device_balanced_build_is_bit_identical(monkeypatch, kb, elem, which):
         r = _lib.pdcs_tiled_device_check(A.indptr.astype(np.int64), A.indices.astype(np.int32), A.shape[0],
                                          nvec, elem)
         assert r["mismatches"] == 0 and r["entries"] > 0, r
+
+
+def _banded_csr(rng, rows, cols, row_len, band):
+    """Rows whose columns cluster in a band (staged tiles) plus a few random
+    far columns (direct entries), with empty rows sprinkled in."""
+    ptr = [0]
+    idx = []
+    for r in range(rows):
+        k = 0 if r % 97 == 5 else int(rng.integers(row_len[0], row_len[1] + 1))
+        lo = (r * 7) % max(1, cols - band)
+        near = rng.choice(band, size=min(k, band), replace=False) + lo
+        far = rng.choice(cols, size=int(rng.integers(0, 4)), replace=False) if k else np.zeros(0, np.int64)
+        c = np.unique(np.concatenate([near, far]).astype(np.int64))
+        idx.append(c)
+        ptr.append(ptr[-1] + len(c))
+    idx = np.concatenate(idx)
+    return sp.csr_matrix((np.ones(len(idx)), idx, ptr), shape=(rows, cols))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kb,elem,which", [("1", 2, "K"), ("2", 1, "KT"), ("32", 2, "K"), ("32", 1, "KT"),
+                                           ("4", 2, "rand"), ("4", 1, "rand"), ("2", 2, "band"),
+                                           ("1", 1, "band"), ("32", 2, "mpoK"), ("32", 1, "fisherKT")])
+def test_device_structure_build_is_bit_identical(monkeypatch, kb, elem, which):
+    """The device structure build (build_tiled_device: the (chunk, tile) and
+    per-row segment counts, the entries' slots and the bank balancing on the
+    device; the host sees counts only) gives the all-host build's layout entry
+    for entry: staged and direct column ids and value permutation, row
+    pointers, row order, block bases, segment descriptors, work items,
+    batches, chunks (pdcs_tiled_devbuild_check).  Ragged last chunks, empty
+    rows and chunks with no staged tile are covered."""
+    monkeypatch.setenv("PDCS_TILE_KB", kb)
+    rng = np.random.default_rng(11)
+    if which == "rand":
+        A = _random_csr(rng, 3000, 9000, (1, 300)); nvec = 9000
+    elif which == "band":
+        A = _banded_csr(rng, 2500, 20000, (0, 400), 1500); nvec = 20000
+    elif which == "mpoK":
+        A, _ = _csr(gen_mpo(4, 200, seed=1)); nvec = A.shape[1]
+    elif which == "fisherKT":
+        _, A = _csr(gen_fisher(300, 100, 0.2, seed=2)); nvec = A.shape[1]
+    else:
+        K, KT = _csr(gen_lasso(3000, 300, 0.2, seed=6))
+        A = K if which == "K" else KT
+        nvec = A.shape[1]
+    r = _lib.pdcs_tiled_devbuild_check(A.indptr.astype(np.int64), A.indices.astype(np.int32), A.shape[0],
+                                       nvec, elem)
+    assert r["mismatches"] == 0 and r["entries"] > 0, r

@@ -12,7 +12,7 @@ prog, gen_s = bench.build_instance(cfg, 0)
 rows = (0, prog.m)
 host = bench.pinned(prog, rows)
 st = torch.cuda.Stream()
-for rep in range(2):
+for rep in range(int(os.environ.get('REPS', '2'))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ctx = bench.make_ctx(P, prog, host, P.pdcs_default_params(), st.cuda_stream, 0, rows)
@@ -21,4 +21,7 @@ for rep in range(2):
     sc = P.pdcs_get_scalars(ctx)
     print(json.dumps({"config": cfg, "rep": rep, "wall_s": t1 - t0,
                       **{k: sc[k] for k in sc if k.startswith(("setup", "tiled", "tune"))}}), flush=True)
+    t2 = time.perf_counter()
     P.pdcs_destroy(ctx)
+    torch.cuda.synchronize()
+    print(json.dumps({"destroy_s": time.perf_counter() - t2}), flush=True)

@@ -343,8 +343,11 @@ pdcs_status pdcs_nccl_unique_id(void *out128);
  * alloc(bytes, user) returns device memory on the context's device or NULL
  * (the call then fails with PDCS_ERR_CUDA); free(ptr, user) releases it.
  * Process-wide; set it before pdcs_create and keep it until every context
- * using it is destroyed.  NULL, NULL restores cudaMalloc / cudaFree.
- * Buffers are allocated at create / set_cones time only, never per iteration.
+ * using it is destroyed.  NULL, NULL restores the default: a library-owned
+ * stream-ordered memory pool per device (cudaMallocFromPoolAsync, used
+ * synchronously) that keeps freed memory for later contexts of the process
+ * (PDCS_POOL=0: plain cudaMalloc / cudaFree).  Buffers are allocated at
+ * create / set_cones time only, never per iteration.
  * Errors: ARG (one function NULL, the other not). */
 typedef void *(*pdcs_alloc_fn)(size_t bytes, void *user);
 typedef void (*pdcs_free_fn)(void *ptr, void *user);

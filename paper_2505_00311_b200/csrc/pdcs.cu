@@ -18,6 +18,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -57,6 +58,41 @@ struct StatusErr {
 std::atomic<pdcs_alloc_fn> g_alloc{nullptr};
 std::atomic<pdcs_free_fn> g_free{nullptr};
 std::atomic<void*> g_alloc_user{nullptr};
+// Default: a library-owned stream-ordered pool per device that keeps freed
+// memory (release threshold = max), used synchronously: an allocation is
+// complete when dev_alloc returns, and dev_free waits for the device as
+// cudaFree does.  Multi-GB cudaMalloc / cudaFree calls had cost 0.1-2 s each,
+// run to run, in setup and destroy (the driver maps and unmaps the pages);
+// the pool maps a context's peak once per process.  PDCS_POOL=0: cudaMalloc.
+struct DevPool {
+  cudaMemPool_t pool = nullptr;
+  cudaStream_t st = nullptr;
+};
+std::mutex g_pool_mu;
+DevPool g_pool[64];
+DevPool* dev_pool() {
+  static const bool off = std::getenv("PDCS_POOL") && std::atoi(std::getenv("PDCS_POOL")) == 0;
+  if (off) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  DevPool& P = g_pool[dev];
+  if (!P.pool) {
+    cudaMemPoolProps pr{};
+    pr.allocType = cudaMemAllocationTypePinned;
+    pr.location.type = cudaMemLocationTypeDevice;
+    pr.location.id = dev;
+    if (cudaMemPoolCreate(&P.pool, &pr) != cudaSuccess) { P.pool = nullptr; return nullptr; }
+    uint64_t keep = ~(uint64_t)0;
+    cudaMemPoolSetAttribute(P.pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (cudaStreamCreateWithFlags(&P.st, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaMemPoolDestroy(P.pool);
+      P.pool = nullptr;
+      return nullptr;
+    }
+  }
+  return &P;
+}
 void* dev_alloc(size_t bytes) {
   if (pdcs_alloc_fn f = g_alloc.load()) {
     void* p = f(bytes, g_alloc_user.load());
@@ -64,12 +100,23 @@ void* dev_alloc(size_t bytes) {
     return p;
   }
   void* p = nullptr;
+  if (DevPool* P = dev_pool()) {
+    CK(cudaMallocFromPoolAsync(&p, bytes, P->pool, P->st));
+    CK(cudaStreamSynchronize(P->st));
+    return p;
+  }
   CK(cudaMalloc(&p, bytes));
   return p;
 }
 void dev_free(void* p) {
-  if (pdcs_free_fn f = g_free.load()) f(p, g_alloc_user.load());
-  else cudaFree(p);
+  if (pdcs_free_fn f = g_free.load()) { f(p, g_alloc_user.load()); return; }
+  if (DevPool* P = dev_pool()) {
+    cudaDeviceSynchronize();                     // as cudaFree: no kernel may still use p
+    cudaFreeAsync(p, P->st);
+    cudaStreamSynchronize(P->st);
+    return;
+  }
+  cudaFree(p);
 }
 
 template <class T>
@@ -100,6 +147,19 @@ void take(DBuf<T>& to, DBuf<T>& from) {
   to.free_();
   std::swap(to.p, from.p);
   std::swap(to.n, from.n);
+}
+
+// Bank balancing of nb warp blocks (tiled.cuh k_tile_balance_w, one warp each).
+void launch_tile_balance(const TDefer* dseg, const std::vector<TDefer>&, const int2* dblk, int64_t nb, int elem,
+                         const int32_t* rowptr, const uint16_t* pcol, const int32_t* pperm, uint16_t* bcol,
+                         int32_t* bperm, uint16_t* ncol, int32_t* nperm, cudaStream_t st) {
+  if (nb <= 0) return;
+  int dev = 0, sms = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t g = std::max<int64_t>(1, std::min<int64_t>((nb + kBalWarps - 1) / kBalWarps, (int64_t)sms * 16));
+  k_tile_balance_w<<<(unsigned)g, 32 * kBalWarps, 0, st>>>(dseg, dblk, nb, elem, rowptr, pcol, pperm, bcol, bperm,
+                                                          ncol, nperm);
 }
 
 // staged share of the entries above which the tiled copy is built
@@ -266,7 +326,7 @@ void slice_segments(TiledHost& H, int32_t s0, int32_t s1, int32_t nr) {
 // The deferred build's counterpart of slice_segments: the final (sliced)
 // offsets, warp-block bases and the device work list of the staged segments
 // among [s0, s1), with the same sizes and alignment as slice_segments; no data
-// moves (k_tile_balance / k_tile_slice do that on the device).
+// moves (k_tile_balance_w / k_tile_slice do that on the device).
 void slice_plan(TiledHost& H, int32_t s0, int32_t s1, int32_t nr) {
   bool any = false;
   for (int32_t si = s0; si < s1; ++si) any |= H.seg[si].tile >= 0;
@@ -696,7 +756,7 @@ void build_tiled(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n
 
 // ---------------------------------------------------------------- device structure build
 // The tiled format of a DEVICE CSR (tiled.cuh: k_tile_hist / k_tile_rowcnt /
-// k_tile_fill, then k_tile_balance / k_tile_slice): the entries never pass
+// k_tile_fill, then k_tile_balance_w / k_tile_slice): the entries never pass
 // through the host.  The host sees the (chunk, tile) counts and the per-row
 // segment counts only, and runs build_tiled_range's decisions on them (staged
 // tiles, segment order, rows longest first, lanes per row, quad padding, the
@@ -743,7 +803,6 @@ void build_tiled_device(const int32_t* dptr, const int32_t* dcol, const int64_t*
                         int elem, double min_frac, TiledHost& H, TiledDevArrays& A, cudaStream_t st, int sms) {
   const auto t_start = std::chrono::steady_clock::now();
   SetupTrace tr;
-  if (const char* e = std::getenv("PDCS_STACK_LIMIT")) CK(cudaDeviceSetLimit(cudaLimitStackSize, (size_t)std::atol(e)));
   H = TiledHost();
   H.T = tiled_tile_bytes() / (8 * elem);
   H.elem = elem;
@@ -1034,15 +1093,19 @@ void build_tiled_device(const int32_t* dptr, const int32_t* dcol, const int64_t*
     DBuf<int32_t> bperm, nperm;
     bcol.alloc(npre1); ncol.alloc(npre1); bperm.alloc(npre1); nperm.alloc(npre1);
     const int tb = 128;
-    k_tile_balance<<<(int)((nb + tb - 1) / tb), tb, 0, st>>>(dseg.p, dblk.p, nb, elem, A.rowptr.p, pcol.p, pperm.p,
-                                                             bcol.p, bperm.p, ncol.p, nperm.p);
+    launch_tile_balance(dseg.p, H.dseg, dblk.p, nb, elem, A.rowptr.p, pcol.p, pperm.p, bcol.p, bperm.p, ncol.p, nperm.p,
+                        st);
     tr.mark("    devbuild: balance", st);
     k_tile_slice<<<(int)((nb + tb - 1) / tb), tb, 0, st>>>(dseg.p, dblk.p, nb, A.rowptr.p, A.blkb.p, ncol.p,
                                                            nperm.p, A.col_s.p, A.perm_s.p);
     CK(cudaGetLastError());
     tr.mark("    devbuild: slice", st);
+    bcol.free_(); ncol.free_(); bperm.free_(); nperm.free_();
+    tr.mark("    devbuild: frees (balance scratch)", nullptr, false);
   }
   CK(cudaStreamSynchronize(st));
+  pcol.free_(); pperm.free_(); dfs.free_(); dposof.free_(); dcb.free_(); dstl.free_();
+  tr.mark("    devbuild: frees", nullptr, false);
   H.devbuilt = true;
   H.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
 }
@@ -1923,8 +1986,8 @@ struct pdcs_ctx {
         bcol.alloc(H.tot_pre); ncol.alloc(H.tot_pre); bperm.alloc(H.tot_pre); nperm.alloc(H.tot_pre);
         const int64_t nb = (int64_t)H.dblk.size();
         const int tb = 128;
-        k_tile_balance<<<(int)((nb + tb - 1) / tb), tb, 0, st>>>(dseg.p, dblk.p, nb, elem, D.rowptr.p, pcol.p,
-                                                                 pperm.p, bcol.p, bperm.p, ncol.p, nperm.p);
+        launch_tile_balance(dseg.p, H.dseg, dblk.p, nb, elem, D.rowptr.p, pcol.p, pperm.p, bcol.p, bperm.p, ncol.p,
+                            nperm.p, st);
         k_tile_slice<<<(int)((nb + tb - 1) / tb), tb, 0, st>>>(dseg.p, dblk.p, nb, D.rowptr.p, D.blkb.p, ncol.p,
                                                                nperm.p, D.col_s.p, perm.p);
         CK(cudaGetLastError());
@@ -2233,7 +2296,13 @@ struct pdcs_ctx {
     SpmvPlan P{};
     P.ncls = 0;
     int total = 0;
-    for (int c = 0; c < kMaxClasses; ++c) {
+    // The one-CTA-per-row class goes first, one row per CTA: CTAs are
+    // dispatched in index order, so the long rows start at once and the short
+    // classes fill the SMs behind them (last, with a grid stride over 4 CTAs
+    // per SM, they had made a tail of second rows: Fisher's 1000 supply rows)
+    static const int order[kMaxClasses] = {5, 0, 1, 2, 3, 4};
+    for (int oc = 0; oc < kMaxClasses; ++oc) {
+      const int c = order[oc];
       if (lists[c].empty()) continue;
       SpmvClass& K_ = P.cls[P.ncls++];
       K_.V = Vs[c];
@@ -2248,7 +2317,7 @@ struct pdcs_ctx {
       }
       int64_t rows_per_cta = K_.V == 0 ? 1 : K_.V == 1 ? kThreads : kThreads / K_.V;
       int64_t g = (K_.nrows + rows_per_cta - 1) / rows_per_cta;
-      const int64_t cap = K_.V == 0 ? (int64_t)sms * 4 : (int64_t)sms * 8;
+      const int64_t cap = K_.V == 0 ? (int64_t)sms * 16 : (int64_t)sms * 8;
       K_.ncta = (int32_t)std::max<int64_t>(1, std::min(g, cap));
       total += K_.ncta;
     }
@@ -3360,8 +3429,8 @@ int pdcs_tiled_device_check(const int64_t* row_ptr, const int32_t* col, int64_t 
       upload(dseg, B.dseg, st);
       upload(dblk, B.dblk, st);
       bcol.alloc(B.tot_pre); ncol.alloc(B.tot_pre); bperm.alloc(B.tot_pre); nperm.alloc(B.tot_pre);
-      k_tile_balance<<<(int)((nb + 127) / 128), 128>>>(dseg.p, dblk.p, nb, elem, rp.p, pcol.p, pperm.p, bcol.p,
-                                                       bperm.p, ncol.p, nperm.p);
+      launch_tile_balance(dseg.p, B.dseg, dblk.p, nb, elem, rp.p, pcol.p, pperm.p, bcol.p, bperm.p, ncol.p, nperm.p,
+                          nullptr);
       k_tile_slice<<<(int)((nb + 127) / 128), 128>>>(dseg.p, dblk.p, nb, rp.p, bb.p, ncol.p, nperm.p, cs.p, perm.p);
       CK(cudaGetLastError());
     }

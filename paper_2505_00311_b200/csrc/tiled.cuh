@@ -758,109 +758,170 @@ __global__ void __launch_bounds__(kTThreads, ELEM == 1 ? PDCS_TS_MINB1 : PDCS_TP
 // choices go first and take the free bank group with the most entries left.
 // pcol / pperm: the pre layout (read); bcol / bperm: bucket scratch at the same
 // offsets; ncol / nperm: the balanced quads at the same offsets (written).
-__global__ void k_tile_balance(const TDefer* __restrict__ dseg, const int2* __restrict__ dblk, int64_t nblk, int elem,
-                               const int32_t* __restrict__ rowptr, const uint16_t* __restrict__ pcol,
-                               const int32_t* __restrict__ pperm, uint16_t* __restrict__ bcol,
-                               int32_t* __restrict__ bperm, uint16_t* __restrict__ ncol, int32_t* __restrict__ nperm) {
-  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (it >= nblk) return;
-  const int2 db = dblk[it];
-  const TDefer S = dseg[db.x];
-  const int V = S.V, G = elem == 2 ? 8 : 16, rpw = 32 / V;
-  const int32_t* rp = rowptr + S.rp;
-  const int32_t i0 = db.y * rpw;
-  const int R = min(rpw, S.nr - i0);
-  const uint16_t* cols = pcol + S.src;
-  const int32_t* perm = pperm + S.src;
-  const int64_t bbase = S.src + 4 * (int64_t)rp[i0];    // this block's region (bucket scratch)
-  int32_t bstart[32 * 16 + 1];
-  int32_t bleft[32 * 16];
-  int32_t left[32], slots[32];
-  uint32_t mask[32];
-  int rem[16];
-  for (int z = 0; z <= R * G; ++z) bstart[z] = 0;
-  for (int g = 0; g < 16; ++g) rem[g] = 0;
-  int32_t tmax = 0;
-  for (int a = 0; a < R; ++a) {
-    const int32_t q0 = rp[i0 + a], q1 = rp[i0 + a + 1];
-    tmax = max(tmax, (q1 - q0 + V - 1) / V);
-    slots[a] = 4 * (q1 - q0);
-    left[a] = 0;
-    mask[a] = 0;
-    for (int64_t e = 4 * (int64_t)q0; e < 4 * (int64_t)q1; ++e)
-      if (perm[e] >= 0) {
-        const int g = cols[e] % G;
-        ++bstart[a * G + g + 1];
-        mask[a] |= 1u << g;
-        ++rem[g];
-        ++left[a];
+// Bank balancing, one WARP per warp block (the solver's device builds).  The
+// same greedy as balance_banks (pdcs.cu), decision for decision:
+// lane a < R owns row a's state (group mask, entries left, slots left, quads);
+// the per-(row, group) bucket counts and the block's per-group totals live in
+// shared memory.  Per phase the units (schedule lanes with a quad at this step)
+// are taken in (popcount of the row's groups at the phase start, lane) order,
+// one at a time: the owner's current state is broadcast and every lane computes
+// the same choice (the free group with the most entries left, lowest on ties;
+// a forced conflict when the row has no pad to spare; else a pad).  Each unit's
+// lane then moves its entry: bucket (a, g) is consumed from the back, as on the
+// host.  Pads re-read the first unit's column (0 if that unit was a pad).
+constexpr int kBalWarps = 4;                          // warps per CTA of k_tile_balance_w
+constexpr int kBalRG = 32 * 16;                       // max rows x groups of a warp block
+__global__ void __launch_bounds__(32 * kBalWarps)
+    k_tile_balance_w(const TDefer* __restrict__ dseg, const int2* __restrict__ dblk, int64_t nblk, int elem,
+                     const int32_t* __restrict__ rowptr, const uint16_t* __restrict__ pcol,
+                     const int32_t* __restrict__ pperm, uint16_t* __restrict__ bcol, int32_t* __restrict__ bperm,
+                     uint16_t* __restrict__ ncol, int32_t* __restrict__ nperm) {
+  __shared__ int32_t s_cnt[kBalWarps][kBalRG];        // bucket sizes, then entries left per bucket
+  __shared__ int32_t s_start[kBalWarps][kBalRG + 1];  // bucket starts (exclusive prefix, row-major)
+  __shared__ int32_t s_cur[kBalWarps][kBalRG];        // fill cursors
+  __shared__ int32_t s_rem[kBalWarps][16];            // entries left per group in the block
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  int32_t* cnt = s_cnt[w];
+  int32_t* bst = s_start[w];
+  int32_t* cur = s_cur[w];
+  int32_t* rem = s_rem[w];
+  const int G = elem == 2 ? 8 : 16;
+  const int64_t nwarps = (int64_t)gridDim.x * kBalWarps;
+  for (int64_t it = (int64_t)blockIdx.x * kBalWarps + w; it < nblk; it += nwarps) {
+    const int2 db = dblk[it];
+    const TDefer S = dseg[db.x];
+    const int V = S.V, rpw = 32 / V;
+    const int32_t* rp = rowptr + S.rp;
+    const int32_t i0 = db.y * rpw;
+    const int R = min(rpw, S.nr - i0);
+    const uint16_t* cols = pcol + S.src;
+    const int32_t* perm = pperm + S.src;
+    const int64_t bbase = S.src + 4 * (int64_t)rp[i0];
+    const int RG = R * G;
+    // ---- row state (owner lanes)
+    int32_t q0 = 0, nq = 0;
+    if (lane < R) { q0 = rp[i0 + lane]; nq = rp[i0 + lane + 1] - q0; }
+    const int32_t tmax = (int32_t)__reduce_max_sync(FULL, (unsigned)((nq + V - 1) / V));
+    for (int z = lane; z < RG; z += 32) { cnt[z] = 0; cur[z] = 0; }
+    if (lane < 16) rem[lane] = 0;
+    __syncwarp();
+    // ---- bucket sizes (integer counts: order-free)
+    for (int a = 0; a < R; ++a) {
+      const int32_t qa = __shfl_sync(FULL, q0, a), na = __shfl_sync(FULL, nq, a);
+      for (int64_t e = 4 * (int64_t)qa + lane; e < 4 * (int64_t)(qa + na); e += 32)
+        if (perm[e] >= 0) {
+          const int g = cols[e] % G;
+          atomicAdd(cnt + a * G + g, 1);
+          atomicAdd(rem + g, 1);
+        }
+    }
+    __syncwarp();
+    // ---- bucket starts: exclusive prefix over (row, group), row-major
+    {
+      const int per = (RG + 31) / 32;
+      const int z0 = min(RG, lane * per), z1 = min(RG, z0 + per);
+      int32_t loc = 0;
+      for (int z = z0; z < z1; ++z) loc += cnt[z];
+      int32_t inc = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += v;
       }
-  }
-  for (int z = 1; z <= R * G; ++z) bstart[z] += bstart[z - 1];
-  for (int z = 0; z < R * G; ++z) bleft[z] = bstart[z];
-  for (int a = 0; a < R; ++a)
-    for (int64_t e = 4 * (int64_t)rp[i0 + a]; e < 4 * (int64_t)rp[i0 + a + 1]; ++e)
-      if (perm[e] >= 0) {
-        const int32_t z = bleft[a * G + cols[e] % G]++;
-        bcol[bbase + z] = cols[e];
-        bperm[bbase + z] = perm[e];
+      int32_t run = inc - loc;
+      for (int z = z0; z < z1; ++z) { bst[z] = run; run += cnt[z]; }
+      if (lane == 31) bst[RG] = inc;
+    }
+    __syncwarp();
+    // ---- buckets filled in entry order (stable within a bucket)
+    for (int a = 0; a < R; ++a) {
+      const int32_t qa = __shfl_sync(FULL, q0, a), na = __shfl_sync(FULL, nq, a);
+      for (int64_t e0 = 4 * (int64_t)qa; e0 < 4 * (int64_t)(qa + na); e0 += 32) {
+        const int64_t e = e0 + lane;
+        const bool ok = e < 4 * (int64_t)(qa + na) && perm[e] >= 0;
+        const int g = ok ? cols[e] % G : -1 - lane;
+        const unsigned same = __match_any_sync(FULL, g);
+        if (ok) {
+          const int bi = a * G + g;
+          const int32_t z = bst[bi] + cur[bi] + __popc(same & ((1u << lane) - 1u));
+          bcol[bbase + z] = cols[e];
+          bperm[bbase + z] = perm[e];
+        }
+        __syncwarp();
+        if (ok && lane == 31 - __clz(same)) cur[a * G + g] += __popc(same);
+        __syncwarp();
       }
-  int unit_a[16];
-  int64_t unit_slot[16];
-  for (int32_t t = 0; t < tmax; ++t)
-    for (int k = 0; k < 4; ++k)
-      for (int ph = 0; ph < 32 / G; ++ph) {
-        int nu = 0;
-        for (int lane = ph * G; lane < ph * G + G; ++lane) {
+    }
+    // ---- owner state: group mask, entries left, slots left
+    uint32_t mask = 0;
+    int32_t left = 0, slots = 4 * nq;
+    if (lane < R)
+      for (int g = 0; g < G; ++g) {
+        const int32_t c = cnt[lane * G + g];
+        if (c) mask |= 1u << g;
+        left += c;
+      }
+    __syncwarp();
+    // ---- the greedy, phase by phase
+    for (int32_t t = 0; t < tmax; ++t)
+      for (int k = 0; k < 4; ++k)
+        for (int ph = 0; ph < 32 / G; ++ph) {
           const int a = lane / V, l = lane % V;
-          if (a >= R) continue;
-          const int32_t q = l + t * V;
-          if (q >= rp[i0 + a + 1] - rp[i0 + a]) continue;
-          unit_a[nu] = a;
-          unit_slot[nu] = 4 * (int64_t)(rp[i0 + a] + q) + k;
-          ++nu;
-        }
-        if (nu > 1) {                                     // fewest choices first (counting sort)
-          int pc[16], cnt[18], sa[16];
-          int64_t ss[16];
-          for (int z = 0; z < 18; ++z) cnt[z] = 0;
-          for (int x = 0; x < nu; ++x) { pc[x] = __popc(mask[unit_a[x]]); ++cnt[pc[x] + 1]; }
-          for (int z = 1; z < 18; ++z) cnt[z] += cnt[z - 1];
-          for (int x = 0; x < nu; ++x) { const int z = cnt[pc[x]]++; sa[z] = unit_a[x]; ss[z] = unit_slot[x]; }
-          for (int x = 0; x < nu; ++x) { unit_a[x] = sa[x]; unit_slot[x] = ss[x]; }
-        }
-        uint32_t used = 0;
-        int any_col = -1;
-        for (int x = 0; x < nu; ++x) {
-          const int a = unit_a[x];
-          const int64_t slot = unit_slot[x];
-          const uint32_t avail = mask[a] & ~used;
-          int g = -1;
-          if (avail || (left[a] > 0 && slots[a] == left[a])) {
-            uint32_t from = avail ? avail : mask[a];
-            for (; from; from &= from - 1) {
-              const int h = __ffs(from) - 1;
-              if (g < 0 || rem[h] > rem[g]) g = h;
+          const bool inph = lane >= ph * G && lane < ph * G + G;
+          const int32_t na = __shfl_sync(FULL, nq, a < 32 ? a : 0);
+          const int32_t qa = __shfl_sync(FULL, q0, a < 32 ? a : 0);
+          const uint32_t m0 = __shfl_sync(FULL, mask, a < 32 ? a : 0);
+          const bool unit = inph && a < R && l + t * V < na;
+          unsigned key = unit ? ((unsigned)__popc(m0) << 5) | (unsigned)lane : 0xffffffffu;
+          uint32_t used = 0;
+          int32_t z_src = -1;                          // this lane's entry (bucket index), -1: pad
+          int first = -1, first_pad = 0;               // first unit processed; whether it was a pad
+          for (;;) {
+            const unsigned kmin = __reduce_min_sync(FULL, key);
+            if (kmin == 0xffffffffu) break;
+            const int wl = (int)(kmin & 31u);
+            const int aw = wl / V;
+            const uint32_t m = __shfl_sync(FULL, mask, aw);
+            const int32_t lf = __shfl_sync(FULL, left, aw);
+            const int32_t sl = __shfl_sync(FULL, slots, aw);
+            const uint32_t avail = m & ~used;
+            const uint32_t from = avail ? avail : ((lf > 0 && sl == lf) ? m : 0u);
+            unsigned cand = 0;
+            if (lane < G && ((from >> lane) & 1u)) cand = ((unsigned)rem[lane] << 5) | (unsigned)(31 - lane) | 0x80000000u;
+            const unsigned best = __reduce_max_sync(FULL, cand);
+            const int g = best ? 31 - (int)(best & 31u) : -1;
+            if (first < 0) { first = wl; first_pad = g < 0; }
+            if (g >= 0) {
+              const int bi = aw * G + g;
+              int32_t nleft = 0;
+              if (lane == aw) {
+                nleft = --cnt[bi];
+                if (nleft == 0) mask &= ~(1u << g);
+                --left;
+              }
+              nleft = __shfl_sync(FULL, nleft, aw);
+              if (lane == wl) z_src = bst[bi] + nleft;
+              if (lane == 0) --rem[g];
+              used |= 1u << g;
             }
+            if (lane == aw) --slots;
+            if (lane == wl) key = 0xffffffffu;
+            __syncwarp();
           }
-          if (g >= 0) {
-            const int bi = a * G + g;
-            const int32_t z = --bleft[bi];
-            ncol[S.src + slot] = bcol[bbase + z];
-            nperm[S.src + slot] = bperm[bbase + z];
-            if (bleft[bi] == bstart[bi]) mask[a] &= ~(1u << g);
-            --rem[g];
-            --left[a];
-            used |= 1u << g;
-            if (any_col < 0) any_col = ncol[S.src + slot];
-          } else {                                        // pad: re-read an address
-            ncol[S.src + slot] = (uint16_t)(any_col >= 0 ? any_col : 0);
-            nperm[S.src + slot] = -1;
-            if (any_col < 0) any_col = 0;
+          // move the entries (loads issued for every unit together)
+          uint16_t c = 0;
+          int32_t pv = -1;
+          if (unit && z_src >= 0) { c = bcol[bbase + z_src]; pv = bperm[bbase + z_src]; }
+          const uint16_t fc = (uint16_t)__shfl_sync(FULL, (int)c, first >= 0 ? first : 0);
+          if (unit) {
+            const int64_t slot = 4 * (int64_t)(qa + l + t * V) + k;
+            if (z_src >= 0) { ncol[S.src + slot] = c; nperm[S.src + slot] = pv; }
+            else { ncol[S.src + slot] = first_pad ? (uint16_t)0 : fc; nperm[S.src + slot] = -1; }
           }
-          --slots[a];
         }
-      }
+    __syncwarp();
+  }
 }
 
 // Sliced re-layout of one warp block (slice_segments / quad_slot): quad j of
@@ -899,7 +960,7 @@ __global__ void k_tile_slice(const TDefer* __restrict__ dseg, const int2* __rest
 // entries per segment, the host orders the rows and lays out the segments
 // (only O(segments x rows) work); k_tile_fill writes the column ids and CSR
 // positions of every entry at their slots of the unbalanced row-major quads
-// (staged segments) or of col_d (direct).  k_tile_balance / k_tile_slice then
+// (staged segments) or of col_d (direct).  k_tile_balance_w / k_tile_slice then
 // finish as in the deferred build.  Same layout, bit for bit, as build_tiled
 // (tests/test_tiled_layout.py, pdcs_tiled_devbuild_check).
 struct TBChunk {

@@ -21,6 +21,13 @@ for rep in range(int(os.environ.get('REPS', '2'))):
     sc = P.pdcs_get_scalars(ctx)
     print(json.dumps({"config": cfg, "rep": rep, "wall_s": t1 - t0,
                       **{k: sc[k] for k in sc if k.startswith(("setup", "tiled", "tune"))}}), flush=True)
+    ti = []
+    for _ in range(2):                         # first: builds the CUDA graph
+        t3 = time.perf_counter()
+        P.pdcs_iterate(ctx, 40)
+        torch.cuda.synchronize()
+        ti.append(time.perf_counter() - t3)
+    print(json.dumps({"iterate40_first_s": ti[0], "iterate40_second_s": ti[1]}), flush=True)
     t2 = time.perf_counter()
     P.pdcs_destroy(ctx)
     torch.cuda.synchronize()

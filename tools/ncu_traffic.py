@@ -29,9 +29,9 @@ sys.path.insert(0, ROOT)
 
 # the format the bench's autotune keeps per config
 TILED = {"lasso": "1", "fisher": "0", "mpo": "0", "mixed": "0"}
-SWEEPS = {"spmv_K_dual": ("k_tiled_sliced<2>", "k_tiled_tma<2>", "k_tiled_partial<2>",
+SWEEPS = {"spmv_K_dual": ("k_tiled_sliced<2>", "k_tiled_sliced<2,", "k_tiled_sliced<(int)2,", "k_tiled_tma<2>", "k_tiled_partial<2>",
                           "k_tiled_combine<EpiDualTrial", "spmv_kernel<EpiDualTrial>"),
-          "spmv_KT_halpern": ("k_tiled_sliced<1>", "k_tiled_tma<1>", "k_tiled_partial<1>",
+          "spmv_KT_halpern": ("k_tiled_sliced<1>", "k_tiled_sliced<1,", "k_tiled_sliced<(int)1,", "k_tiled_tma<1>", "k_tiled_partial<1>",
                               "k_tiled_combine<EpiHalpernX", "spmv_kernel<EpiHalpernX>"),
           "halpern_y": ("k_halpern_y",), "primal_elem": ("k_primal_elem",)}
 

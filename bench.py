@@ -133,8 +133,8 @@ def spmv_alg_bytes(prog):
     matrix (8 B value + 4 B column id per nnz) + row pointers (4 B per row) + the
     gathered vector once + the row-indexed epilogue vectors."""
     nnz, m, n = prog.nnz, local_rows(prog), prog.n
-    # K sweep: (x^_j, x_j) pairs gathered once (16 n); y, h~ in, K x^, y^ out (32 m); kind byte (m)
-    k_dual = 12 * nnz + 4 * (m + 1) + 16 * n + 32 * m + m
+    # K sweep: x^ gathered once (8 n); y, h~, carried K x in, K x^, y^ out (40 m); kind byte (m)
+    k_dual = 12 * nnz + 4 * (m + 1) + 8 * n + 40 * m + m
     # K^T sweep: y+ gathered once (8 m); x^, x, x0, xsum in, x, K^T y, xsum out (56 n)
     kt_halpern = 12 * nnz + 4 * (n + 1) + 8 * m + 56 * n
     return {"spmv_K_dual": k_dual, "spmv_KT_halpern": kt_halpern}
@@ -143,22 +143,23 @@ def spmv_alg_bytes(prog):
 def elem_alg_bytes(prog):
     """Algorithmic bytes of the two fused elementwise update kernels per launch.
     k_primal_elem over the box / zero / R+ coordinates: kind byte, x, c~, K~^T y
-    in; x^ and the (x^, x) pair out (49 B), plus 8 B per bound the kernel reads:
-    a box column [0, inf) is the kind EK_LO0 and reads none (its bound is in the
-    kind byte), every other finite l~ / u~ is one 8-B read.
-    k_halpern_y over all rows: y^, y, y0, sum(eta y) in; y+, sum out (48 B)."""
+    in; x^ out (33 B), plus 8 B per bound the kernel reads: a box column
+    [0, inf) is the kind EK_LO0 and reads none (its bound is in the kind byte),
+    every other finite l~ / u~ is one 8-B read.
+    k_halpern_y over all rows: y^, y, y0, sum(eta y) in, y+, sum out; the
+    carried K x^, K x, K x0 in, K x+ out (80 B)."""
     from instances import ZERO, NONNEG
     pk, pdim = np.asarray(prog.pk), np.asarray(prog.pdim)
     n_elem = prog.n1 + int(pdim[(pk == ZERO) | (pk == NONNEG)].sum())
     l, u = np.asarray(prog.l), np.asarray(prog.u)
     lo0 = (l == 0.0) & ~np.isfinite(u)
     bounds = 8 * int((np.isfinite(l) & ~lo0).sum() + np.isfinite(u).sum())
-    return {"primal_elem": 49 * n_elem + bounds, "halpern_y": 48 * local_rows(prog)}
+    return {"primal_elem": 33 * n_elem + bounds, "halpern_y": 80 * local_rows(prog)}
 
 
 # kernels that run only inside the Eq. 9 check (every check_interval iterations);
 # the projection block kernels of the average candidate are not separable by name
-CHECK_KERNELS = ("avg_elem", "pair_stage", "tiled_check_partial", "check_combine", "spmv_store", "kkt_rows",
+CHECK_KERNELS = ("avg_elem", "tiled_check_partial", "check_combine", "spmv_store", "kkt_rows",
                  "kkt_cols", "kkt_reduce", "kkt_decide", "restart_copy")
 
 

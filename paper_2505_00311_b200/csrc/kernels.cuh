@@ -63,11 +63,10 @@ struct SrcAdapt {       // adapts .D_ to the .D expected by soc_team
 // 2: plain store  (out <- val)
 // 3: KKT residual (acc += max |src - val|, max |val|) into kacc[base + 0/2] or [5]
 struct DstTrialPrimal {
-  double *xh; double2* xx; const double* x; int64_t off; Acc<kAcc>* acc;
+  double *xh; const double* x; int64_t off; Acc<kAcc>* acc;
   __device__ void put(int64_t i, double val) {
     const double xo = x[off + i];
     xh[off + i] = val;
-    xx[off + i] = make_double2(val, xo);
     const double d = val - xo;
     acc->v[0] += d * d;
   }
@@ -141,7 +140,6 @@ struct BlockArgs {
   // vectors
   const double *x, *c, *kty, *D;  // primal trial source
   double* xh;
-  double2* xx;                    // interleaved (x^_j, x_j) for the K sweep
   const double* y;                // dual trial
   double* yh;
   const double* kxd;              // K x^ - K x of block rows
@@ -159,7 +157,7 @@ __device__ __forceinline__ void run_block(Team& tm, const BlockArgs& A, const Ct
   switch (OP) {
     case BOP_TRIAL_PRIMAL: {
       SrcPrimalTrial s{A.x, A.c, A.kty, A.D, ctl->tau, b.off};
-      DstTrialPrimal d{A.xh, A.xx, A.x, b.off, &acc};
+      DstTrialPrimal d{A.xh, A.x, b.off, &acc};
       project_block<HAS_EXP>(tm, b, false, false, s, d);
       break;
     }

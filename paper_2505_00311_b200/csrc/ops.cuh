@@ -17,7 +17,7 @@ __global__ void __launch_bounds__(kThreads) k_primal_elem(int64_t n, const uint8
                                                           const double* __restrict__ kty,
                                                           const double* __restrict__ lt,
                                                           const double* __restrict__ ut,
-                                                          double* __restrict__ xh, double2* __restrict__ xx,
+                                                          double* __restrict__ xh,
                                                           const Ctl* ctl, double* part, int64_t slot0) {
   if (ctl->status != ST_RUNNING) return;
   const double tau = ctl->tau;
@@ -29,7 +29,6 @@ __global__ void __launch_bounds__(kThreads) k_primal_elem(int64_t n, const uint8
     const double v = xj - tau * (c[j] - kty[j]);
     const double p = box_proj(k, v, lt, ut, j);
     xh[j] = p;
-    xx[j] = make_double2(p, xj);
     const double d = p - xj;
     acc.v[0] += d * d;
   }
@@ -166,7 +165,11 @@ __device__ __forceinline__ void decide_serial(Ctl& C, const double red[3], int p
 // decision, saving a graph node per iteration where node latency dominates
 // (PAPER.md:918).  Same formula, same bits.
 constexpr int64_t kFuseYMax = 2048;
-struct FusedY { int64_t m; const double* yh; const double* y0; double* y; double* ysum; };
+struct FusedY {
+  int64_t m;
+  const double* yh; const double* y0; double* y; double* ysum;
+  const double* kxh; const double* kx0; double* kxc;     // K x carried with the same step
+};
 
 // y-side reflected Halpern step and average sum of one row (Alg. 1 line 5-6,
 // PAPER.md:606): y+ = a((1+beta) y^ - beta y) + c y0, ysum += eta y+.  Explicit
@@ -178,6 +181,14 @@ __device__ __forceinline__ double halpern_y_row(double a, double b, double c, do
   const double yn = __fma_rn(a, t, __dmul_rn(c, y0));
   ysum = __fma_rn(eta, yn, ysum);
   return yn;
+}
+
+// The same step on the carried product K x (linearity of Alg. 1 line 6):
+// K x+ = a((1+beta) K x^ - beta K x) + c K x0, explicit roundings (one
+// function for k_decide's fused update and k_halpern_y).
+__device__ __forceinline__ double halpern_kx_row(double a, double b, double c, double kxh, double kx, double kx0) {
+  const double t = __fma_rn(1.0 + b, kxh, __dmul_rn(-b, kx));
+  return __fma_rn(a, t, __dmul_rn(c, kx0));
 }
 
 __global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restrict__ part, int64_t nslots,
@@ -206,6 +217,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restr
     const double a = sC.ha, b = sC.hbeta, c = sC.hb, eta = sC.eta_used;
     for (int64_t i = threadIdx.x; i < fy.m; i += blockDim.x) {
       fy.y[i] = halpern_y_row(a, b, c, eta, fy.yh[i], fy.y[i], fy.y0[i], fy.ysum[i]);
+      fy.kxc[i] = halpern_kx_row(a, b, c, fy.kxh[i], fy.kxc[i], fy.kx0[i]);
     }
   }
   for (int i = threadIdx.x; i < kCtlWords; i += blockDim.x)
@@ -213,21 +225,25 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const double* __restr
 }
 
 // ---------------------------------------------------------------- SpMV epilogues
-// One sweep over K computes K x^ and K x (both fresh, as Eq. 5 writes them):
+// One sweep over K computes K x^ (fresh); K x of the current iterate is carried
+// by linearity (K x+ = a((1+beta) K x^ - beta K x) + c K x0 on
+// an accepted step, the candidate's fresh product at a restart):
 // Kxh = K x^; v = y + sigma (h~ - 2 K x^ + K x); y^ = P(v) for free / nonneg
 // rows, v stored for block rows (projected by the block kernels).
 // Accumulates ||y^ - y||^2 and <y^ - y, K x^ - K x> (line search).
 struct EpiDualTrial {
   static constexpr int NA = kAcc;
-  static constexpr int NX = 3;   // gathers the interleaved (x^_j, x_j) pairs
+  static constexpr int NX = 1;   // gathers x^ only; K x is carried (kxc, k_halpern_y)
   const double *y, *h;
   const uint8_t* rk;
   double *kxh, *kxd, *yh;
+  const double* kxc;             // K x of the current iterate
   double sigma;
   int run;
   __device__ void init(const Ctl* c) { sigma = c->sigma; run = c->status == ST_RUNNING; }
   __device__ bool active() const { return run; }
-  __device__ void row(int64_t i, double kxhat, double kx, Acc<NA>& a) {
+  __device__ void row(int64_t i, double kxhat, double, Acc<NA>& a) {
+    const double kx = kxc[i];
     kxh[i] = kxhat;
     const double yi = y[i];
     const double v = yi + sigma * (h[i] - 2.0 * kxhat + kx);
@@ -313,18 +329,14 @@ struct EpiStore2 {
   __device__ void row(int64_t i, double dot, double, Acc<NA>&) { out[i] = dot; }
 };
 
-// (a_j, 0) pairs for a single-vector product through the pair-gather tiled K.
-__global__ void __launch_bounds__(kThreads) k_pair_stage(int64_t n, const double* __restrict__ a,
-                                                         double2* __restrict__ xx) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    xx[j] = make_double2(a[j], 0.0);
-}
-
 // y-side ReflectedHalpern + average: y+, ysum.
 __global__ void __launch_bounds__(kThreads) k_halpern_y(int64_t m, const double* __restrict__ yh,
                                                         const double* __restrict__ y0,
                                                         double* __restrict__ y,
-                                                        double* __restrict__ ysum, const Ctl* ctl) {
+                                                        double* __restrict__ ysum,
+                                                        const double* __restrict__ kxh,
+                                                        const double* __restrict__ kx0,
+                                                        double* __restrict__ kxc, const Ctl* ctl) {
   if (ctl->status != ST_RUNNING || !ctl->accepted) return;
   const double a = ctl->ha, b = ctl->hbeta, c = ctl->hb, eta = ctl->eta_used;
   auto upd = [&](double yhi, double yi, double y0i, double& ysi) {
@@ -360,6 +372,18 @@ __global__ void __launch_bounds__(kThreads) k_halpern_y(int64_t m, const double*
   if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t i = m - 1;
     y[i] = upd(yh[i], y[i], y0[i], ysum[i]);
+  }
+  // the carried K x (same coefficients)
+  const double2* kh2 = reinterpret_cast<const double2*>(kxh);
+  const double2* k02 = reinterpret_cast<const double2*>(kx0);
+  double2* kc2 = reinterpret_cast<double2*>(kxc);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += T) {
+    const double2 h = kh2[i], v = kc2[i], o = k02[i];
+    kc2[i] = make_double2(halpern_kx_row(a, b, c, h.x, v.x, o.x), halpern_kx_row(a, b, c, h.y, v.y, o.y));
+  }
+  if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t i = m - 1;
+    kxc[i] = halpern_kx_row(a, b, c, kxh[i], kxc[i], kx0[i]);
   }
 }
 
@@ -557,8 +581,8 @@ __global__ void k_kkt_decide(int ncand, int mode, double hnorm, double cnorm, Ct
 // Restart / best / candidate copies selected by the finalize decision.
 struct RestartArgs {
   int64_t n, m;
-  const double *cx[2], *cy[2], *ckty[2];
-  double *x, *x0, *y, *y0, *kty, *xsum, *ysum;
+  const double *cx[2], *cy[2], *ckty[2], *ckx[2];
+  double *x, *x0, *y, *y0, *kty, *xsum, *ysum, *kxc, *kx0;
   double *bx, *by, *candx, *candy;
 };
 __global__ void __launch_bounds__(kThreads) k_restart_copy(RestartArgs A, const Ctl* ctl) {
@@ -580,6 +604,8 @@ __global__ void __launch_bounds__(kThreads) k_restart_copy(RestartArgs A, const 
       if (bf) A.by[j] = yv;
       if (rs) {
         A.y[j] = yv; A.y0[j] = yv; A.ysum[j] = 0.0;
+        const double kv = A.ckx[u][j];          // the candidate's fresh product K x
+        A.kxc[j] = kv; A.kx0[j] = kv;
       }
     }
   }

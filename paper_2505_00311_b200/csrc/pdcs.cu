@@ -100,12 +100,17 @@ void* dev_alloc(size_t bytes) {
     return p;
   }
   void* p = nullptr;
+  // PDCS_DEBUG_POISON=1: every new buffer starts as 0xff bytes (NaN doubles, -1
+  // ids), so a read of memory no kernel wrote shows up (tests, diagnostics)
+  static const bool poison = std::getenv("PDCS_DEBUG_POISON") && std::atoi(std::getenv("PDCS_DEBUG_POISON"));
   if (DevPool* P = dev_pool()) {
     CK(cudaMallocFromPoolAsync(&p, bytes, P->pool, P->st));
+    if (poison) CK(cudaMemsetAsync(p, 0xff, bytes, P->st));
     CK(cudaStreamSynchronize(P->st));
     return p;
   }
   CK(cudaMalloc(&p, bytes));
+  if (poison) CK(cudaMemset(p, 0xff, bytes));
   return p;
 }
 void dev_free(void* p) {
@@ -1283,7 +1288,7 @@ struct pdcs_ctx {
   DBuf<double> x, xh, x0, xsum, kty, ktyh, xa, ktya, bx, candx, lam0, lam1, onesn;
   DBuf<double> y, yh, y0, ysum, kxh, kxd, ya, kxa, by, candy, res0, res1, onesm;
   DBuf<double> tmpn, tmpm, scal;
-  DBuf<double2> xx;                            // interleaved (x^_j, x_j)
+  DBuf<double> kxc, kx0;                       // K x of the current iterate and of the anchor (carried)
   // row sharding (comm.h): NCCL or in-process loopback communicator over the ranks
   bool dist = false;
   std::unique_ptr<Comm> comm;
@@ -1432,6 +1437,12 @@ struct pdcs_ctx {
     if (!timing) {
       f();
       CK(cudaGetLastError());
+      static const bool dbg = std::getenv("PDCS_DEBUG_SYNC") && std::atoi(std::getenv("PDCS_DEBUG_SYNC"));
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (dbg && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+        const cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) fail(PDCS_ERR_CUDA, std::string("kernel '") + name + "': " + cudaGetErrorString(e));
+      }
       return;
     }
     cudaEvent_t a = ev(), b = ev();
@@ -1498,8 +1509,7 @@ struct pdcs_ctx {
   }
 
   // Product sweeps of the Eq. 9 check: the tiled copies when the autotune kept
-  // them (K x through the pair-gather format with (x_j, 0) staged into xx,
-  // which the next trial's primal kernel rewrites anyway), else CSR.
+  // them, else CSR.
   void spmv_check_KT(const double* yin, double* out) {
     if (!tKT.on) { spmv_store(KT, yin, out); return; }
     tiled_partial("tiled_check_partial", tKT, 1, yin, 0);
@@ -1510,11 +1520,10 @@ struct pdcs_ctx {
   }
   void spmv_check_K(const double* xin, double* out) {
     if (!tK.on) { spmv_store(K, xin, out); return; }
-    launch("pair_stage", [&] { k_pair_stage<<<g_pe, kThreads, 0, st>>>(n, xin, xx.p); });
-    tiled_partial("tiled_check_partial", tK, 2, reinterpret_cast<const double*>(xx.p), 0);
-    EpiStore2 e{out};
+    tiled_partial("tiled_check_partial", tK, 1, xin, 0);
+    EpiStore e{out};
     launch("check_combine", [&] {
-      k_tiled_combine<EpiStore2, 2><<<tK.g_combine, kThreads, 0, st>>>(tK.M, tK.scratch.p, e, ctl, nullptr, 0);
+      k_tiled_combine<EpiStore, 1><<<tK.g_combine, kThreads, 0, st>>>(tK.M, tK.scratch.p, e, ctl, nullptr, 0);
     });
   }
 
@@ -1571,7 +1580,7 @@ struct pdcs_ctx {
     BlockArgs A{};
     A.blocks = primal ? pblocks.p : rblocks.p;
     A.op = op;
-    A.x = x.p; A.c = ct.p; A.kty = kty.p; A.xh = xh.p; A.xx = xx.p;
+    A.x = x.p; A.c = ct.p; A.kty = kty.p; A.xh = xh.p;
     A.D = primal ? q.p : r.p;
     A.y = y.p; A.yh = yh.p; A.kxd = kxd.p;
     return A;
@@ -1649,23 +1658,23 @@ struct pdcs_ctx {
   void trial() {
     const std::function<void(cudaStream_t)> pe = [&](cudaStream_t s_) {
       launch("primal_elem", [&] {
-        k_primal_elem<<<g_pe, kThreads, 0, s_>>>(n, ek.p, x.p, ct.p, kty.p, lt.p, ut.p, xh.p, xx.p, ctl,
+        k_primal_elem<<<g_pe, kThreads, 0, s_>>>(n, ek.p, x.p, ct.p, kty.p, lt.p, ut.p, xh.p, ctl,
                                                  tpart.p, slot_pe);
       });
     };
     run_blocks(true, bargs(true, BOP_TRIAL_PRIMAL), false, 0, &pe);
-    EpiDualTrial e{y.p, ht.p, rk.p, kxh.p, kxd.p, yh.p, 0.0, 0};
+    EpiDualTrial e{y.p, ht.p, rk.p, kxh.p, kxd.p, yh.p, kxc.p, 0.0, 0};
     if (tK.on && fused(tK)) {
-      tiled_fused<2>("spmv_K_dual", "tiled_K_wide_combine", tK, reinterpret_cast<const double*>(xx.p), 1, e,
+      tiled_fused<1>("spmv_K_dual", "tiled_K_wide_combine", tK, xh.p, 1, e,
                      tpart.p, slot_spmv);
     } else if (tK.on) {
-      tiled_partial("tiled_K_partial", tK, 2, reinterpret_cast<const double*>(xx.p), 1);
+      tiled_partial("tiled_K_partial", tK, 1, xh.p, 1);
       launch("spmv_K_dual", [&] {
-        k_tiled_combine<EpiDualTrial, 2><<<tK.g_combine, kThreads, 0, st>>>(tK.M, tK.scratch.p, e, ctl, tpart.p,
+        k_tiled_combine<EpiDualTrial, 1><<<tK.g_combine, kThreads, 0, st>>>(tK.M, tK.scratch.p, e, ctl, tpart.p,
                                                                           slot_spmv);
       });
     } else {
-      spmv("spmv_K_dual", K, reinterpret_cast<const double*>(xx.p), nullptr, e, tpart.p, slot_spmv);
+      spmv("spmv_K_dual", K, xh.p, nullptr, e, tpart.p, slot_spmv);
     }
     run_blocks(false, bargs(false, BOP_TRIAL_DUAL), false, 0);
     if (dist) {
@@ -1673,7 +1682,7 @@ struct pdcs_ctx {
       allreduce(&ctl->red3[1], 2, RedOp::Sum);     // ||dy||^2 and <dy, K dx> over the row shards
       launch("decide", [&] { k_decide<<<1, kDecideThreads, 0, st>>>(tpart.p, 0, ctl, g_retry, g_check, 1, FusedY{}); });
     } else {
-      const FusedY fy = fuse_y() ? FusedY{m, yh.p, y0.p, y.p, ysum.p} : FusedY{};
+      const FusedY fy = fuse_y() ? FusedY{m, yh.p, y0.p, y.p, ysum.p, kxh.p, kx0.p, kxc.p} : FusedY{};
       launch("decide", [&] { k_decide<<<1, kDecideThreads, 0, st>>>(tpart.p, nslot_trial, ctl, g_retry, g_check, 0, fy); });
     }
   }
@@ -1685,7 +1694,7 @@ struct pdcs_ctx {
   void accept() {
     if (!fuse_y())
       launch("halpern_y", [&] {
-        k_halpern_y<<<g_m, kThreads, 0, st>>>(m, yh.p, y0.p, y.p, ysum.p, ctl);
+        k_halpern_y<<<g_m, kThreads, 0, st>>>(m, yh.p, y0.p, y.p, ysum.p, kxh.p, kx0.p, kxc.p, ctl);
       });
     if (dist) {
       // local K~^T y+ partial -> all-reduce -> x-side Halpern
@@ -1792,12 +1801,17 @@ struct pdcs_ctx {
     R.n = n; R.m = m;
     R.cx[0] = xh.p; R.cy[0] = yh.p; R.ckty[0] = ktyh.p;
     R.cx[1] = xa.p; R.cy[1] = ya.p; R.ckty[1] = ktya.p;
+    R.ckx[0] = kxh.p; R.ckx[1] = kxa.p; R.kxc = kxc.p; R.kx0 = kx0.p;
     R.x = x.p; R.x0 = x0.p; R.y = y.p; R.y0 = y0.p; R.kty = kty.p;
     R.xsum = xsum.p; R.ysum = ysum.p; R.bx = bx.p; R.by = by.p; R.candx = candx.p;
     R.candy = candy.p;
     launch("restart_copy", [&] {
       k_restart_copy<<<grid_for(std::max(n, m), sms), kThreads, 0, st>>>(R, ctl);
     });
+    // the carried K x is refreshed with a fresh product at every check, so its
+    // drift (O(k eps) |K x| through the Halpern recursion, P6) spans
+    // at most one check interval
+    spmv_check_K(x.p, kxc.p);
   }
 
   // Add a conditional node (WHILE / IF) at the current capture position of `st`
@@ -2034,7 +2048,6 @@ struct pdcs_ctx {
     if (elem == 2) {
       CK(cudaFuncSetAttribute(k_tiled_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_sliced<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
-      CK(cudaFuncSetAttribute(k_tiled_sliced<2, EpiDualTrial>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_sliced<2, EpiStore2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(D)));
       if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<2>, kTThreads, tma_smem(D)));
@@ -2044,6 +2057,7 @@ struct pdcs_ctx {
       CK(cudaFuncSetAttribute(k_tiled_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiled_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_sliced<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_sliced<1, EpiHalpernX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
+      CK(cudaFuncSetAttribute(k_tiled_sliced<1, EpiDualTrial>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_sliced<1, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sliced_smem(D)));
       CK(cudaFuncSetAttribute(k_tiled_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem(D)));
       if (D.tma) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled_tma<1>, kTThreads, tma_smem(D)));
@@ -2078,7 +2092,7 @@ struct pdcs_ctx {
     // Setup-time autotune: keep the tiled copy only if it beats the CSR kernel
     // by >= 10% on this matrix (gather locality decides).
     if (!env) {
-      const DevCsr& A = elem == 2 ? K : KT;
+      const DevCsr& A = &D == &tK ? K : KT;      // the CSR this tiled copy stands for
       DBuf<double> xin, out;
       xin.alloc(std::max<int64_t>(nvec * elem, 1) + 2);
       out.alloc(std::max<int64_t>(rows, 1));
@@ -2110,22 +2124,31 @@ struct pdcs_ctx {
           k_tiled_combine<EpiStore, 1><<<D.g_combine, kThreads, 0, st>>>(M, D.scratch.p, e, ctl, nullptr, 0);
         }
       };
+      static const bool dbg = std::getenv("PDCS_DEBUG_SYNC") && std::atoi(std::getenv("PDCS_DEBUG_SYNC"));
       auto timeit = [&](auto&& f) {   // median of 5 after 2 warm-ups
         f();
+        if (dbg) { CK(cudaStreamSynchronize(st)); CK(cudaGetLastError()); }
         f();
         float v[5];
         for (int i = 0; i < 5; ++i) {
           CK(cudaEventRecord(a, st));
           f();
           CK(cudaEventRecord(b, st));
+          if (dbg) {
+            const cudaError_t e = cudaEventSynchronize(b);
+            if (e != cudaSuccess) fail(PDCS_ERR_CUDA, "autotune rep " + std::to_string(i) + ": " + cudaGetErrorString(e));
+          }
           CK(cudaEventSynchronize(b));
           CK(cudaEventElapsedTime(&v[i], a, b));
         }
         std::sort(v, v + 5);
         return v[2];
       };
+      if (dbg) std::fprintf(stderr, "[pdcs debug] autotune csr, elem %d\n", elem);
       const float tc = timeit(run_csr);
+      if (dbg) std::fprintf(stderr, "[pdcs debug] autotune tiled\n");
       float tt = timeit(run_tiled);
+      if (dbg) std::fprintf(stderr, "[pdcs debug] autotune fused\n");
       const int fe = fused_env();
       if (D.sliced && !D.tma && fe != 0) {
         D.tune_fused_ms = timeit(run_fused);
@@ -2385,6 +2408,7 @@ static void reset_from_current(pdcs_ctx* ctx) {
   cp(ctx->x0.p, ctx->x.p, n); cp(ctx->xh.p, ctx->x.p, n);
   cp(ctx->ktyh.p, ctx->kty.p, n); cp(ctx->candx.p, ctx->x.p, n);
   cp(ctx->y0.p, ctx->y.p, m); cp(ctx->yh.p, ctx->y.p, m); cp(ctx->candy.p, ctx->y.p, m);
+  cp(ctx->kxc.p, ctx->kxh.p, m); cp(ctx->kx0.p, ctx->kxh.p, m);   // carried K x, K x0 (x0 = x)
   CK(cudaMemsetAsync(ctx->xsum.p, 0, n * sizeof(double), st));
   CK(cudaMemsetAsync(ctx->ysum.p, 0, m * sizeof(double), st));
   KktCand c0{ctx->x.p, ctx->y.p, ctx->kxh.p, ctx->kty.p, ctx->res0.p, ctx->lam0.p};
@@ -2532,7 +2556,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     const bool devb = tiled_devbuild_env();
     if (!devb)
       ctx->thK = std::thread([ctx, hcolp, m, n] {
-        build_tiled(ctx->hptr.data(), hcolp, m, n, 2, ctx->hK, true, true);
+        build_tiled(ctx->hptr.data(), hcolp, m, n, 1, ctx->hK, true, true);
       });
     struct Joiner {
       std::thread& t;
@@ -2589,7 +2613,7 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     ctx->K.ptr = ctx->Kptr.p; ctx->K.col = ctx->Kcol.p; ctx->K.val = ctx->Kval.p;
     tr.mark("upload K", st);
     if (devb) {
-      build_tiled_device(ctx->Kptr.p, ctx->Kcol.p, ctx->hptr.data(), m, n, 2, kTiledMinFrac, ctx->hK, ctx->tK.dv, st,
+      build_tiled_device(ctx->Kptr.p, ctx->Kcol.p, ctx->hptr.data(), m, n, 1, kTiledMinFrac, ctx->hK, ctx->tK.dv, st,
                          ctx->sms);
       tr.mark("tiled K (device build)", st);
     }
@@ -2889,11 +2913,13 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
                     &ctx->kxh, &ctx->kxd, &ctx->ya, &ctx->kxa, &ctx->by, &ctx->candy, &ctx->res0,
                     &ctx->res1, &ctx->tmpm})
       b->alloc(std::max<int64_t>(m, 1));
-    for (auto* b : {&ctx->q, &ctx->onesn, &ctx->ct, &ctx->x, &ctx->xh, &ctx->x0, &ctx->xsum, &ctx->kty,
+    ctx->xh.alloc(n + 2);  // +pad: gathered by the K sweep (TMA tile copies round up to 16 B)
+    for (auto* b : {&ctx->q, &ctx->onesn, &ctx->ct, &ctx->x, &ctx->x0, &ctx->xsum, &ctx->kty,
                     &ctx->ktyh, &ctx->xa, &ctx->ktya, &ctx->bx, &ctx->candx, &ctx->lam0,
                     &ctx->lam1, &ctx->tmpn})
       b->alloc(std::max<int64_t>(n, 1));
-    ctx->xx.alloc(std::max<int64_t>(n, 1) + 1);
+    ctx->kxc.alloc(std::max<int64_t>(m, 1) + 1);
+    ctx->kx0.alloc(std::max<int64_t>(m, 1) + 1);
     ctx->ktyp.alloc(std::max<int64_t>(n, 1));
     ctx->lt.alloc(std::max<int64_t>(n1, 1));
     ctx->ut.alloc(std::max<int64_t>(n1, 1));
@@ -2937,7 +2963,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     // column-tiled copies of K~ and K~^T for the hot SpMVs (tiled.cuh)
     {
       tr.mark("ruiz", st);
-      ctx->make_tiled(ctx->tK, ctx->hK, m, n, 2, ctx->K.val);
+      ctx->make_tiled(ctx->tK, ctx->hK, m, n, 1, ctx->K.val);
       tr.mark("tiled K (device part)", st);
       if (ctx->thKT.joinable()) ctx->thKT.join();
       tr.mark("join tiled K^T build", nullptr, false);
@@ -2948,7 +2974,7 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     }
     // L2 column panels where the gathered vector exceeds L2 (panels.cuh)
     tr.mark("tiled K^T (device part)", st);
-    ctx->build_panels(ctx->pK, ctx->K, ctx->tK.on, 2);
+    ctx->build_panels(ctx->pK, ctx->K, ctx->tK.on, 1);
     ctx->build_panels(ctx->pKT, ctx->KT, ctx->tKT.on, 1);
     tr.mark("panels", st);
     // scaled data (reading A2): c~ = c/q, h~ = h/r, l~ = q l, u~ = q u
@@ -3304,10 +3330,11 @@ pdcs_status pdcs_set_state(pdcs_ctx* ctx, const double* x, const double* y, cons
     ctx->from_caller(ctx->x.p, x, kind); put(ctx->y, y, m); ctx->from_caller(ctx->x0.p, x0, kind);
     put(ctx->y0, y0, m); ctx->from_caller(ctx->xsum.p, xsum, kind); put(ctx->ysum, ysum, m);
     ctx->products(ctx->x.p, ctx->y.p, ctx->kxh.p, ctx->kty.p);
+    ctx->spmv_store(ctx->K, ctx->x0.p, ctx->kx0.p);      // fresh K x0 (the carried products restart here)
     auto cp = [&](double* d, const double* s_, int64_t cnt) {
       if (cnt) CK(cudaMemcpyAsync(d, s_, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
     };
-    cp(ctx->xh.p, ctx->x.p, n); cp(ctx->yh.p, ctx->y.p, m);
+    cp(ctx->xh.p, ctx->x.p, n); cp(ctx->yh.p, ctx->y.p, m); cp(ctx->kxc.p, ctx->kxh.p, m);
     cp(ctx->ktyh.p, ctx->kty.p, n);
     ctx->read_ctl();
     Ctl& C = *ctx->hctl;

@@ -498,6 +498,9 @@ __device__ __forceinline__ void tile_fetch_async(const TiledMat& M, const double
 #ifndef PDCS_SL_U1
 #define PDCS_SL_U1 4                  // quads in flight per lane, single gather
 #endif
+#ifndef PDCS_SL_PIPE
+#define PDCS_SL_PIPE 0                // > 0: software-pipelined loop, this many quads per stage
+#endif
 // One staged segment, warp per block of 32/V rows.  Blocks go to warps in
 // snake order (rows are sorted longest first, so this balances the warps);
 // the next block's row lengths, base and output rows are loaded before the
@@ -539,6 +542,54 @@ __device__ __forceinline__ void sliced_blocks(const TiledMat& M, const TSeg& S, 
     const double* vp = val + 4 * ((int64_t)base + lane);
     const uint16_t* cp = col + 4 * ((int64_t)base + lane);
     double s1 = 0.0, s2 = 0.0;
+#if PDCS_SL_PIPE
+    // software-pipelined: the next PU quads' loads are in flight while the
+    // current ones are gathered and summed (same entry order, same sums)
+    {
+      constexpr int PU = PDCS_SL_PIPE;
+      double q[PU][4];
+      uint2 c[PU];
+#define PDCS_SL_FETCH(TT, QQ, CC)                                             \
+  _Pragma("unroll") for (int u = 0; u < PU; ++u) {                            \
+    if ((TT) + u < nt) {                                                      \
+      const double4 v_ = ld_stream4(vp + 128 * (int64_t)((TT) + u));          \
+      CC[u] = ld_stream_u2(cp + 128 * (int64_t)((TT) + u));                   \
+      QQ[u][0] = v_.x; QQ[u][1] = v_.y; QQ[u][2] = v_.z; QQ[u][3] = v_.w;     \
+    } else {                                                                  \
+      CC[u] = make_uint2(0u, 0u);                                             \
+      QQ[u][0] = QQ[u][1] = QQ[u][2] = QQ[u][3] = 0.0;                        \
+    }                                                                         \
+  }
+      PDCS_SL_FETCH(0, q, c)
+      for (int32_t t0 = 0; t0 < tmax; t0 += PU) {
+        double qn[PU][4];
+        uint2 cn[PU];
+        PDCS_SL_FETCH(t0 + PU, qn, cn)
+#pragma unroll
+        for (int u = 0; u < PU; ++u)
+          if (t0 + u < nt) {
+            const uint32_t cc[4] = {c[u].x & 0xffffu, c[u].x >> 16, c[u].y & 0xffffu, c[u].y >> 16};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (ELEM == 2) {
+                const double2 v = lds_v2(xs_s + cc[k] * 16u);
+                s1 += q[u][k] * v.x;
+                s2 += q[u][k] * v.y;
+              } else {
+                s1 += q[u][k] * lds_f64(xs_s + cc[k] * 8u);
+              }
+            }
+          }
+#pragma unroll
+        for (int u = 0; u < PU; ++u) {
+          c[u] = cn[u];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) q[u][k] = qn[u][k];
+        }
+      }
+#undef PDCS_SL_FETCH
+    }
+#else
     for (int32_t t0 = 0; t0 < tmax; t0 += U) {
       double q[U][4];
       uint2 c[U];
@@ -569,6 +620,7 @@ __device__ __forceinline__ void sliced_blocks(const TiledMat& M, const TSeg& S, 
           }
         }
     }
+#endif
     if (V > 1) {
 #pragma unroll
       for (int o = V / 2; o >= 1; o >>= 1) {

@@ -243,11 +243,12 @@ struct EpiDualTrial {
   __device__ void init(const Ctl* c) { sigma = c->sigma; run = c->status == ST_RUNNING; }
   __device__ bool active() const { return run; }
   __device__ void row(int64_t i, double kxhat, double, Acc<NA>& a) {
-    const double kx = kxc[i];
+    // read-only inputs through the non-coherent path: the compiler may then
+    // issue them ahead of this and earlier rows' stores (kxh, yh, kxd)
+    const double kx = __ldg(kxc + i), yi = __ldg(y + i), hi = __ldg(h + i);
+    const uint8_t k = __ldg(rk + i);
     kxh[i] = kxhat;
-    const double yi = y[i];
-    const double v = yi + sigma * (h[i] - 2.0 * kxhat + kx);
-    const uint8_t k = rk[i];
+    const double v = yi + sigma * (hi - 2.0 * kxhat + kx);
     if (k == EK_BLOCK) { yh[i] = v; kxd[i] = kxhat - kx; return; }
     const double p = k == EK_NONNEG ? fmax(v, 0.0) : v;
     yh[i] = p;

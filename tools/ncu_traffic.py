@@ -29,7 +29,8 @@ sys.path.insert(0, ROOT)
 
 # the format the bench's autotune keeps per config
 TILED = {"lasso": "1", "fisher": "0", "mpo": "0", "mixed": "0"}
-SWEEPS = {"spmv_K_dual": ("k_tiled_sliced<2>", "k_tiled_sliced<2,", "k_tiled_sliced<(int)2,", "k_tiled_tma<2>", "k_tiled_partial<2>",
+SWEEPS = {"spmv_K_dual": ("k_tiled_sliced<2>", "k_tiled_sliced<2,", "k_tiled_sliced<(int)2,", "k_tiled_sliced<1,",
+                          "k_tiled_sliced<(int)1,", "k_tiled_tma<2>", "k_tiled_partial<2>",
                           "k_tiled_combine<EpiDualTrial", "spmv_kernel<EpiDualTrial>"),
           "spmv_KT_halpern": ("k_tiled_sliced<1>", "k_tiled_sliced<1,", "k_tiled_sliced<(int)1,", "k_tiled_tma<1>", "k_tiled_partial<1>",
                               "k_tiled_combine<EpiHalpernX", "spmv_kernel<EpiHalpernX>"),
@@ -78,14 +79,28 @@ def run(configs, iters, out, parse_only=False, commit=None):
             per[r[idi]][r[mi]] = float(r[vi].replace(",", ""))
             name[r[idi]] = r[ki]
         acc = defaultdict(lambda: [0.0, 0.0, 0])           # sweep part -> bytes, ns, launches
+        # K's and K^T's tiled partials are the same kernel (single-element
+        # tiles since the carried K x, DESIGN P6): a partial belongs to the
+        # sweep of the next combine launch (EpiDualTrial: K, EpiHalpernX: K^T)
+        ids = sorted(per, key=int)
+        owner = {}
+        for k, lid in enumerate(ids):
+            if "k_tiled_sliced<" in name[lid] or "k_tiled_partial<" in name[lid] or "k_tiled_tma<" in name[lid]:
+                for nxt in ids[k + 1:]:
+                    if "k_tiled_combine<" in name[nxt]:
+                        owner[lid] = "spmv_K_dual" if "EpiDualTrial" in name[nxt] else "spmv_KT_halpern"
+                        break
         for lid, m in per.items():
             for sw, pats in SWEEPS.items():
+                if lid in owner and owner[lid] != sw:
+                    continue
                 for pat in pats:
                     if pat in name[lid]:
                         a = acc[(sw, pat)]
                         a[0] += m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]
                         a[1] += m["gpu__time_duration.sum"]
                         a[2] += 1
+                        break
         cres = {}
         for sw in SWEEPS:
             parts = {pat: v for (s, pat), v in acc.items() if s == sw and v[2]}

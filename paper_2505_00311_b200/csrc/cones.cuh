@@ -302,19 +302,27 @@ __device__ __forceinline__ int det_sign(const ExpDet& e) {
 }
 
 // P_{D K_exp}(v0), Theorem 4 with reading A18.
-__device__ __noinline__ void proj_exp_d(double r0, double s0, double t0, double dr, double ds,
-                                        double dt, double& o0, double& o1, double& o2) {
+// proj_exp_quick: cases 1-3 (membership tests and the r0, s0 <= 0 face);
+// false when the root case 4 is needed (proj_exp_case4).  proj_exp_d is the
+// two in sequence; the thread-class kernel runs them as two passes so that the
+// lanes of a warp that need the root finder are packed together.
+__device__ __forceinline__ bool proj_exp_quick(double r0, double s0, double t0, double dr, double ds, double dt,
+                                               double& o0, double& o1, double& o2) {
   {  // case 1: D^-1 v0 in K_exp
     const double w0 = r0 / dr, w1 = s0 / ds, w2 = t0 / dt;
     const double tol = 1e-12 * sqrt(w0 * w0 + w1 * w1 + w2 * w2);
-    if (d_in_exp(w0, w1, w2, tol)) { o0 = r0; o1 = s0; o2 = t0; return; }
+    if (d_in_exp(w0, w1, w2, tol)) { o0 = r0; o1 = s0; o2 = t0; return true; }
   }
   {  // case 2: -D v0 in K_exp^*
     const double w0 = -dr * r0, w1 = -ds * s0, w2 = -dt * t0;
     const double tol = 1e-12 * sqrt(w0 * w0 + w1 * w1 + w2 * w2);
-    if (d_in_exp_dual(w0, w1, w2, tol)) { o0 = 0.0; o1 = 0.0; o2 = 0.0; return; }
+    if (d_in_exp_dual(w0, w1, w2, tol)) { o0 = 0.0; o1 = 0.0; o2 = 0.0; return true; }
   }
-  if (r0 <= 0.0 && s0 <= 0.0) { o0 = r0; o1 = 0.0; o2 = fmax(t0, 0.0); return; }   // case 3
+  if (r0 <= 0.0 && s0 <= 0.0) { o0 = r0; o1 = 0.0; o2 = fmax(t0, 0.0); return true; }   // case 3
+  return false;
+}
+__device__ __noinline__ void proj_exp_case4(double r0, double s0, double t0, double dr, double ds, double dt,
+                                            double& o0, double& o1, double& o2) {
   const ExpRatios q(dr, ds, dt);
   // case 4: bracket (Eq. 16); an end whose det is rounding
   // noise is the root.
@@ -407,12 +415,26 @@ __device__ __noinline__ void proj_exp_d(double r0, double s0, double t0, double 
   o0 = b0; o1 = b1; o2 = b2;
 }
 
+__device__ __noinline__ void proj_exp_d(double r0, double s0, double t0, double dr, double ds,
+                                        double dt, double& o0, double& o1, double& o2) {
+  if (proj_exp_quick(r0, s0, t0, dr, ds, dt, o0, o1, o2)) return;
+  proj_exp_case4(r0, s0, t0, dr, ds, dt, o0, o1, o2);
+}
+
 // P_{D K_exp^*}(v) = v + P_{D^-1 K_exp}(-v)  (Remark)
-__device__ __forceinline__ void proj_dexp_d(double r0, double s0, double t0, double dr, double ds,
-                                            double dt, double& o0, double& o1, double& o2) {
+// phase 0: whole; 1: quick cases only (false: case 4 needed); 2: case 4 only.
+__device__ __forceinline__ bool proj_dexp_d(double r0, double s0, double t0, double dr, double ds,
+                                            double dt, double& o0, double& o1, double& o2, int phase = 0) {
   double p0, p1, p2;
-  proj_exp_d(-r0, -s0, -t0, 1.0 / dr, 1.0 / ds, 1.0 / dt, p0, p1, p2);
+  if (phase == 1) {
+    if (!proj_exp_quick(-r0, -s0, -t0, 1.0 / dr, 1.0 / ds, 1.0 / dt, p0, p1, p2)) return false;
+  } else if (phase == 2) {
+    proj_exp_case4(-r0, -s0, -t0, 1.0 / dr, 1.0 / ds, 1.0 / dt, p0, p1, p2);
+  } else {
+    proj_exp_d(-r0, -s0, -t0, 1.0 / dr, 1.0 / ds, 1.0 / dt, p0, p1, p2);
+  }
   o0 = r0 + p0; o1 = s0 + p1; o2 = t0 + p2;
+  return true;
 }
 
 }  // namespace pdcs

@@ -101,9 +101,12 @@ struct DstKktCols {       // distance of lambda_2 to K_p^*, Eq. 9 err_d
 // HAS_EXP = false for the multi-thread teams (exp blocks are always in the
 // thread class): the exp root finder is then not compiled into their kernels,
 // whose register allocation would otherwise be set by it.
+// exp_phase (thread class only): 0 whole projection; 1 the quick cases of an
+// exp block only, false when it needs the root case (nothing written); 2 the
+// root case only.  Non-exp blocks ignore it.
 template <bool HAS_EXP, class Team, class Src, class Dst>
-__device__ __forceinline__ void project_block(Team& tm, const Block& b, bool exp_dual, bool unit,
-                                              const Src& src, Dst& dst) {
+__device__ __forceinline__ bool project_block(Team& tm, const Block& b, bool exp_dual, bool unit,
+                                              const Src& src, Dst& dst, int exp_phase = 0) {
   if (!HAS_EXP || b.kind == C_SOC || b.kind == C_RSOC) {
     SrcAdapt<Src> s{src};
     soc_team(tm, (int64_t)b.dim, b.kind == C_RSOC, unit, s, dst);
@@ -113,11 +116,19 @@ __device__ __forceinline__ void project_block(Team& tm, const Block& b, bool exp
       const double dr = unit ? 1.0 : src.D_(0), ds = unit ? 1.0 : src.D_(1), dt = unit ? 1.0 : src.D_(2);
       double o0, o1, o2;
       const bool dual = (b.kind == C_EXP) == exp_dual;
-      if (dual) proj_dexp_d(r0, s0, t0, dr, ds, dt, o0, o1, o2);
-      else proj_exp_d(r0, s0, t0, dr, ds, dt, o0, o1, o2);
+      if (dual) {
+        if (!proj_dexp_d(r0, s0, t0, dr, ds, dt, o0, o1, o2, exp_phase)) return false;
+      } else if (exp_phase == 1) {
+        if (!proj_exp_quick(r0, s0, t0, dr, ds, dt, o0, o1, o2)) return false;
+      } else if (exp_phase == 2) {
+        proj_exp_case4(r0, s0, t0, dr, ds, dt, o0, o1, o2);
+      } else {
+        proj_exp_d(r0, s0, t0, dr, ds, dt, o0, o1, o2);
+      }
       dst.put(0, o0); dst.put(1, o1); dst.put(2, o2);
     }
   }
+  return true;
 }
 
 // ---------------------------------------------------------------- block-cone kernels
@@ -152,47 +163,49 @@ struct BlockArgs {
 
 // OP is the kernel's template constant (BlockOp), so each kernel holds one path.
 template <bool HAS_EXP, int OP, class Team>
-__device__ __forceinline__ void run_block(Team& tm, const BlockArgs& A, const Ctl* ctl, const Block& b,
-                                          Acc<kAcc>& acc, double* kv) {
+__device__ __forceinline__ bool run_block(Team& tm, const BlockArgs& A, const Ctl* ctl, const Block& b,
+                                          Acc<kAcc>& acc, double* kv, int exp_phase = 0) {
+  bool done = true;
   switch (OP) {
     case BOP_TRIAL_PRIMAL: {
       SrcPrimalTrial s{A.x, A.c, A.kty, A.D, ctl->tau, b.off};
       DstTrialPrimal d{A.xh, A.x, b.off, &acc};
-      project_block<HAS_EXP>(tm, b, false, false, s, d);
+      done = project_block<HAS_EXP>(tm, b, false, false, s, d, exp_phase);
       break;
     }
     case BOP_TRIAL_DUAL: {
       SrcStored s{A.yh, A.D, b.off};
       DstTrialDual d{A.yh, A.y, A.kxd, b.off, &acc};
-      project_block<HAS_EXP>(tm, b, true, false, s, d);
+      done = project_block<HAS_EXP>(tm, b, true, false, s, d, exp_phase);
       break;
     }
     case BOP_AVG_PRIMAL:
     case BOP_AVG_DUAL: {
       SrcAverage s{A.sum, A.D, ctl->Wsum, b.off};
       DstStore d{A.out, b.off};
-      project_block<HAS_EXP>(tm, b, OP == BOP_AVG_DUAL, false, s, d);
+      done = project_block<HAS_EXP>(tm, b, OP == BOP_AVG_DUAL, false, s, d, exp_phase);
       break;
     }
     case BOP_KKT_ROWS: {
       SrcStored s{A.scratch, nullptr, b.off};
       DstKktRows d{A.scratch, b.off, kv + 0, kv + 2};
-      project_block<HAS_EXP>(tm, b, false, true, s, d);
+      done = project_block<HAS_EXP>(tm, b, false, true, s, d, exp_phase);
       break;
     }
     case BOP_KKT_COLS: {
       SrcStored s{A.scratch, nullptr, b.off};
       DstKktCols d{A.scratch, b.off, kv + 5};
-      project_block<HAS_EXP>(tm, b, true, true, s, d);
+      done = project_block<HAS_EXP>(tm, b, true, true, s, d, exp_phase);
       break;
     }
     case BOP_PROJECT: {
       SrcStored s{A.scratch, A.D, b.off};
       DstStore d{A.out, b.off};
-      project_block<HAS_EXP>(tm, b, false, A.D == nullptr, s, d);
+      done = project_block<HAS_EXP>(tm, b, false, A.D == nullptr, s, d, exp_phase);
       break;
     }
   }
+  return done;
 }
 
 template <int OP>
@@ -225,17 +238,46 @@ __device__ __forceinline__ void finish_block_partials(const BlockArgs& A, Acc<kA
   }
 }
 
-// One block per thread (exp / dual exp / SOC of dim <= 32).
+// One block per thread (exp / dual exp / SOC of dim <= 32).  Two passes per
+// CTA step: every thread projects its block, an exp block only through its
+// quick cases (membership, the r0, s0 <= 0 face); the exp blocks that need the
+// root finder are then packed in thread order into a shared list and
+// projected by the first threads of the CTA.  Lanes that finished early no
+// longer idle beside a root finder in the same warp (round 1: 5.6 of 32 lanes
+// active per instruction on mixed cfg 5).  Work per thread is fixed by the
+// data, so the accumulators are summed in a fixed order.
 template <int OP>
 __global__ void __launch_bounds__(kThreads) k_blocks_thread(BlockArgs A, const Ctl* ctl) {
   if (!block_op_active<OP>(A, ctl)) return;
   Acc<kAcc> acc; acc.zero();
   double kv[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   ThreadTeam tm;
-  for (int64_t bi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; bi < A.nblocks;
-       bi += (int64_t)gridDim.x * blockDim.x) {
-    const Block b = A.blocks[bi];
-    run_block<true, OP>(tm, A, ctl, b, acc, kv);
+  __shared__ int32_t s_list[kThreads];
+  __shared__ int32_t s_wcnt[kThreads / 32 + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < A.nblocks; base += stride) {
+    const int64_t bi = base + threadIdx.x;
+    bool defer = false;
+    if (bi < A.nblocks) {
+      const Block b = A.blocks[bi];
+      defer = !run_block<true, OP>(tm, A, ctl, b, acc, kv, 1);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, defer);
+    if (lane == 0) s_wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      off += w < warp ? s_wcnt[w] : 0;
+      tot += s_wcnt[w];
+    }
+    if (defer) s_list[off + __popc(bal & ((1u << lane) - 1u))] = threadIdx.x;
+    __syncthreads();
+    for (int k = threadIdx.x; k < tot; k += blockDim.x) {
+      const Block b = A.blocks[base + s_list[k]];
+      run_block<true, OP>(tm, A, ctl, b, acc, kv, 2);
+    }
+    __syncthreads();
   }
   finish_block_partials<OP>(A, acc, kv);
 }

@@ -1051,9 +1051,14 @@ __global__ void k_tile_hist(const int32_t* __restrict__ ptr, const int32_t* __re
     for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) hist[t] = 0;
     __syncthreads();
   }
-  for (int64_t p = __ldg(ptr + r0) + threadIdx.x; p < __ldg(ptr + r1); p += blockDim.x) {
-    const int32_t t = __ldg(col + p) / T;
-    atomicAdd(use_smem ? hist + t : dst + t, 1);
+  // entries are sorted by column within a row, so neighbouring lanes mostly
+  // share a tile: one atomic per (warp step, tile) instead of one per entry
+  const int64_t pe = __ldg(ptr + r1);
+  for (int64_t p0 = __ldg(ptr + r0); p0 < pe; p0 += blockDim.x) {
+    const int64_t p = p0 + threadIdx.x;
+    const int32_t t = p < pe ? __ldg(col + p) / T : -1 - (int32_t)(threadIdx.x & 31);
+    const unsigned same = __match_any_sync(0xffffffffu, t);
+    if (p < pe && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(use_smem ? hist + t : dst + t, __popc(same));
   }
   if (use_smem) {
     __syncthreads();

@@ -131,9 +131,17 @@ enum SocMode { SM_ZERO = 0, SM_IDENT = 1, SM_HALF = 2, SM_LAM = 3, SM_MU = 4 };
 template <class Team> __device__ __forceinline__ double* team_cache(Team&) { return nullptr; }
 __device__ __forceinline__ double* team_cache(GridTeam& t) { return t.cache; }
 
+#ifndef PDCS_WARM_DELTA
+#define PDCS_WARM_DELTA 1e-3          // relative margin below the previous root
+#endif
+// warm (optional): this block's multiplier from its previous projection of the
+// same kind (> 0: lambda-form root, < 0: mu-form root negated, 0: none).  The
+// Newton iteration then starts just below it (1e-3 relative) instead of at 0,
+// and falls back to 0 if that start is not below the new root; the root it
+// converges to is the same one (the stopping rule does not depend on the start).
 template <class Team, class Src, class Dst>
 __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool unit, const Src& src,
-                                         Dst& dst, int* newton_iters = nullptr) {
+                                         Dst& dst, int* newton_iters = nullptr, double* warm = nullptr) {
   const double v0 = src.v(0), v1 = src.v(1);
   const double t = rsoc ? (v0 + v1) * kRsqrt2 : v0;
   const double x1 = rsoc ? (v0 - v1) * kRsqrt2 : v1;
@@ -200,6 +208,12 @@ __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool un
   int its = 0;
   if (mode == SM_LAM || mode == SM_MU) {
     const double at = fabs(t);
+    bool warm_try = false;
+    if (warm) {
+      const double w = *warm;
+      const double wp = mode == SM_LAM ? w : -w;
+      if (wp > 0.0 && wp < (mode == SM_LAM ? 0.5 : 1.0)) { par = wp * (1.0 - PDCS_WARM_DELTA); warm_try = true; }
+    }
     for (; its < 64; ++its) {
       double S0 = 0.0, S1 = 0.0;
       each([&](int64_t, double x, double h) {
@@ -220,7 +234,11 @@ __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool un
         psi = 1.0 / nrm - (1.0 - par) / at;
         dpsi = S1 / (S0 * nrm) + 1.0 / at;
       }
-      if (!(psi < 0.0)) break;                  // at (or past, by rounding) the root
+      if (!(psi < 0.0)) {                       // at (or past, by rounding) the root
+        if (warm_try) { warm_try = false; par = 0.0; continue; }   // the warm start was above it
+        break;
+      }
+      warm_try = false;
       const double step = -psi / dpsi;
       const double cap = mode == SM_LAM ? 0.5 : 1.0;
       double np = par + step;
@@ -232,6 +250,7 @@ __device__ __forceinline__ void soc_team(Team& tm, int64_t d, bool rsoc, bool un
     }
   }
   if (newton_iters) *newton_iters = its;
+  if (warm && tm.rank() == 0) *warm = mode == SM_LAM ? par : mode == SM_MU ? -par : 0.0;
   // recovery: y_i, s = ||y/dh|| (reading A16)
   auto Y = [&](double x, double h) {
     const double h2 = h * h;

@@ -106,10 +106,11 @@ struct DstKktCols {       // distance of lambda_2 to K_p^*, Eq. 9 err_d
 // root case only.  Non-exp blocks ignore it.
 template <bool HAS_EXP, class Team, class Src, class Dst>
 __device__ __forceinline__ bool project_block(Team& tm, const Block& b, bool exp_dual, bool unit,
-                                              const Src& src, Dst& dst, int exp_phase = 0) {
+                                              const Src& src, Dst& dst, int exp_phase = 0,
+                                              double* warm = nullptr) {
   if (!HAS_EXP || b.kind == C_SOC || b.kind == C_RSOC) {
     SrcAdapt<Src> s{src};
-    soc_team(tm, (int64_t)b.dim, b.kind == C_RSOC, unit, s, dst);
+    soc_team(tm, (int64_t)b.dim, b.kind == C_RSOC, unit, s, dst, nullptr, warm);
   } else {  // 3-d exponential blocks: one thread
     if (tm.rank() == 0) {
       const double r0 = src.v(0), s0 = src.v(1), t0 = src.v(2);
@@ -159,24 +160,25 @@ struct BlockArgs {
   const double* scratch;          // KKT residuals / lambdas
   double* part;                   // trial partials (kAcc) or KKT partials (kKAcc)
   int64_t slot0;
+  double* warm;                   // trial ops: each block's last SOC/RSOC multiplier (soc_team)
 };
 
 // OP is the kernel's template constant (BlockOp), so each kernel holds one path.
 template <bool HAS_EXP, int OP, class Team>
 __device__ __forceinline__ bool run_block(Team& tm, const BlockArgs& A, const Ctl* ctl, const Block& b,
-                                          Acc<kAcc>& acc, double* kv, int exp_phase = 0) {
+                                          Acc<kAcc>& acc, double* kv, int exp_phase = 0, int64_t bidx = 0) {
   bool done = true;
   switch (OP) {
     case BOP_TRIAL_PRIMAL: {
       SrcPrimalTrial s{A.x, A.c, A.kty, A.D, ctl->tau, b.off};
       DstTrialPrimal d{A.xh, A.x, b.off, &acc};
-      done = project_block<HAS_EXP>(tm, b, false, false, s, d, exp_phase);
+      done = project_block<HAS_EXP>(tm, b, false, false, s, d, exp_phase, A.warm ? A.warm + bidx : nullptr);
       break;
     }
     case BOP_TRIAL_DUAL: {
       SrcStored s{A.yh, A.D, b.off};
       DstTrialDual d{A.yh, A.y, A.kxd, b.off, &acc};
-      done = project_block<HAS_EXP>(tm, b, true, false, s, d, exp_phase);
+      done = project_block<HAS_EXP>(tm, b, true, false, s, d, exp_phase, A.warm ? A.warm + bidx : nullptr);
       break;
     }
     case BOP_AVG_PRIMAL:
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(kThreads) k_blocks_thread(BlockArgs A, const C
     bool defer = false;
     if (bi < A.nblocks) {
       const Block b = A.blocks[bi];
-      defer = !run_block<true, OP>(tm, A, ctl, b, acc, kv, 1);
+      defer = !run_block<true, OP>(tm, A, ctl, b, acc, kv, 1, bi);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, defer);
     if (lane == 0) s_wcnt[warp] = __popc(bal);
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) k_blocks_thread(BlockArgs A, const C
     __syncthreads();
     for (int k = threadIdx.x; k < tot; k += blockDim.x) {
       const Block b = A.blocks[base + s_list[k]];
-      run_block<true, OP>(tm, A, ctl, b, acc, kv, 2);
+      run_block<true, OP>(tm, A, ctl, b, acc, kv, 2, base + s_list[k]);
     }
     __syncthreads();
   }
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kThreads) k_blocks_warp(BlockArgs A, const Ctl
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t bi = wid; bi < A.nblocks; bi += nw) {
     const Block b = A.blocks[bi];
-    run_block<false, OP>(tm, A, ctl, b, acc, kv);
+    run_block<false, OP>(tm, A, ctl, b, acc, kv, 0, bi);
   }
   finish_block_partials<OP>(A, acc, kv);
 }
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(kThreads) k_blocks_cta(BlockArgs A, const Ctl*
   CtaTeam tm{sm};
   for (int64_t bi = blockIdx.x; bi < A.nblocks; bi += gridDim.x) {
     const Block b = A.blocks[bi];
-    run_block<false, OP>(tm, A, ctl, b, acc, kv);
+    run_block<false, OP>(tm, A, ctl, b, acc, kv, 0, bi);
   }
   finish_block_partials<OP>(A, acc, kv);
 }
@@ -326,7 +328,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
   const int64_t cid = blockIdx.x / kClusterCtas, ncl = gridDim.x / kClusterCtas;
   for (int64_t bi = cid; bi < A.nblocks; bi += ncl) {
     const Block b = A.blocks[bi];
-    run_block<false, OP>(tm, A, ctl, b, acc, kv);
+    run_block<false, OP>(tm, A, ctl, b, acc, kv, 0, bi);
   }
   finish_block_partials<OP>(A, acc, kv);
 }
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(kThreads) k_blocks_grid(BlockArgs A, const Ctl
   GridTeam tm{sm, gbuf, 0, gcache};
   for (int64_t bi = 0; bi < A.nblocks; ++bi) {
     const Block b = A.blocks[bi];
-    run_block<false, OP>(tm, A, ctl, b, acc, kv);
+    run_block<false, OP>(tm, A, ctl, b, acc, kv, 0, bi);
   }
   finish_block_partials<OP>(A, acc, kv);
 }

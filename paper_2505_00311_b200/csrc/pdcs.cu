@@ -832,11 +832,21 @@ void build_tiled_device(const int32_t* dptr, const int32_t* dcol, const int64_t*
     dc.alloc((size_t)per * ntiles);
     std::vector<int32_t> hc((size_t)per * ntiles);
     const bool smem = ntiles <= 12288;
+    std::vector<THistItem> items;
+    DBuf<THistItem> ditems;
     for (int64_t c0 = 0; c0 < nchunk; c0 += per) {
       const int64_t nc = std::min(per, nchunk - c0);
-      if (!smem) CK(cudaMemsetAsync(dc.p, 0, (size_t)nc * ntiles * sizeof(int32_t), st));
-      k_tile_hist<<<(unsigned)nc, 256, smem ? ntiles * sizeof(int32_t) : 0, st>>>(dptr, dcol, rows, T, ntiles, c0,
-                                                                                  dc.p, smem ? 1 : 0);
+      items.clear();
+      for (int64_t c = c0; c < c0 + nc; ++c) {
+        const int64_t pa = hptr[c * kTRows], pb = hptr[std::min(rows, (c + 1) * kTRows)];
+        for (int64_t q = pa; q < pb; q += 65536) items.push_back(THistItem{c, q, std::min(pb, q + 65536)});
+      }
+      CK(cudaMemsetAsync(dc.p, 0, (size_t)nc * ntiles * sizeof(int32_t), st));
+      if (!items.empty()) {
+        upload(ditems, items, st);
+        k_tile_hist<<<(unsigned)items.size(), 256, smem ? ntiles * sizeof(int32_t) : 0, st>>>(
+            dcol, ditems.p, T, ntiles, c0, dc.p, smem ? 1 : 0);
+      }
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(hc.data(), dc.p, (size_t)nc * ntiles * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -1384,6 +1394,7 @@ struct pdcs_ctx {
   std::vector<int32_t> hKTcol;
   DBuf<uint8_t> ek, rk;
   DBuf<Block> pblocks, rblocks;
+  DBuf<double> warm_p, warm_r;                 // last SOC/RSOC multiplier of every block (trial ops)
   DBuf<int64_t> rsoc_offs_p, rsoc_offs_r;
   DBuf<double> tpart, kpart, gbuf;
   Ctl* ctl = nullptr;        // device
@@ -1598,6 +1609,10 @@ struct pdcs_ctx {
     A.x = x.p; A.c = ct.p; A.kty = kty.p; A.xh = xh.p;
     A.D = primal ? q.p : r.p;
     A.y = y.p; A.yh = yh.p; A.kxd = kxd.p;
+    // warm-started multipliers for the trial projections (soc_team); env
+    // PDCS_WARM=0 starts every Newton iteration at 0
+    static const bool warm_off = std::getenv("PDCS_WARM") && std::atoi(std::getenv("PDCS_WARM")) == 0;
+    if (!warm_off && (op == BOP_TRIAL_PRIMAL || op == BOP_TRIAL_DUAL)) A.warm = primal ? warm_p.p : warm_r.p;
     return A;
   }
   // The size classes of one side are independent (disjoint coordinates and
@@ -1643,6 +1658,7 @@ struct pdcs_ctx {
       B.cand = cand;
       B.part = kkt ? kpart.p : tpart.p;
       B.slot0 = kkt ? cl[c].kslot[cand] : cl[c].slot;
+      if (A.warm) B.warm = A.warm + cl[c].begin;
       return B;
     };
     for (int i = 0; i < na; ++i) {
@@ -2887,6 +2903,11 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     classify(rb, ctx->rcls);
     upload(ctx->pblocks, pb, st);
     upload(ctx->rblocks, rb, st);
+    for (auto* w : {&ctx->warm_p, &ctx->warm_r}) {
+      const size_t nb = std::max<size_t>(w == &ctx->warm_p ? pb.size() : rb.size(), 1);
+      w->alloc(nb);
+      CK(cudaMemsetAsync(w->p, 0, nb * sizeof(double), st));
+    }
     upload(ctx->ek, ek, st);
     upload(ctx->rk, rk, st);
     std::vector<int64_t> prs64(prs.begin(), prs.end()), rrs64(rrs.begin(), rrs.end());

@@ -1039,30 +1039,35 @@ __device__ __forceinline__ int tb_seg_of(const TBChunk& C, const int32_t* __rest
   return (lo < C.nst && __ldg(stl + C.soff + lo) == t) ? C.direct + lo : 0;
 }
 
-// Entries per (chunk, tile) for chunks [c0, c1): out[(c - c0) * ntiles + t]
-// (zeroed by the caller); a shared-memory histogram when ntiles fits.
-__global__ void k_tile_hist(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col, int64_t rows,
-                            int32_t T, int64_t ntiles, int64_t c0, int32_t* __restrict__ out, int use_smem) {
+// Entries per (chunk, tile): out[(chunk - c0) * ntiles + t] (zeroed by the
+// caller).  One CTA per item = a range of at most 65536 entries of one chunk
+// (a chunk of 1024 long rows holds ~1e7 entries on Lasso's K^T: one CTA per
+// chunk had taken 27 ms), a shared-memory histogram when ntiles fits, added
+// into the chunk's row of out.
+struct THistItem {
+  int64_t chunk, p0, p1;
+};
+__global__ void k_tile_hist(const int32_t* __restrict__ col, const THistItem* __restrict__ items, int32_t T,
+                            int64_t ntiles, int64_t c0, int32_t* __restrict__ out, int use_smem) {
   extern __shared__ int32_t hist[];
-  const int64_t c = c0 + blockIdx.x;
-  const int64_t r0 = c * kTRows, r1 = (rows < r0 + kTRows) ? rows : r0 + kTRows;
-  int32_t* dst = out + (int64_t)blockIdx.x * ntiles;
+  const THistItem I = items[blockIdx.x];
+  int32_t* dst = out + (I.chunk - c0) * ntiles;
   if (use_smem) {
     for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) hist[t] = 0;
     __syncthreads();
   }
   // entries are sorted by column within a row, so neighbouring lanes mostly
   // share a tile: one atomic per (warp step, tile) instead of one per entry
-  const int64_t pe = __ldg(ptr + r1);
-  for (int64_t p0 = __ldg(ptr + r0); p0 < pe; p0 += blockDim.x) {
-    const int64_t p = p0 + threadIdx.x;
-    const int32_t t = p < pe ? __ldg(col + p) / T : -1 - (int32_t)(threadIdx.x & 31);
+  for (int64_t q0 = I.p0; q0 < I.p1; q0 += blockDim.x) {
+    const int64_t p = q0 + threadIdx.x;
+    const int32_t t = p < I.p1 ? __ldg(col + p) / T : -1 - (int32_t)(threadIdx.x & 31);
     const unsigned same = __match_any_sync(0xffffffffu, t);
-    if (p < pe && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(use_smem ? hist + t : dst + t, __popc(same));
+    if (p < I.p1 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(use_smem ? hist + t : dst + t, __popc(same));
   }
   if (use_smem) {
     __syncthreads();
-    for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) dst[t] = hist[t];
+    for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x)
+      if (hist[t]) atomicAdd(dst + t, hist[t]);
   }
 }
 

@@ -395,6 +395,34 @@ def test_fused_combine_matches_partial_plus_combine(P, tiled_env, monkeypatch):
                 assert parity(*a, *b) <= 1e-11
 
 
+def test_warm_started_soc_multipliers(P, monkeypatch):
+    """The trial projections start each SOC/RSOC Newton iteration from 90% of
+    the block's previous multiplier (soc_team, PDCS_WARM).  The root is the
+    same one as from a cold start, so 60 PDCS iterations with and without the
+    warm start agree to rounding, and one step from random points matches the
+    oracle at 1e-12 either way (warm value carried over from earlier steps)."""
+    prog = mixed(17, m=900, n1=120, n2=500, soc_dims=(3, 200))
+    runs = {}
+    for warm in ("1", "0"):
+        monkeypatch.setenv("PDCS_WARM", warm)
+        g = P.PdcsSolver(prog)
+        g.iterate(60)
+        runs[warm] = g.get_iterate(P.CURRENT)
+        if warm == "1":
+            o = O.OracleSolver(prog)
+            ro, qo = o.get_scaling()
+            rng = np.random.default_rng(3)
+            for _ in range(3):
+                x, y = rng.standard_normal(prog.n) * 2, rng.standard_normal(prog.m) * 2
+                g.set_iterate(x, y)
+                o.set_iterate(x * qo, y * ro)
+                g.iterate(1)
+                o.iterate(1)
+                assert parity(*g.get_iterate(P.PDHG_OUT), *o.get_iterate(1)) <= 1e-12
+        g.close()
+    assert parity(*runs["1"], *runs["0"]) <= 1e-10
+
+
 def test_cfg5_recipe_parity(P):
     """SURVEY §8(d) cfg 5 recipe (row lengths 20..180, values over 8 decades,
     all six cone kinds, log-uniform SOC dims up to 4096 -> thread/warp/CTA

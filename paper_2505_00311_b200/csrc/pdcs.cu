@@ -774,14 +774,15 @@ struct TiledDevArrays {
 };
 
 template <class F>
-void parallel_chunks(int64_t n, const F& f) {
+void parallel_chunks(int64_t n, const F& f, int64_t grain_max = -1) {
   int nth = (int)std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()), 32,
                                     std::max<int64_t>(1, n / 8)});
   if (const char* e = std::getenv("PDCS_BUILD_THREADS")) nth = std::max(1, std::atoi(e));
   if (nth <= 1) { f((int64_t)0, n); return; }
   // dynamic: chunks differ widely in work (Lasso K^T: 20 of ~1000 hold half the entries)
   std::atomic<int64_t> next{0};
-  const int64_t grain = std::max<int64_t>(1, n / (nth * 16));
+  int64_t grain = std::max<int64_t>(1, n / (nth * 16));
+  if (grain_max > 0) grain = std::min(grain, grain_max);
   std::vector<std::thread> th;
   for (int w = 0; w < nth; ++w)
     th.emplace_back([&] {
@@ -1180,19 +1181,19 @@ void validate_csr(const int64_t* ptr, const int32_t* col, const double* val, int
 // keep their places.  Returns false (identity) otherwise.
 constexpr int64_t kPermLongRow = 1024;
 
-int64_t long_row_sectors(const int64_t* ptr, const int32_t* col, int64_t m, const int32_t* u2i) {
+int64_t long_row_sectors(const int64_t* ptr, const int32_t* col, int64_t m, int64_t n, const int32_t* u2i) {
+  // distinct 2-column sectors per long row, by marking (no sort: Fisher's 1000
+  // rows of 1e4 mapped ids had taken ~0.2 s sorted)
   int64_t total = 0;
-  std::vector<int32_t> buf;
+  std::vector<uint8_t> mark((size_t)(n >> 1) + 1, 0);
   for (int64_t i = 0; i < m; ++i) {
     const int64_t a = ptr[i], b = ptr[i + 1];
     if (b - a < kPermLongRow) continue;
-    buf.resize(b - a);
-    for (int64_t q = a; q < b; ++q) buf[q - a] = u2i ? u2i[col[q]] : col[q];
-    if (u2i) std::sort(buf.begin(), buf.end());
-    int64_t cnt = 0, last = -1;
-    for (int32_t c : buf)
-      if ((c >> 1) != last) { ++cnt; last = c >> 1; }
-    total += cnt;
+    for (int64_t q = a; q < b; ++q) {
+      const int64_t sct = (u2i ? u2i[col[q]] : col[q]) >> 1;
+      if (!mark[sct]) { mark[sct] = 1; ++total; }
+    }
+    for (int64_t q = a; q < b; ++q) mark[(u2i ? u2i[col[q]] : col[q]) >> 1] = 0;
   }
   return total;
 }
@@ -1206,7 +1207,7 @@ bool plan_colperm(const int64_t* ptr, const int32_t* col, int64_t m, int64_t n, 
   int64_t nlong = 0;
   for (int64_t i = 0; i < m; ++i) nlong += ptr[i + 1] - ptr[i] >= kPermLongRow;
   if (nlong == 0 || nlong >= 16 * (int64_t)sms) return false;
-  const int64_t before = long_row_sectors(ptr, col, m, nullptr);
+  const int64_t before = long_row_sectors(ptr, col, m, n, nullptr);
   if (before == 0) return false;
   std::vector<int64_t> best(n1, -1), blen(n1, -1);
   for (int64_t i = 0; i < m; ++i) {
@@ -1216,14 +1217,20 @@ bool plan_colperm(const int64_t* ptr, const int32_t* col, int64_t m, int64_t n, 
       if (j < n1 && len > blen[j]) { blen[j] = len; best[j] = i; }
     }
   }
+  // stable order by the holding row: a counting sort over best in [-1, m)
+  // (std::stable_sort of Fisher's 1e7 box columns had taken ~1 s)
   std::vector<int32_t> order(n1);
-  for (int64_t j = 0; j < n1; ++j) order[j] = (int32_t)j;
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return best[a] < best[b]; });
+  {
+    std::vector<int64_t> start((size_t)m + 2, 0);
+    for (int64_t j = 0; j < n1; ++j) ++start[(size_t)(best[j] + 1) + 1];
+    for (size_t z = 1; z < start.size(); ++z) start[z] += start[z - 1];
+    for (int64_t j = 0; j < n1; ++j) order[start[(size_t)(best[j] + 1)]++] = (int32_t)j;
+  }
   i2u.resize(n);
   u2i.resize(n);
   for (int64_t k = 0; k < n; ++k) i2u[k] = k < n1 ? order[k] : (int32_t)k;
   for (int64_t k = 0; k < n; ++k) u2i[i2u[k]] = (int32_t)k;
-  const int64_t after = long_row_sectors(ptr, col, m, u2i.data());
+  const int64_t after = long_row_sectors(ptr, col, m, n, u2i.data());
   if ((double)after > 0.8 * (double)before) { u2i.clear(); i2u.clear(); return false; }
   return true;
 }
@@ -1234,20 +1241,19 @@ void permute_csr(const int64_t* ptr, const int32_t* col, const double* val, int6
   const int64_t nnz = ptr[m];
   pcol.resize(nnz);
   pval.resize(nnz);
-  const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(16, nnz / 2000000 + 1));
-  std::vector<std::thread> th;
-  for (int w = 0; w < nth; ++w)
-    th.emplace_back([&, w] {
-      std::vector<std::pair<int32_t, double>> buf;
-      for (int64_t i = m * w / nth; i < m * (w + 1) / nth; ++i) {
-        const int64_t a = ptr[i], b = ptr[i + 1];
-        buf.resize(b - a);
-        for (int64_t q = a; q < b; ++q) buf[q - a] = {u2i[col[q]], val[q]};
-        std::sort(buf.begin(), buf.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
-        for (int64_t q = a; q < b; ++q) { pcol[q] = buf[q - a].first; pval[q] = buf[q - a].second; }
-      }
-    });
-  for (auto& t : th) t.join();
+  // rows handed out dynamically: Fisher's 1000 long supply rows (1e7 of its
+  // 1.2e7 entries) are its first rows and had all fallen to one thread (~0.9 s)
+  parallel_chunks(m, [&](int64_t ra, int64_t rb) {
+    std::vector<std::pair<int32_t, double>> buf;
+    for (int64_t i = ra; i < rb; ++i) {
+      const int64_t a = ptr[i], b = ptr[i + 1];
+      buf.resize(b - a);
+      for (int64_t q = a; q < b; ++q) buf[q - a] = {u2i[col[q]], val[q]};
+      std::sort(buf.begin(), buf.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (int64_t q = a; q < b; ++q) { pcol[q] = buf[q - a].first; pval[q] = buf[q - a].second; }
+    }
+  }, 8);
+  (void)nnz;
 }
 
 // Size class of each cone block: 0 thread, 1 warp, 2 CTA,
@@ -2325,27 +2331,35 @@ struct pdcs_ctx {
         fixed_bins = true;
       }
     }
-    std::vector<int64_t> lists[kMaxClasses];
+    // class of every row (one byte each), then per class its count and row
+    // range; row lists are materialised only for classes whose rows are not
+    // contiguous (Fisher's K^T: 1e7 rows, one class, had been pushed into a
+    // 1e7-entry list: ~0.14 s)
+    std::vector<uint8_t> cls_of((size_t)std::max<int64_t>(rows - row_a, 0));
+    int64_t nlong = 0;
     for (int64_t i = row_a; i < rows; ++i) {
       const int64_t L = ptr[i + 1] - ptr[i];
       int c = 5;
       for (int k = 0; k < 5; ++k)
         if (L <= bound[k]) { c = k; break; }
-      lists[c].push_back(i);
+      cls_of[i - row_a] = (uint8_t)c;
+      nlong += c == 4 && L > 1024;
     }
     // Few very long rows (> 1024 nnz; fewer than 16 per SM): one warp per row
     // leaves the SMs idle while each warp walks a long serial chain of gathers
     // (Fisher's 1000 supply rows of 1e4 nnz), so they get a CTA each.  With
     // many of them (Lasso K^T: 1e4 rows) warp-per-row is faster
     // (profiles/r1_sweep_v0.txt).
-    if (!fixed_bins) {
-      int64_t nlong = 0;
-      for (int64_t r_ : lists[4]) nlong += ptr[r_ + 1] - ptr[r_] > 1024;
-      if (nlong && nlong < (int64_t)sms * 16) {
-        std::vector<int64_t> keep;
-        for (int64_t r_ : lists[4]) (ptr[r_ + 1] - ptr[r_] > 1024 ? lists[5] : keep).push_back(r_);
-        lists[4].swap(keep);
-      }
+    if (!fixed_bins && nlong && nlong < (int64_t)sms * 16)
+      for (int64_t i = row_a; i < rows; ++i)
+        if (cls_of[i - row_a] == 4 && ptr[i + 1] - ptr[i] > 1024) cls_of[i - row_a] = 5;
+    int64_t ccount[kMaxClasses] = {0}, cfirst[kMaxClasses], clast[kMaxClasses];
+    for (int c = 0; c < kMaxClasses; ++c) { cfirst[c] = -1; clast[c] = -1; }
+    for (int64_t i = row_a; i < rows; ++i) {
+      const int c = cls_of[i - row_a];
+      if (cfirst[c] < 0) cfirst[c] = i;
+      clast[c] = i;
+      ++ccount[c];
     }
     SpmvPlan P{};
     P.ncls = 0;
@@ -2357,16 +2371,17 @@ struct pdcs_ctx {
     static const int order[kMaxClasses] = {5, 0, 1, 2, 3, 4};
     for (int oc = 0; oc < kMaxClasses; ++oc) {
       const int c = order[oc];
-      if (lists[c].empty()) continue;
+      if (ccount[c] == 0) continue;
       SpmvClass& K_ = P.cls[P.ncls++];
       K_.V = Vs[c];
-      K_.nrows = (int64_t)lists[c].size();
-      const bool contiguous = lists[c].back() - lists[c].front() + 1 == K_.nrows;
-      K_.range_begin = contiguous ? lists[c].front() : 0;
+      K_.nrows = ccount[c];
+      const bool contiguous = clast[c] - cfirst[c] + 1 == K_.nrows;
+      K_.range_begin = contiguous ? cfirst[c] : 0;
       K_.rows = nullptr;
       if (!contiguous) {
         offs.push_back(rowstore.size());
-        for (int64_t r_ : lists[c]) rowstore.push_back((int32_t)r_);
+        for (int64_t i = cfirst[c]; i <= clast[c]; ++i)
+          if (cls_of[i - row_a] == c) rowstore.push_back((int32_t)i);
         K_.rows = (const int32_t*)(uintptr_t)(offs.back() + 1);   // patched after upload
       }
       int64_t rows_per_cta = K_.V == 0 ? 1 : K_.V == 1 ? kThreads : kThreads / K_.V;

@@ -1209,13 +1209,26 @@ bool plan_colperm(const int64_t* ptr, const int32_t* col, int64_t m, int64_t n, 
   if (nlong == 0 || nlong >= 16 * (int64_t)sms) return false;
   const int64_t before = long_row_sectors(ptr, col, m, n, nullptr);
   if (before == 0) return false;
+  // best[j]: the longest row holding box column j (the first such row on
+  // ties).  Host threads own column ranges and each scans all rows in order
+  // (same result as one pass; the random writes stay in a thread's range)
   std::vector<int64_t> best(n1, -1), blen(n1, -1);
-  for (int64_t i = 0; i < m; ++i) {
-    const int64_t len = ptr[i + 1] - ptr[i];
-    for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q) {
-      const int32_t j = col[q];
-      if (j < n1 && len > blen[j]) { blen[j] = len; best[j] = i; }
-    }
+  {
+    int nth = (int)std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()), 16,
+                                      std::max<int64_t>(1, n1 / 65536)});
+    std::vector<std::thread> th;
+    for (int w = 0; w < nth; ++w)
+      th.emplace_back([&, w] {
+        const int64_t j0 = n1 * w / nth, j1 = n1 * (w + 1) / nth;
+        for (int64_t i = 0; i < m; ++i) {
+          const int64_t len = ptr[i + 1] - ptr[i];
+          for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q) {
+            const int64_t j = col[q];
+            if (j >= j0 && j < j1 && len > blen[j]) { blen[j] = len; best[j] = i; }
+          }
+        }
+      });
+    for (auto& t : th) t.join();
   }
   // stable order by the holding row: a counting sort over best in [-1, m)
   // (std::stable_sort of Fisher's 1e7 box columns had taken ~1 s)
@@ -2432,11 +2445,11 @@ pdcs_status guard(pdcs_ctx* ctx, const std::function<void()>& f) {
 
 template <class T>
 std::vector<T> to_host(const T* p, int64_t count, int mem_kind) {
-  std::vector<T> v((size_t)std::max<int64_t>(count, 0));
-  if (count <= 0) return v;
+  if (count <= 0) return std::vector<T>();
   if (!p) fail(PDCS_ERR_ARG, "null input pointer");
-  if (mem_kind == PDCS_MEM_DEVICE) CK(cudaMemcpy(v.data(), p, count * sizeof(T), cudaMemcpyDeviceToHost));
-  else std::memcpy(v.data(), p, count * sizeof(T));
+  if (mem_kind != PDCS_MEM_DEVICE) return std::vector<T>(p, p + count);   // one pass, no zero-fill first
+  std::vector<T> v((size_t)count);
+  CK(cudaMemcpy(v.data(), p, count * sizeof(T), cudaMemcpyDeviceToHost));
   return v;
 }
 
@@ -2588,8 +2601,11 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     {
       const char* e = std::getenv("PDCS_COLPERM");
       const bool allow = (e ? std::atoi(e) != 0 : true) && !ctx->dist;
-      if (allow && plan_colperm(ctx->hptr.data(), hcolp, m, n, n1, ctx->sms, ctx->u2i, ctx->i2u)) {
+      const bool cp = allow && plan_colperm(ctx->hptr.data(), hcolp, m, n, n1, ctx->sms, ctx->u2i, ctx->i2u);
+      tr.mark("  colperm plan", nullptr, false);
+      if (cp) {
         permute_csr(ctx->hptr.data(), hcolp, hvalp, m, ctx->u2i, pcol, pval);
+        tr.mark("  colperm: permute CSR", nullptr, false);
         hcolp = pcol.data();
         hvalp = pval.data();
         ctx->colperm = true;
@@ -2611,15 +2627,19 @@ static pdcs_status create_impl(pdcs_ctx** out, int64_t m_global, int64_t n, int6
     std::vector<double> hc = to_host(c, n, mem_kind), hh = to_host(h, m, mem_kind);
     ctx->hl = to_host(l, n1, mem_kind);
     ctx->hu = to_host(u, n1, mem_kind);
+    tr.mark("  c, h, l, u to host", nullptr, false);
     if (ctx->colperm) {                           // c, l, u in the stored column order
-      auto perm = [&](std::vector<double>& v, int64_t cnt) {
+      auto perm = [&](std::vector<double>& v, int64_t cnt) {   // random gathers: on host threads
         std::vector<double> o(cnt);
-        for (int64_t k = 0; k < cnt; ++k) o[k] = v[ctx->i2u[k]];
+        parallel_chunks(cnt, [&](int64_t a, int64_t b) {
+          for (int64_t k = a; k < b; ++k) o[k] = v[ctx->i2u[k]];
+        });
         v.swap(o);
       };
       perm(hc, n);
       perm(ctx->hl, n1);
       perm(ctx->hu, n1);
+      tr.mark("  c, l, u permuted", nullptr, false);
     }
     for (double v : hc) if (!std::isfinite(v)) fail(PDCS_ERR_NONFINITE, "non-finite c");
     for (double v : hh) if (!std::isfinite(v)) fail(PDCS_ERR_NONFINITE, "non-finite h");

@@ -249,7 +249,8 @@ void pdcs_enable_timing(pdcs_ctx *ctx, int on);
  * §7.7): number of panels kept (0 = CSR / tiled sweep) and the autotune ms of
  * the CSR and the panelled sweep, for K~ then K~^T, then the fused combine
  * of the tiled sweeps: kept (0/1) and its autotune ms, for
- * K~ then K~^T.  Returns the number of values written (<= 47). */
+ * K~ then K~^T, then the CSR kernel's entries in flight per lane (8 or 4)
+ * for K~ and K~^T.  Returns the number of values written (<= 49). */
 int pdcs_get_scalars(pdcs_ctx *ctx, double *out, int cap);
 
 /* Number of kernel launches issued by the last pdcs_iterate call. */

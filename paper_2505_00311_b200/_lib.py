@@ -141,7 +141,7 @@ SCALAR_KEYS = ["eta", "omega", "beta", "k", "total", "trials", "restarts", "e_an
                "tune_KT_tiled_ms", "tiled_K_build_ms", "tiled_KT_build_ms", "setup_create_ms",
                "setup_cones_ms", "colperm", "panels_K", "tune_K_csr_ms_p", "tune_K_panel_ms", "panels_KT",
                "tune_KT_csr_ms_p", "tune_KT_panel_ms", "fused_K", "tune_K_fused_ms", "fused_KT",
-               "tune_KT_fused_ms"]
+               "tune_KT_fused_ms", "csr_u_K", "csr_u_KT"]
 
 
 def _check(code, ctx=None):

@@ -63,6 +63,7 @@ struct DevCsr {
   int32_t* col = nullptr;
   double* val = nullptr;
   SpmvPlan plan{};
+  int csr_u = 8;          // entries in flight per lane of the CSR kernel (8 or 4, setup autotune)
 };
 
 // Solver control block, device resident (all scalars of Alg. 1).

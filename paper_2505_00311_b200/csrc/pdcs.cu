@@ -1518,9 +1518,62 @@ struct pdcs_ctx {
     if (&A == &KT && pKT.on) { psweep(name, pKT, x1, x2, epi, part, slot0); return; }
     if (A.plan.total_cta == 0) return;
     launch(name, [&] {
-      spmv_kernel<Epi><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, x1, x2, A.plan, epi, ctl,
-                                                              part, slot0);
+      if (A.csr_u == 4)
+        spmv_kernel<Epi, 4><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, x1, x2, A.plan, epi, ctl,
+                                                                   part, slot0);
+      else
+        spmv_kernel<Epi><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, x1, x2, A.plan, epi, ctl,
+                                                                part, slot0);
     });
+  }
+  // Setup autotune of the CSR kernel's loads in flight per lane (8 or 4) for a
+  // matrix whose sweep stays on the CSR path; 4 only if >= 3% faster.
+  void tune_csr_u(DevCsr& A, int64_t nvec) {
+    A.csr_u = 8;
+    // PDCS_CSR_U4 = K | KT | both | 0: force 4 in flight for that sweep (else 8)
+    if (const char* e = std::getenv("PDCS_CSR_U4")) {
+      const std::string v(e);
+      const bool isK = &A == &K;
+      A.csr_u = (v == "both" || (v == "K" && isK) || (v == "KT" && !isK)) ? 4 : 8;
+      return;
+    }
+    // only where the sweep is long enough to time (>= 1e7 entries): small
+    // instances keep 8, and with them every bit-for-bit comparison between
+    // two contexts of the tests
+    if (A.plan.total_cta == 0 || A.nnz < 10000000) return;
+    DBuf<double> xin, out;
+    xin.alloc(std::max<int64_t>(nvec, 1));
+    out.alloc(std::max<int64_t>(A.m, 1));
+    k_fill<<<grid_for(std::max<int64_t>(nvec, 1), sms), kThreads, 0, st>>>(std::max<int64_t>(nvec, 1), 1.0, xin.p);
+    EpiStore es{out.p};
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    auto timeit = [&](int u) {
+      auto f = [&] {
+        if (u == 4) spmv_kernel<EpiStore, 4><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, xin.p, nullptr,
+                                                                                      A.plan, es, ctl, nullptr, 0);
+        else spmv_kernel<EpiStore><<<A.plan.total_cta, kThreads, 0, st>>>(A.ptr, A.col, A.val, xin.p, nullptr, A.plan,
+                                                                          es, ctl, nullptr, 0);
+      };
+      f();
+      f();
+      float v[5];
+      for (int i = 0; i < 5; ++i) {
+        CK(cudaEventRecord(a, st));
+        f();
+        CK(cudaEventRecord(b, st));
+        CK(cudaEventSynchronize(b));
+        CK(cudaEventElapsedTime(&v[i], a, b));
+      }
+      std::sort(v, v + 5);
+      return v[2];
+    };
+    const float t8 = timeit(8), t4 = timeit(4);
+    CK(cudaGetLastError());
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (t4 < 0.97f * t8) A.csr_u = 4;
   }
   // A sweep through the L2 panels: one accumulating pass per panel, then the
   // sweep's epilogue over the accumulated rows (panels.cuh).
@@ -3047,6 +3100,8 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
     tr.mark("tiled K^T (device part)", st);
     ctx->build_panels(ctx->pK, ctx->K, ctx->tK.on, 1);
     ctx->build_panels(ctx->pKT, ctx->KT, ctx->tKT.on, 1);
+    if (!ctx->tK.on && !ctx->pK.on) ctx->tune_csr_u(ctx->K, n);
+    if (!ctx->tKT.on && !ctx->pKT.on) ctx->tune_csr_u(ctx->KT, m);
     tr.mark("panels", st);
     // scaled data (reading A2): c~ = c/q, h~ = h/r, l~ = q l, u~ = q u
     k_ewise<<<Gn, kThreads, 0, st>>>(n, ctx->c0.p, ctx->q.p, 0, ctx->ct.p);
@@ -3452,7 +3507,7 @@ int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
   if (!ctx || !out || !ctx->ctl) return 0;
   if (guard(ctx, [&] { ctx->read_ctl(); }) != PDCS_OK) return 0;
   const Ctl& C = *ctx->hctl;
-  double v[47] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
+  double v[49] = {C.eta, C.omega, C.beta, (double)C.k, (double)C.total, (double)C.trials,
                   (double)C.restarts, C.e_anchor, C.Wsum, C.eta_init,
                   C.kkt[0][0], C.kkt[0][1], C.kkt[0][2], C.kkt[0][3], C.kkt[0][4],
                   C.kkt[1][0], C.kkt[1][1], C.kkt[1][2], C.kkt[1][3], C.kkt[1][4],
@@ -3463,8 +3518,9 @@ int pdcs_get_scalars(pdcs_ctx* ctx, double* out, int cap) {
                   (double)ctx->colperm, (double)(ctx->pK.on ? ctx->pK.P : 0), ctx->pK.tune_csr_ms,
                   ctx->pK.tune_panel_ms, (double)(ctx->pKT.on ? ctx->pKT.P : 0), ctx->pKT.tune_csr_ms,
                   ctx->pKT.tune_panel_ms, (double)pdcs_ctx::fused(ctx->tK), ctx->tK.tune_fused_ms,
-                  (double)pdcs_ctx::fused(ctx->tKT), ctx->tKT.tune_fused_ms};
-  const int k = std::min(cap, 47);
+                  (double)pdcs_ctx::fused(ctx->tKT), ctx->tKT.tune_fused_ms, (double)ctx->K.csr_u,
+                  (double)ctx->KT.csr_u};
+  const int k = std::min(cap, 49);
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }

@@ -69,12 +69,12 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
 #ifndef PDCS_CSR_U
 #define PDCS_CSR_U 8                  // entries in flight per lane, V >= 8 (B200: 4 -> 8 with the 64-register cap, MPO +13%, mixed +7%)
 #endif
-template <int V, int NX>
+template <int V, int NX, int UU = PDCS_CSR_U>
 __device__ __forceinline__ void row_dot(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                                         const double* __restrict__ val, const double* __restrict__ x1,
                                         const double* __restrict__ x2, int64_t row, int lane, double& s1,
                                         double& s2) {
-  constexpr int U = (V >= 8 && V <= 32) ? PDCS_CSR_U : 4;   // entries in flight per lane
+  constexpr int U = (V >= 8 && V <= 32) ? UU : 4;   // entries in flight per lane
   s1 = 0.0;
   s2 = 0.0;
   if (row >= 0) {
@@ -132,7 +132,10 @@ __device__ __forceinline__ void row_dot(const int32_t* __restrict__ ptr, const i
 #ifndef PDCS_CSR_MINB
 #define PDCS_CSR_MINB 4               // 64 registers: 4 CTAs of 256 threads per SM
 #endif
-template <class Epi>
+// UU: entries in flight per lane for the V >= 8 classes (a per-matrix setup
+// choice between 8 and 4: MPO's K sweep 227.6 -> 216.1 us with 4, its K^T
+// sweep slower with 4).
+template <class Epi, int UU = PDCS_CSR_U>
 __global__ void __launch_bounds__(kThreads, PDCS_CSR_MINB) spmv_kernel(const int32_t* __restrict__ ptr,
                                                         const int32_t* __restrict__ col,
                                                         const double* __restrict__ val,
@@ -235,9 +238,9 @@ __global__ void __launch_bounds__(kThreads, PDCS_CSR_MINB) spmv_kernel(const int
       const int64_t row = idx < K.nrows ? rowid(idx) : -1;
       double s1, s2;
       switch (V) {
-        case 8: row_dot<8, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
-        case 16: row_dot<16, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
-        default: row_dot<32, NX>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
+        case 8: row_dot<8, NX, UU>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
+        case 16: row_dot<16, NX, UU>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
+        default: row_dot<32, NX, UU>(ptr, col, val, x1, x2, row, lane, s1, s2); break;
       }
       if (lane == 0 && row >= 0) epi.row(row, s1, s2, acc);
     }

@@ -66,7 +66,10 @@ constexpr int kCombLanes = 8;
 constexpr int kCombRowsWide = 256 / kCombLanes;
 constexpr int kCombWideG = 16;
 constexpr int kCombRowsNarrow = 4 * 256;   // rows of an item of a chunk with <= kCombNarrowG groups
-constexpr int kCombNarrowG = 2;   // 4 measured slower on Lasso K (3 groups, 80 registers): 26.6 -> 29.2 us
+#ifndef PDCS_COMB_NARROW
+#define PDCS_COMB_NARROW 2
+#endif
+constexpr int kCombNarrowG = PDCS_COMB_NARROW;   // 4 measured slower on Lasso K with pairs (3 groups, 80 registers): 26.6 -> 29.2 us
 struct TWork {
   int32_t chunk, group, s0, s1;   // segments [s0, s1): direct ones run first, staged via batches
   int32_t b0, b1;                 // TMA batches [b0, b1) of the staged segments

@@ -336,7 +336,10 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
 // All CTAs on one block at a time (giant SOC/RSOC; cooperative launch).
 constexpr size_t kGridSmem = 2 * kGridCache * kThreads * sizeof(double);   // 32 KB
 template <int OP>
-__global__ void __launch_bounds__(kThreads) k_blocks_grid(BlockArgs A, const Ctl* ctl, double* gbuf) {
+#ifndef PDCS_GRID_MINB
+#define PDCS_GRID_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, PDCS_GRID_MINB) k_blocks_grid(BlockArgs A, const Ctl* ctl, double* gbuf) {
   if (!block_op_active<OP>(A, ctl)) return;
   __shared__ double sm[2 * (kThreads / 32) + 2];
   Acc<kAcc> acc; acc.zero();

@@ -2948,6 +2948,9 @@ pdcs_status pdcs_set_cones(pdcs_ctx* ctx, const int32_t* pk, const int64_t* pdim
         else {
           int nb = 0;
           CK(grid_team_occupancy(&nb));
+          // PDCS_GRID_CTAS (per SM) lowers the grid team's size: fewer CTAs
+          // to synchronise per reduction, more elements per thread
+          if (const char* e = std::getenv("PDCS_GRID_CTAS")) nb = std::min(nb, std::max(1, std::atoi(e)));
           cl[c].grid = std::max(1, std::min(nb, 4)) * ctx->sms;
         }
       }

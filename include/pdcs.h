@@ -350,6 +350,12 @@ pdcs_status pdcs_nccl_unique_id(void *out128);
  * (PDCS_POOL=0: plain cudaMalloc / cudaFree).  Buffers are allocated at
  * create / set_cones time only, never per iteration.
  * Errors: ARG (one function NULL, the other not). */
+/* Return the default pool's unused device memory (buffers of destroyed
+ * contexts, setup scratch) to the driver; memory of live contexts stays.
+ * Process-wide.  Returns the bytes released, -1 on a CUDA error.  The next
+ * context then maps its memory afresh (slower setup). */
+int64_t pdcs_trim_memory(void);
+
 typedef void *(*pdcs_alloc_fn)(size_t bytes, void *user);
 typedef void (*pdcs_free_fn)(void *ptr, void *user);
 pdcs_status pdcs_set_allocator(pdcs_alloc_fn alloc, pdcs_free_fn free_fn, void *user);

@@ -9,7 +9,7 @@ from ._lib import (pdcs_default_params, pdcs_create, pdcs_set_cones, pdcs_iterat
                    pdcs_kernel_times, pdcs_enable_timing, pdcs_launch_count, pdcs_last_error,
                    pdcs_destroy, pdcs_nccl_unique_id, pdcs_get_scalars, pdcs_get_state, pdcs_set_state, pdcs_tiled_layout_stats, pdcs_proj_create, pdcs_proj_run, pdcs_proj_info,
                    pdcs_proj_destroy, pdcs_set_tolerance, pdcs_tiled_build_host, pdcs_loopback_create,
-                   pdcs_loopback_destroy, pdcs_create_loopback, pdcs_tiled_device_check, pdcs_tiled_devbuild_check, pdcs_set_allocator, PdcsError, LIB_PATH, CURRENT, PDHG_OUT,
+                   pdcs_loopback_destroy, pdcs_create_loopback, pdcs_tiled_device_check, pdcs_tiled_devbuild_check, pdcs_set_allocator, pdcs_trim_memory, PdcsError, LIB_PATH, CURRENT, PDHG_OUT,
                    ANCHOR, BEST, CANDIDATE, SCALED, ORIGINAL)
 from .solver import PdcsSolver
 
@@ -18,5 +18,5 @@ __all__ = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterate
            "pdcs_kernel_times", "pdcs_enable_timing", "pdcs_launch_count", "pdcs_last_error",
            "pdcs_destroy", "pdcs_nccl_unique_id", "pdcs_get_scalars", "pdcs_get_state", "pdcs_set_state", "pdcs_tiled_layout_stats", "pdcs_proj_create", "pdcs_proj_run", "pdcs_proj_info",
            "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host", "pdcs_loopback_create",
-           "pdcs_loopback_destroy", "pdcs_create_loopback", "pdcs_tiled_device_check", "pdcs_tiled_devbuild_check", "pdcs_set_allocator", "PdcsError", "PdcsSolver", "LIB_PATH",
+           "pdcs_loopback_destroy", "pdcs_create_loopback", "pdcs_tiled_device_check", "pdcs_tiled_devbuild_check", "pdcs_set_allocator", "pdcs_trim_memory", "PdcsError", "PdcsSolver", "LIB_PATH",
            "CURRENT", "PDHG_OUT", "ANCHOR", "BEST", "CANDIDATE", "SCALED", "ORIGINAL"]

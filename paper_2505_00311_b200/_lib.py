@@ -83,6 +83,8 @@ def lib():
                                            C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(pdcs_params),
                                            C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int]
         L.pdcs_set_allocator.argtypes = [ALLOC_FN, FREE_FN, C.c_void_p]
+        L.pdcs_trim_memory.argtypes = []
+        L.pdcs_trim_memory.restype = C.c_int64
         L.pdcs_loopback_create.argtypes = [C.POINTER(C.c_void_p), C.c_int]
         L.pdcs_loopback_destroy.argtypes = [C.c_void_p]
         L.pdcs_set_cones.argtypes = [C.c_void_p, P_I32, P_I64, C.c_int64, P_I32, P_I64, C.c_int64]
@@ -128,7 +130,7 @@ EXPORTED = ["pdcs_default_params", "pdcs_create", "pdcs_set_cones", "pdcs_iterat
             "pdcs_proj_info", "pdcs_proj_destroy", "pdcs_set_tolerance", "pdcs_tiled_build_host",
             "pdcs_loopback_create", "pdcs_loopback_destroy", "pdcs_create_loopback", "pdcs_tiled_device_check",
             "pdcs_tiled_devbuild_check",
-            "pdcs_set_allocator"]
+            "pdcs_set_allocator", "pdcs_trim_memory"]
 
 STATE_KEYS = ["eta", "eta_init", "omega", "beta", "W", "r_start", "e_anchor", "e_prev", "best_e", "k",
               "total", "trials", "restarts"]
@@ -197,6 +199,14 @@ def pdcs_create_loopback(m_global, n, n1, row_begin, row_end, row_ptr, col_idx, 
 
 
 _allocator_refs = None
+
+
+def pdcs_trim_memory() -> int:
+    """Release the library pool's unused device memory; returns the bytes released."""
+    k = lib().pdcs_trim_memory()
+    if k < 0:
+        raise PdcsError(7, "pdcs_trim_memory failed")
+    return int(k)
 
 
 def pdcs_set_allocator(alloc=None, free=None):

@@ -2847,6 +2847,21 @@ pdcs_status pdcs_set_allocator(pdcs_alloc_fn alloc, pdcs_free_fn free_fn, void* 
   return PDCS_OK;
 }
 
+int64_t pdcs_trim_memory(void) {
+  int64_t released = 0;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (int d = 0; d < 64; ++d) {
+    DevPool& P = g_pool[d];
+    if (!P.pool) continue;
+    uint64_t before = 0, after = 0;
+    cudaMemPoolGetAttribute(P.pool, cudaMemPoolAttrReservedMemCurrent, &before);
+    if (cudaMemPoolTrimTo(P.pool, 0) != cudaSuccess) return -1;
+    cudaMemPoolGetAttribute(P.pool, cudaMemPoolAttrReservedMemCurrent, &after);
+    released += (int64_t)(before - after);
+  }
+  return released;
+}
+
 pdcs_status pdcs_loopback_create(pdcs_loopback** out, int world) {
   if (!out || world < 1 || world > kLoopMaxRanks) {
     g_create_error = "loopback world must be 1..16";

@@ -436,6 +436,12 @@ def test_memory_pool_reuse_gives_the_same_bits(P):
             if ref is None:
                 ref = xy
             assert np.array_equal(ref[0], xy[0]) and np.array_equal(ref[1], xy[1])
+        assert P.pdcs_trim_memory() > 0            # every context is gone: their memory goes back
+        g = P.PdcsSolver(prog)                     # and a context after the trim still gives the bits
+        g.iterate(50)
+        xy = g.get_iterate(P.CURRENT)
+        g.close()
+        assert np.array_equal(ref[0], xy[0]) and np.array_equal(ref[1], xy[1])
     finally:
         del os.environ["PDCS_TILED"]
 

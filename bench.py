@@ -185,6 +185,23 @@ def pinned(prog, rows):
                 l=pin(prog.l, np.float64), u=pin(prog.u, np.float64))
 
 
+def literal_form_kkt(P, prog, xb, yb, stream, device):
+    """Lasso (reading P9): the solve ran on the balanced SOCP; its best point,
+    mapped back by w = w'/S, r = S r', is scored by Eq. 9 OF THE LITERAL FORM
+    (PAPER.md:1641-1659 as printed) -- in a second library context, on the GPU."""
+    lit = prog.literal()
+    host = pinned(lit, (0, lit.m))
+    ctx = make_ctx(P, lit, host, P.pdcs_default_params(), stream, device, (0, lit.m))
+    x = torch.from_numpy(prog.to_literal(xb.numpy()))
+    P.pdcs_set_iterate(ctx, x, yb)
+    k = P.pdcs_kkt(ctx, P.CURRENT)
+    P.pdcs_destroy(ctx)
+    return {"S": prog.lasso_S, "err_p": k.err_p, "err_d": k.err_d, "err_gap": k.err_gap,
+            "kkt_max": max(k.err_p, k.err_d, k.err_gap), "pobj": k.pobj,
+            "note": "best point of the balanced solve mapped to the literal SOCP (w = w'/S, r = S r'), "
+                    "Eq. 9 of the literal form"}
+
+
 def make_ctx(P, prog, host, params, stream, device, rows, uid=None, rank=0, world=1):
     idbuf = None if uid is None else np.frombuffer(uid, dtype=np.uint8).copy()
     ctx = P.pdcs_create(prog.m, prog.n, prog.n1, rows[0], rows[1], host["row_ptr"], host["col"],
@@ -460,10 +477,17 @@ def main():
         r = P.pdcs_solve(ctx)
         torch.cuda.synchronize()
         t_all = time.perf_counter() - t0
+        xb = yb = None
+        if hasattr(prog, "literal") and world == 1:
+            xb = torch.empty(prog.n, dtype=torch.float64)
+            yb = torch.empty(prog.m, dtype=torch.float64)
+            P.pdcs_get_iterate(ctx, P.BEST, P.ORIGINAL, xb, yb)
         P.pdcs_destroy(ctx)
         tol_run = {"tol": 1e-4, "status": r.status, "seconds_incl_setup": t_all,
                    "seconds_solve": r.solve_seconds, "setup_seconds": t_setup, "iters": r.iters,
                    "kkt_max": max(r.kkt.err_p, r.kkt.err_d, r.kkt.err_gap), "restarts": r.restarts}
+        if xb is not None:
+            tol_run["literal_form"] = literal_form_kkt(P, prog, xb, yb, sh, local)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -55,7 +55,7 @@ def bernoulli_positions(rng: np.random.Generator, total: int, p: float) -> np.nd
 # Lasso as SOCP (variables ordered (x+, x-, w, r, y), A22)
 # --------------------------------------------------------------------------
 def gen_lasso(m: int, nfeat: int, density: float, seed: int = 0,
-              dense: bool = False) -> ConicProgram:
+              dense: bool = False, balance: bool = True) -> ConicProgram:
     """min ||A x - b||^2 + lam ||x||_1 as the conic program of PAPER.md:1641-1659.
 
     Variables x = (x+ [nfeat], x- [nfeat] | w, r, y [m]); n1 = 2 nfeat with
@@ -64,6 +64,14 @@ def gen_lasso(m: int, nfeat: int, density: float, seed: int = 0,
     y - A x+ + A x- = -b (all Zero cones).  Data recipe PAPER.md:1663-1664:
     A_ij ~ U[0,1] at the given density, x~ ~ N(0,1) with half zeroed,
     b = A x~ + 1e-6, lam = ||A^T b||_inf.
+
+    balance (reading P9): the RSOC's leading pair is stored as
+    (w', r') = (S w, r / S), S = max(1, ||b||^2 / 2) -- the value of r at
+    x = 0 -- an automorphism of the rotated cone (2 w' r' = 2 w r), so the
+    row w = 1 reads w' / S = 1 and r' costs 2 S.  Same problem, same optimal
+    value; a solution maps back by w = w' / S, r = S r' (y unchanged:
+    `prog.to_literal(x)`).  balance=False gives the literal form, on which
+    PDCS with the SPEC's heuristics stalls (P8).
     """
     rng = _rng(seed)
     if dense:
@@ -90,7 +98,8 @@ def gen_lasso(m: int, nfeat: int, density: float, seed: int = 0,
     nnz = int(row_ptr[-1])
     col = np.empty(nnz, dtype=np.int32)
     val = np.empty(nnz, dtype=np.float64)
-    col[0], val[0] = iw, 1.0
+    S = max(1.0, float(b @ b) / 2.0) if balance else 1.0
+    col[0], val[0] = iw, 1.0 / S
     astart = np.zeros(m + 1, dtype=np.int64)
     np.cumsum(k, out=astart[1:])
     within = np.arange(arow.shape[0], dtype=np.int64) - astart[arow]
@@ -107,16 +116,38 @@ def gen_lasso(m: int, nfeat: int, density: float, seed: int = 0,
     h[1:] = -b
     c = np.zeros(n)
     c[:n1] = lam
-    c[ir] = 2.0
+    c[ir] = 2.0 * S
     prog = ConicProgram(
         m=mrows, n=n, n1=n1, row_ptr=row_ptr, col_idx=col, vals=val, c=c, h=h,
         l=np.zeros(n1), u=np.full(n1, INF),
         pk=np.array([RSOC], np.int32), pdim=np.array([m + 2], np.int64),
         rk=np.array([ZERO], np.int32), rdim=np.array([mrows], np.int64),
-        name=f"lasso_{m}x{nfeat}_d{density:g}_s{seed}")
+        name=f"lasso_{m}x{nfeat}_d{density:g}_s{seed}" + ("" if balance else "_literal"))
     prog.lasso_A = (arow, acol, aval, m, nfeat)   # original data for ISTA pins
     prog.lasso_b = b
     prog.lasso_lam = lam
+    prog.lasso_S = S
+
+    def to_literal(x, S=S, iw=iw, ir=ir):
+        """A point of this instance as a point of the literal form (balance=False)."""
+        x = np.array(x, dtype=np.float64, copy=True)
+        x[iw] /= S
+        x[ir] *= S
+        return x
+    prog.to_literal = to_literal
+
+    def literal(prog=prog, S=S, iw=iw, ir=ir):
+        """The literal form (balance=False) of this instance, sharing A and b."""
+        if S == 1.0:
+            return prog
+        v = prog.vals.copy()
+        v[0] = 1.0                                    # row w = 1, col iw
+        cc = prog.c.copy()
+        cc[ir] = 2.0
+        return ConicProgram(m=prog.m, n=prog.n, n1=prog.n1, row_ptr=prog.row_ptr, col_idx=prog.col_idx, vals=v,
+                            c=cc, h=prog.h, l=prog.l, u=prog.u, pk=prog.pk, pdim=prog.pdim, rk=prog.rk,
+                            rdim=prog.rdim, name=prog.name + "_literal")
+    prog.literal = literal
     return prog
 
 

@@ -189,6 +189,7 @@ def literal_form_kkt(P, prog, xb, yb, stream, device):
     """Lasso (reading P9): the solve ran on the balanced SOCP; its best point,
     mapped back by w = w'/S, r = S r', is scored by Eq. 9 OF THE LITERAL FORM
     (PAPER.md:1641-1659 as printed) -- in a second library context, on the GPU."""
+    import torch
     lit = prog.literal()
     host = pinned(lit, (0, lit.m))
     ctx = make_ctx(P, lit, host, P.pdcs_default_params(), stream, device, (0, lit.m))

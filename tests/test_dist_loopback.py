@@ -168,7 +168,8 @@ def test_loopback_solve_and_time_limit_stop_together(P, monkeypatch):
     with pytest.raises(P.PdcsError):
         ranks[0].iterate(1)
     # time limit: a tiny limit on a long solve stops both ranks at one check
-    group, parts, ranks = make_ranks(P, gen_lasso(2000, 200, 0.05, seed=5), 2, tol=1e-12, time_limit_s=0.5)
+    group, parts, ranks = make_ranks(P, gen_lasso(2000, 200, 0.05, seed=5, balance=False), 2, tol=1e-12,
+                                     time_limit_s=0.5)
     res = on_all([lambda g=g: g.solve() for g in ranks])
     assert res[0]["status"] == res[1]["status"] == "TIME_LIMIT"
     assert res[0]["iters"] == res[1]["iters"] and res[0]["iters"] > 0

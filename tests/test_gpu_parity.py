@@ -133,8 +133,13 @@ def _shadow(P, prog, steps, seg=10):
         # decisions exact (k, total, trials, restarts, beta); eta/omega/W to STOL
         assert np.array_equal(sg["sc"][9:], so["sc"][9:]), (s, sg["sc"], so["sc"])
         assert sg["sc"][3] == so["sc"][3], (s, sg["sc"], so["sc"])
+        # near the optimum eta-bar = ||dz||^2 / (2 |<dy, K dx>|) is a ratio of
+        # differences of size e |z| (e = the best Eq. 9 error so far), so its
+        # rounding error grows like 1/e: the tolerance widens below e = 1e-5
+        # (measured on configs[0]: 4.9e-6 relative at e = 1e-7, 8.5e-2 at e = 2.4e-11)
+        stol = STOL * max(1.0, 1e-5 / max(st["sc"][8], 1e-12))
         for i in (0, 2, 4):
-            assert abs(sg["sc"][i] - so["sc"][i]) <= STOL * abs(so["sc"][i]), (s, i, sg["sc"], so["sc"])
+            assert abs(sg["sc"][i] - so["sc"][i]) <= stol * abs(so["sc"][i]), (s, i, stol, sg["sc"], so["sc"])
         worst = max(worst, rel(sg["x0"], so["x0"]), rel(sg["y0"], so["y0"]))
         if so["sc"][4] > 0:   # the average z = sum eta z / sum eta (Alg. 1 line 7)
             worst = max(worst, rel(sg["xsum"] / sg["sc"][4], so["xsum"] / so["sc"][4]),
@@ -152,6 +157,15 @@ def test_pdcs_parity_tiny_lasso_2000(P):
     assert worst <= TOL, worst
     free = _free_running(P, prog, 200)
     assert max(free) <= TOL, free
+
+
+def test_pdcs_parity_tiny_lasso_2000_literal_form(P):
+    """configs[0] in the literal form of PAPER.md:1641-1659 (balance=False,
+    reading P9): the trajectory that stalls far from the optimum, 2000 steps
+    segment by segment."""
+    prog = gen_lasso(100, 50, 1.0, seed=0, dense=True, balance=False)
+    worst = _shadow(P, prog, 2000)
+    assert worst <= TOL, worst
 
 
 @pytest.mark.parametrize("name,make,steps", [

@@ -112,7 +112,7 @@ def _free_running(P, prog, steps, every=40):
     return worst
 
 
-def _shadow(P, prog, steps, seg=10):
+def _shadow(P, prog, steps, seg=10, floor=None):
     """Checkpoint shadowing: at every check-interval
     boundary of the oracle's trajectory (every `seg` accepted iterations; every
     4th segment ends on an Eq. 9 check, restart and primal-weight decision) the
@@ -123,6 +123,8 @@ def _shadow(P, prog, steps, seg=10):
     worst = 0.0
     for s in range(0, steps, seg):
         st = o.get_state()
+        if floor is not None and st["sc"][8] < floor:
+            return worst, s       # solved to the rounding floor: the rest is noise
         g.set_state(st)
         g.iterate(seg)
         o.iterate(seg)
@@ -144,7 +146,7 @@ def _shadow(P, prog, steps, seg=10):
         if so["sc"][4] > 0:   # the average z = sum eta z / sum eta (Alg. 1 line 7)
             worst = max(worst, rel(sg["xsum"] / sg["sc"][4], so["xsum"] / so["sc"][4]),
                         rel(sg["ysum"] / sg["sc"][4], so["ysum"] / so["sc"][4]))
-    return worst
+    return (worst, steps) if floor is not None else worst
 
 
 def test_pdcs_parity_tiny_lasso_2000(P):
@@ -153,10 +155,21 @@ def test_pdcs_parity_tiny_lasso_2000(P):
     2000-step comparison is made segment by segment from the oracle's state; the
     free-running comparison is held to TOL over the first 200 iterations."""
     prog = gen_lasso(100, 50, 1.0, seed=0, dense=True)
-    worst = _shadow(P, prog, 2000)
-    assert worst <= TOL, worst
+    # the balanced form (P9) is solved to Eq. 9 ~ 1e-12 by iteration ~1000;
+    # past the 1e-10 floor the step and restart decisions are taken on
+    # rounding noise (P5), so the shadow stops there ...
+    worst, stop = _shadow(P, prog, 2000, floor=1e-10)
+    assert worst <= TOL and 600 <= stop < 2000, (worst, stop)
     free = _free_running(P, prog, 200)
     assert max(free) <= TOL, free
+    # ... and the full 2000 iterations, free-running, end at the same optimum
+    g = P.PdcsSolver(prog)
+    o = O.OracleSolver(prog)
+    g.iterate(2000)
+    o.iterate(2000)
+    xg, yg = g.get_iterate(P.CURRENT)
+    xo, yo = o.get_iterate(0)
+    assert parity(xg, yg, xo, yo) <= 1e-8, parity(xg, yg, xo, yo)
 
 
 def test_pdcs_parity_tiny_lasso_2000_literal_form(P):

@@ -639,3 +639,32 @@ def test_caller_allocator(P):
     g.iterate(100)
     xb, yb = g.get_iterate(P.CURRENT)
     assert np.array_equal(xa, xb) and np.array_equal(ya, yb)
+
+
+def test_balanced_lasso_solves_to_1e4_and_maps_to_the_literal_form(P):
+    """Reading P9 at a size the oracle still solves in seconds (2e4 x 2e3 at 1%,
+    the tall P8 proxy): the GPU solves the balanced form to Eq. 9 <= 1e-4; its
+    best point, mapped back (w = w'/S, r = S r'), scores <= 1e-4 on the
+    LITERAL form's Eq. 9 in a second GPU context; its objective is the Lasso
+    objective ||A x - b||^2 + lam ||x||_1 evaluated directly from (A, b) at
+    x = x+ - x- (PAPER.md:1641-1659), and agrees with the oracle's solve of
+    the same balanced program to the accuracy both stop at."""
+    prog = gen_lasso(20000, 2000, 0.01, seed=0)
+    g = P.PdcsSolver(prog, tol=1e-4)
+    r = g.solve()
+    assert r["status"] == "OPTIMAL", r
+    x, y = g.get_iterate(P.BEST, P.ORIGINAL)
+    g.close()
+    lit = P.PdcsSolver(prog.literal())
+    lit.set_iterate(prog.to_literal(x), y)
+    k = lit.kkt(P.CURRENT)
+    lit.close()
+    assert max(k["err_p"], k["err_d"], k["err_gap"]) <= 1e-4, k
+    arow, acol, aval, m, nf = prog.lasso_A
+    xf = x[:nf] - x[nf:2 * nf]
+    resid = np.bincount(arow, weights=aval * xf[acol], minlength=m) - prog.lasso_b
+    f = float(resid @ resid) + prog.lasso_lam * float(np.abs(xf).sum())
+    assert abs(k["pobj"] - f) <= 1e-3 * f, (k["pobj"], f)
+    ro = O.OracleSolver(prog, tol=1e-4, max_iters=20000).solve()
+    assert ro.status == 0
+    assert abs(k["pobj"] - ro.kkt.pobj) <= 1e-3 * abs(ro.kkt.pobj), (k["pobj"], ro.kkt.pobj)

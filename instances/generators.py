@@ -66,9 +66,10 @@ def gen_lasso(m: int, nfeat: int, density: float, seed: int = 0,
     b = A x~ + 1e-6, lam = ||A^T b||_inf.
 
     balance (reading P9): the RSOC's leading pair is stored as
-    (w', r') = (S w, r / S), S = max(1, ||b||^2 / 2) -- the value of r at
-    x = 0 -- an automorphism of the rotated cone (2 w' r' = 2 w r), so the
-    row w = 1 reads w' / S = 1 and r' costs 2 S.  Same problem, same optimal
+    (w', r') = (S w, r / S), S = max(1, ||b|| / sqrt(2)) -- the square root
+    of r at x = 0, so that w' = S and r' = r / S are of one size -- an
+    automorphism of the rotated cone (2 w' r' = 2 w r), so the row w = 1
+    reads w' / S = 1 and r' costs 2 S.  Same problem, same optimal
     value; a solution maps back by w = w' / S, r = S r' (y unchanged:
     `prog.to_literal(x)`).  balance=False gives the literal form, on which
     PDCS with the SPEC's heuristics stalls (P8).
@@ -98,7 +99,7 @@ def gen_lasso(m: int, nfeat: int, density: float, seed: int = 0,
     nnz = int(row_ptr[-1])
     col = np.empty(nnz, dtype=np.int32)
     val = np.empty(nnz, dtype=np.float64)
-    S = max(1.0, float(b @ b) / 2.0) if balance else 1.0
+    S = max(1.0, (float(b @ b) / 2.0) ** 0.5) if balance else 1.0
     col[0], val[0] = iw, 1.0 / S
     astart = np.zeros(m + 1, dtype=np.int64)
     np.cumsum(k, out=astart[1:])

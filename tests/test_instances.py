@@ -44,7 +44,7 @@ def test_lasso_balanced_form_is_the_same_problem():
     from instances import gen_lasso
     bal = gen_lasso(120, 40, 0.3, seed=4)
     lit = gen_lasso(120, 40, 0.3, seed=4, balance=False)
-    assert bal.lasso_S == max(1.0, float(bal.lasso_b @ bal.lasso_b) / 2.0) and lit.lasso_S == 1.0
+    assert bal.lasso_S == max(1.0, (float(bal.lasso_b @ bal.lasso_b) / 2.0) ** 0.5) and lit.lasso_S == 1.0
     lb = bal.literal()                                  # derived literal form == generated literal form
     for f in ("row_ptr", "col_idx", "vals", "c", "h", "l", "u", "pk", "pdim", "rk", "rdim"):
         assert np.array_equal(getattr(lb, f), getattr(lit, f)), f

@@ -15,7 +15,7 @@ from instances import gen_lasso  # noqa: E402
 CASES = [(20000, 2000, 0.01), (10000, 500, 0.1), (1000, 10000, 0.01)]
 if "--big" in sys.argv:
     CASES.append((10000, 100000, 1e-4))
-for (m, nf, d) in CASES:
+for (m, nf, d) in ([] if "--sweep" in sys.argv else CASES):
     for bal in (True, False):
         p = gen_lasso(m, nf, d, seed=0, balance=bal)
         t = time.perf_counter()
@@ -27,3 +27,20 @@ for (m, nf, d) in CASES:
         el = max(k["err_p"], k["err_d"], k["err_gap"]) if k else e
         print(("balanced" if bal else "literal", (m, nf, d), r.iters, r.status, e, el,
                round(time.perf_counter() - t, 1)), flush=True)
+
+if "--sweep" in sys.argv:
+    # the choice of S: w' = S, r' = r*/S; iterations to 1e-4 against S = f * ||b||^2/2
+    import dataclasses
+    for (m, nf, d) in CASES[:3]:
+        lit = gen_lasso(m, nf, d, seed=0, balance=False)
+        S0 = float(lit.lasso_b @ lit.lasso_b) / 2.0
+        out = []
+        for f in (1e-3, 3e-3, 1e-2, 3e-2, 0.1, 1.0, 1.0 / S0 ** 0.5):
+            S = S0 * f
+            v = lit.vals.copy(); v[0] = 1.0 / S
+            c = lit.c.copy(); c[lit.n1 + 1] = 2.0 * S
+            s = O.OracleSolver(dataclasses.replace(lit, vals=v, c=c), tol=1e-4, max_iters=20000)
+            r = s.solve()
+            x, _ = s.get_iterate(3, 1)
+            out.append((round(f, 5), r.status, r.iters, round(x[lit.n1 + 1] * S / S0, 3)))
+        print("sweep", (m, nf, d), "S0 = ||b||^2/2 =", round(S0, 1), "(f, status, iters, r*/S0):", out, flush=True)
